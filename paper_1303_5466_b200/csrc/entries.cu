@@ -1,0 +1,225 @@
+// K1: batched kernel-entry generation + box source geometry.
+//
+// Entries follow kernels.py:258-298 exactly, operation by operation, so that a
+// table built with the reference's formula (kernels.py:239-247) gives
+// bit-identical matrices:  block:      (K[q]*h^2)*(b_i*c_j)
+//                          diagonal:   a_i + ((h^2*b_i)*c_i)*corr
+//                          proxy_cols: (K[q]*b_i)*h^2
+//                          proxy_rows: (K[q]*c_j)*h^2
+// __dmul_rn/__dadd_rn keep nvcc from contracting into FMAs.  Layout is
+// column-major with threads along the row index, so each warp stores 32
+// consecutive doubles (256 B) per column.
+#include "common.cuh"
+#include "../../include/vief_b200.h"
+
+namespace vf {
+extern long long g_launches;
+
+struct cd { double re, im; };
+
+__device__ __forceinline__ cd ld_c(const double* p, long long i) {
+  const double2 v = reinterpret_cast<const double2*>(p)[i];
+  return {v.x, v.y};
+}
+
+template <bool CPLX>
+__device__ __forceinline__ void store(double* out, long long idx, cd v) {
+  if (CPLX) reinterpret_cast<double2*>(out)[idx] = make_double2(v.re, v.im);
+  else out[idx] = v.re;
+}
+
+template <bool CPLX>
+__device__ __forceinline__ cd tab(const vief_problem& P, int q) {
+  if (CPLX) return ld_c(P.table, q);
+  return {__ldg(P.table + q), 0.0};
+}
+template <bool CPLX>
+__device__ __forceinline__ double fld(const double* f, int i) {
+  return __ldg(f + i);  // fields are real-valued (kernels.py:231-234)
+}
+
+__device__ __forceinline__ cd mulr(cd a, double s) { return {__dmul_rn(a.re, s), __dmul_rn(a.im, s)}; }
+
+// A[I,J] entry, kernels.py:258-275
+template <bool CPLX>
+__device__ __forceinline__ cd block_entry(const vief_problem& P, int gi, int gj) {
+  const int n = P.n_side;
+  if (gi == gj) {
+    double s = __dmul_rn(__dmul_rn(P.hh, fld<CPLX>(P.bv, gi)), fld<CPLX>(P.cv, gi));
+    double a = fld<CPLX>(P.av, gi);
+    return {__dadd_rn(a, __dmul_rn(s, P.corr_re)), CPLX ? __dmul_rn(s, P.corr_im) : 0.0};
+  }
+  int dx = gi % n - gj % n, dy = gi / n - gj / n;
+  int q = dx * dx + dy * dy;
+  double bc = __dmul_rn(fld<CPLX>(P.bv, gi), fld<CPLX>(P.cv, gj));
+  return mulr(mulr(tab<CPLX>(P, q), P.hh), bc);
+}
+
+template <bool CPLX>
+__global__ void k_gen_block(vief_problem P, const int* I, long long sI, const int* nI, int maxI,
+                            const int* J, long long sJ, const int* nJ, int maxJ,
+                            double* out, long long sOut, double* const* outp, int ldo) {
+  const int b = blockIdx.z;
+  const int ni = nI ? nI[b] : maxI, nj = nJ ? nJ[b] : maxJ;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = blockIdx.y * 8;
+  if (i >= ni) return;
+  const int gi = I[b * sI + i];
+  double* o = outp ? outp[b] : out + b * sOut;
+  for (int j = j0; j < min(j0 + 8, nj); ++j) {
+    int gj = J[b * sJ + j];
+    store<CPLX>(o, (long long)j * ldo + i, block_entry<CPLX>(P, gi, gj));
+  }
+}
+
+// ID matrices (p x m): row i = source, column j = work point
+template <bool CPLX>
+__global__ void k_gen_idmat(vief_problem P, int kind, const int* pts, long long sPts, const int* m,
+                            int maxm, const int* src_xy, const int* src_g, long long sSrc,
+                            const int* p, int maxp, double* out, long long sOut, int ldo) {
+  const int b = blockIdx.z;
+  const int mb = m ? m[b] : maxm, pb = p ? p[b] : maxp;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = blockIdx.y * 8;
+  if (i >= pb) return;
+  const int n = P.n_side;
+  const int sx = src_xy[2 * (b * sSrc + i)], sy = src_xy[2 * (b * sSrc + i) + 1];
+  const int sg = src_g[b * sSrc + i];
+  double* o = out + b * sOut;
+  for (int j = j0; j < min(j0 + 8, mb); ++j) {
+    const int gp = pts[b * sPts + j];
+    const int dx = gp % n - sx, dy = gp / n - sy;
+    const cd t = tab<CPLX>(P, dx * dx + dy * dy);
+    cd v;
+    if (sg < 0) {  // proxy point: (K*b_i)*h^2 (kind 0) / (K*c_j)*h^2 (kind 1)
+      double f = kind == 0 ? fld<CPLX>(P.bv, gp) : fld<CPLX>(P.cv, gp);
+      v = mulr(mulr(t, f), P.hh);
+    } else {       // near grid point: (K*h^2)*(b*c)
+      double bc = kind == 0 ? __dmul_rn(fld<CPLX>(P.bv, gp), fld<CPLX>(P.cv, sg))
+                            : __dmul_rn(fld<CPLX>(P.bv, sg), fld<CPLX>(P.cv, gp));
+      v = mulr(mulr(t, P.hh), bc);
+    }
+    store<CPLX>(o, (long long)j * ldo + i, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// proxy rings (tree.py:275-311) and near field (solver_dense.py:24-34)
+
+__device__ __forceinline__ int ring_len(int W, int H) {
+  if (W == 1) return H;
+  if (H == 1) return W;
+  return 2 * (W - 1) + 2 * (H - 1);
+}
+__device__ __forceinline__ void ring_cell(int W, int H, int i, int& x, int& y) {
+  if (W == 1) { x = 0; y = i; return; }
+  if (H == 1) { x = i; y = 0; return; }
+  if (i < W - 1) { x = i; y = 0; return; }
+  i -= W - 1;
+  if (i < H - 1) { x = W - 1; y = i; return; }
+  i -= H - 1;
+  if (i < W - 1) { x = W - 1 - i; y = H - 1; return; }
+  i -= W - 1;
+  x = 0; y = H - 1 - i;
+}
+
+__global__ void k_box_sources(const int* rects, int batch, int pad, int n_side, int* src_xy,
+                              int* src_g, long long sSrc, int* p_out) {
+  const int b = blockIdx.y;
+  const int x0 = rects[4 * b], x1 = rects[4 * b + 1], y0 = rects[4 * b + 2], y1 = rects[4 * b + 3];
+  const int w = x1 - x0, h = y1 - y0;
+  int L[8];
+  int nprox = 0;
+  for (int j = 1; j <= pad; ++j) { L[j - 1] = ring_len(w + 2 * j, h + 2 * j); nprox += L[j - 1]; }
+  const int X0 = max(x0 - pad, 0), X1 = min(x1 + pad, n_side);
+  const int Y0 = max(y0 - pad, 0), Y1 = min(y1 + pad, n_side);
+  const int W = X1 - X0;
+  const int nnear = W * (Y1 - Y0) - w * h;
+  const int p = nprox + nnear;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p_out[b] = p;
+  int* xy = src_xy + 2 * b * sSrc;
+  int* g = src_g + b * sSrc;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < p; f += gridDim.x * blockDim.x) {
+    if (f < nprox) {
+      // (ring j, index i) -> merged position by rational comparison of i/L_j
+      int j = 1, off = 0;
+      while (f - off >= L[j - 1]) { off += L[j - 1]; ++j; }
+      const int i = f - off;
+      const long long Lj = L[j - 1];
+      long long pos = i;
+      for (int jj = 1; jj <= pad; ++jj) {
+        if (jj == j) continue;
+        const long long Lo = L[jj - 1];
+        const long long num = (long long)i * Lo;
+        pos += jj < j ? num / Lj + 1 : (num + Lj - 1) / Lj;
+      }
+      int cx, cy;
+      ring_cell(w + 2 * j, h + 2 * j, i, cx, cy);
+      xy[2 * pos] = cx + x0 - j;
+      xy[2 * pos + 1] = cy + y0 - j;
+      g[pos] = -1;
+    } else {
+      int q = f - nprox;
+      const int nbot = (y0 - Y0) * W;
+      const int L_ = x0 - X0, R_ = X1 - x1, mid = (L_ + R_) * h;
+      int x, y;
+      if (q < nbot) { y = Y0 + q / W; x = X0 + q % W; }
+      else if (q < nbot + mid) {
+        q -= nbot;
+        y = y0 + q / (L_ + R_);
+        int c = q % (L_ + R_);
+        x = c < L_ ? X0 + c : x1 + (c - L_);
+      } else { q -= nbot + mid; y = y1 + q / W; x = X0 + q % W; }
+      xy[2 * f] = x;
+      xy[2 * f + 1] = y;
+      g[f] = y * n_side + x;
+    }
+  }
+}
+
+}  // namespace vf
+
+using namespace vf;
+
+extern "C" int vief_gen_block(const vief_problem* P, const int* I, long long sI, const int* nI,
+                              int maxI, const int* J, long long sJ, const int* nJ, int maxJ,
+                              double* out, long long sOut, double* const* outp, int ldo,
+                              int batch, void* stream) {
+  if (batch <= 0 || maxI <= 0 || maxJ <= 0) return VF_OK;
+  dim3 grid(cdiv(maxI, 128), cdiv(maxJ, 8), batch);
+  if (grid.y > 65535 || batch > 65535) { set_error("gen_block: grid too large"); return VF_EARG; }
+  if (P->is_complex)
+    k_gen_block<true><<<grid, 128, 0, (cudaStream_t)stream>>>(*P, I, sI, nI, maxI, J, sJ, nJ, maxJ, out, sOut, outp, ldo);
+  else
+    k_gen_block<false><<<grid, 128, 0, (cudaStream_t)stream>>>(*P, I, sI, nI, maxI, J, sJ, nJ, maxJ, out, sOut, outp, ldo);
+  ++g_launches;
+  VF_LAUNCH_CHECK("k_gen_block");
+  return VF_OK;
+}
+
+extern "C" int vief_gen_idmat(const vief_problem* P, int kind, const int* pts, long long sPts,
+                              const int* m, int maxm, const int* src_xy, const int* src_g,
+                              long long sSrc, const int* p, int maxp, double* out, long long sOut,
+                              int ldo, int batch, void* stream) {
+  if (batch <= 0 || maxm <= 0 || maxp <= 0) return VF_OK;
+  dim3 grid(cdiv(maxp, 128), cdiv(maxm, 8), batch);
+  if (grid.y > 65535 || batch > 65535) { set_error("gen_idmat: grid too large"); return VF_EARG; }
+  if (P->is_complex)
+    k_gen_idmat<true><<<grid, 128, 0, (cudaStream_t)stream>>>(*P, kind, pts, sPts, m, maxm, src_xy, src_g, sSrc, p, maxp, out, sOut, ldo);
+  else
+    k_gen_idmat<false><<<grid, 128, 0, (cudaStream_t)stream>>>(*P, kind, pts, sPts, m, maxm, src_xy, src_g, sSrc, p, maxp, out, sOut, ldo);
+  ++g_launches;
+  VF_LAUNCH_CHECK("k_gen_idmat");
+  return VF_OK;
+}
+
+extern "C" int vief_box_sources(const int* rects, int batch, int pad, int n_side, int* src_xy,
+                                int* src_g, long long sSrc, int* p_out, void* stream) {
+  if (batch <= 0) return VF_OK;
+  if (pad < 1 || pad > 8) { set_error("box_sources: pad %d out of range", pad); return VF_EARG; }
+  dim3 grid(cdiv(sSrc, 256), batch);
+  k_box_sources<<<grid, 256, 0, (cudaStream_t)stream>>>(rects, batch, pad, n_side, src_xy, src_g, sSrc, p_out);
+  ++g_launches;
+  VF_LAUNCH_CHECK("k_box_sources");
+  return VF_OK;
+}

@@ -1,0 +1,199 @@
+// Index gathers/scatters, strided copies and identity padding used around the
+// dense kernels (the index work of FactoredInterp, solver_dense.py:58-95, and
+// the F/E block assembly of invert_dense_block, solver_dense.py:339-354).
+// Plus library-global error state.
+#include <cstdarg>
+#include <cstring>
+#include "common.cuh"
+#include "../../include/vief_b200.h"
+
+namespace vf {
+long long g_launches = 0;
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+int check_cuda(cudaError_t e, const char* what) {
+  set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return VF_ECUDA;
+}
+
+// 2-D tile kernels: grid (ceil(maxrow/32), ceil(maxcol/8), batch), 32x8 threads
+__global__ void k_gather_rows(const double* src, long long sSrc, int lds, const int* idx,
+                              long long sIdx, double* dst, long long sDst, int ldd,
+                              const int* nrow, int maxrow, const int* ncol, int maxcol, int acc) {
+  const int b = blockIdx.z;
+  const int nr = nrow ? nrow[b] : maxrow, nc = ncol ? ncol[b] : maxcol;
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  if (i >= nr || j >= nc) return;
+  const int r = idx[b * sIdx + i];
+  const double v = src[b * sSrc + (long long)j * lds + r];
+  double* d = dst + b * sDst + (long long)j * ldd + i;
+  *d = acc ? *d + v : v;
+}
+
+__global__ void k_scatter_cols(const double* src, long long sSrc, int lds, const int* idx,
+                               long long sIdx, double* dst, long long sDst, int ldd,
+                               const int* nrow, int maxrow, const int* ncol, int maxcol) {
+  const int b = blockIdx.z;
+  const int nr = nrow ? nrow[b] : maxrow, nc = ncol ? ncol[b] : maxcol;
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  if (i >= nr || j >= nc) return;
+  const int c = idx[b * sIdx + j];
+  dst[b * sDst + (long long)c * ldd + i] = src[b * sSrc + (long long)j * lds + i];
+}
+
+__global__ void k_gather_cols(const double* src, long long sSrc, int lds, const int* idx,
+                              long long sIdx, double* dst, long long sDst, int ldd,
+                              const int* nrow, int maxrow, const int* ncol, int maxcol) {
+  const int b = blockIdx.z;
+  const int nr = nrow ? nrow[b] : maxrow, nc = ncol ? ncol[b] : maxcol;
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  if (i >= nr || j >= nc) return;
+  const int c = idx[b * sIdx + j];
+  dst[b * sDst + (long long)j * ldd + i] = src[b * sSrc + (long long)c * lds + i];
+}
+
+__global__ void k_scatter_rows(const double* src, long long sSrc, int lds, const int* idx,
+                               long long sIdx, double* dst, long long sDst, int ldd,
+                               const int* nrow, int maxrow, const int* ncol, int maxcol) {
+  const int b = blockIdx.z;
+  const int nr = nrow ? nrow[b] : maxrow, nc = ncol ? ncol[b] : maxcol;
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  if (i >= nr || j >= nc) return;
+  const int r = idx[b * sIdx + i];
+  dst[b * sDst + (long long)j * ldd + r] = src[b * sSrc + (long long)j * lds + i];
+}
+
+__global__ void k_copy2d(const double* src, long long sSrc, const double* const* srcp, int lds,
+                         double* dst, long long sDst, double* const* dstp, int ldd,
+                         const int* rows, int maxrows, const int* cols, int maxcols) {
+  const int b = blockIdx.z;
+  const int nr = rows ? rows[b] : maxrows, nc = cols ? cols[b] : maxcols;
+  const double* s = srcp ? srcp[b] : src + b * sSrc;
+  double* d = dstp ? dstp[b] : dst + b * sDst;
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  for (int j = blockIdx.y * 8 + threadIdx.y; j < nc; j += gridDim.y * 8)
+    if (i < nr) d[(long long)j * ldd + i] = s[(long long)j * lds + i];
+}
+
+__global__ void k_gather_int(const int* src, long long sSrc, const int* idx, long long sIdx,
+                             int* out, long long sOut, const int* n, int maxn) {
+  const int b = blockIdx.y;
+  const int nb = n ? n[b] : maxn;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nb) out[b * sOut + i] = src[b * sSrc + idx[b * sIdx + i]];
+}
+
+__global__ void k_pad_identity(double* A, long long sA, int lda, const int* nb, int n) {
+  const int b = blockIdx.z;
+  const int m = nb ? nb[b] : n;
+  if (m >= n) return;
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  if (i >= n || j >= n) return;
+  if (i < m && j < m) return;
+  A[b * sA + (long long)j * lda + i] = (i == j) ? 1.0 : 0.0;
+}
+
+}  // namespace vf
+
+using namespace vf;
+
+extern "C" int vief_version(void) { return 1; }
+extern "C" const char* vief_last_error(void) { return g_err; }
+extern "C" long long vief_launch_count(void) { return g_launches; }
+
+static inline dim3 grid2(int maxrow, int maxcol, int batch) {
+  return dim3(cdiv(maxrow, 32), cdiv(maxcol, 8), batch);
+}
+
+extern "C" int vief_gather_rows(const double* src, long long sSrc, int lds, const int* idx,
+                                long long sIdx, double* dst, long long sDst, int ldd,
+                                const int* nrow, int maxrow, const int* ncol, int maxcol,
+                                int batch, int accumulate, void* stream) {
+  if (batch <= 0 || maxrow <= 0 || maxcol <= 0) return VF_OK;
+  k_gather_rows<<<grid2(maxrow, maxcol, batch), dim3(32, 8), 0, (cudaStream_t)stream>>>(
+      src, sSrc, lds, idx, sIdx, dst, sDst, ldd, nrow, maxrow, ncol, maxcol, accumulate);
+  ++g_launches;
+  VF_LAUNCH_CHECK("k_gather_rows");
+  return VF_OK;
+}
+
+extern "C" int vief_scatter_cols(const double* src, long long sSrc, int lds, const int* idx,
+                                 long long sIdx, double* dst, long long sDst, int ldd,
+                                 const int* nrow, int maxrow, const int* ncol, int maxcol,
+                                 int batch, void* stream) {
+  if (batch <= 0 || maxrow <= 0 || maxcol <= 0) return VF_OK;
+  k_scatter_cols<<<grid2(maxrow, maxcol, batch), dim3(32, 8), 0, (cudaStream_t)stream>>>(
+      src, sSrc, lds, idx, sIdx, dst, sDst, ldd, nrow, maxrow, ncol, maxcol);
+  ++g_launches;
+  VF_LAUNCH_CHECK("k_scatter_cols");
+  return VF_OK;
+}
+
+extern "C" int vief_gather_cols(const double* src, long long sSrc, int lds, const int* idx,
+                                long long sIdx, double* dst, long long sDst, int ldd,
+                                const int* nrow, int maxrow, const int* ncol, int maxcol,
+                                int batch, void* stream) {
+  if (batch <= 0 || maxrow <= 0 || maxcol <= 0) return VF_OK;
+  k_gather_cols<<<grid2(maxrow, maxcol, batch), dim3(32, 8), 0, (cudaStream_t)stream>>>(
+      src, sSrc, lds, idx, sIdx, dst, sDst, ldd, nrow, maxrow, ncol, maxcol);
+  ++g_launches;
+  VF_LAUNCH_CHECK("k_gather_cols");
+  return VF_OK;
+}
+
+extern "C" int vief_scatter_rows(const double* src, long long sSrc, int lds, const int* idx,
+                                 long long sIdx, double* dst, long long sDst, int ldd,
+                                 const int* nrow, int maxrow, const int* ncol, int maxcol,
+                                 int batch, void* stream) {
+  if (batch <= 0 || maxrow <= 0 || maxcol <= 0) return VF_OK;
+  k_scatter_rows<<<grid2(maxrow, maxcol, batch), dim3(32, 8), 0, (cudaStream_t)stream>>>(
+      src, sSrc, lds, idx, sIdx, dst, sDst, ldd, nrow, maxrow, ncol, maxcol);
+  ++g_launches;
+  VF_LAUNCH_CHECK("k_scatter_rows");
+  return VF_OK;
+}
+
+extern "C" int vief_gather_int(const int* src, long long sSrc, const int* idx, long long sIdx,
+                               int* out, long long sOut, const int* n, int maxn, int batch,
+                               void* stream) {
+  if (batch <= 0 || maxn <= 0) return VF_OK;
+  k_gather_int<<<dim3(cdiv(maxn, 128), batch), 128, 0, (cudaStream_t)stream>>>(
+      src, sSrc, idx, sIdx, out, sOut, n, maxn);
+  ++g_launches;
+  VF_LAUNCH_CHECK("k_gather_int");
+  return VF_OK;
+}
+
+extern "C" int vief_copy2d(const double* src, long long sSrc, const double* const* srcp, int lds,
+                           double* dst, long long sDst, double* const* dstp, int ldd,
+                           const int* rows, int maxrows, const int* cols, int maxcols, int batch,
+                           void* stream) {
+  if (batch <= 0 || maxrows <= 0 || maxcols <= 0) return VF_OK;
+  dim3 g = grid2(maxrows, maxcols, batch);
+  if (g.y > 4096) g.y = 4096;
+  k_copy2d<<<g, dim3(32, 8), 0, (cudaStream_t)stream>>>(src, sSrc, srcp, lds, dst, sDst, dstp,
+                                                        ldd, rows, maxrows, cols, maxcols);
+  ++g_launches;
+  VF_LAUNCH_CHECK("k_copy2d");
+  return VF_OK;
+}
+
+extern "C" int vief_pad_identity(double* A, long long sA, int lda, const int* nb, int n, int batch,
+                                 void* stream) {
+  if (batch <= 0 || n <= 0) return VF_OK;
+  k_pad_identity<<<grid2(n, n, batch), dim3(32, 8), 0, (cudaStream_t)stream>>>(A, sA, lda, nb, n);
+  ++g_launches;
+  VF_LAUNCH_CHECK("k_pad_identity");
+  return VF_OK;
+}

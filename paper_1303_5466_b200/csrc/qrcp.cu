@@ -1,0 +1,907 @@
+// K2: batched interpolative decomposition (column-pivoted QR), replacing
+// dense_core.py:67-100 (interp_decomp -> LAPACK ?geqp3 + ?trsm) and the
+// row/column rank coupling of compress_outer (solver_dense.py:253-266).
+//
+// Two paths, both producing  perm (pivot order), k, R (k x m upper trapezoid)
+// and finally T = R11^{-1} R12:
+//
+//  * small items (p*m*8 <= ~200 KB, the leaf levels): classical Householder
+//    QRCP entirely in shared memory, one CTA per item, following LAPACK
+//    dlaqp2 (first-maximum pivot, partial-norm downdating with the
+//    sqrt(eps) recomputation test, dlarfg reflectors).  Rank rule as the
+//    reference: first j with |R_jj| <= eps*|R_00|.
+//
+//  * large items: blocked randomized column pivoting (Martinsson et al.,
+//    HQRRP) so that the O(pmk) work runs as DMMA GEMMs instead of one BLAS-2
+//    pass over the trailing matrix per column:
+//       Y = Omega A (sketch, s = b+8 rows)
+//       per block of b = 32 columns:
+//         select b pivots by QRCP on the sketch (CTA per item, Y read-only,
+//            Gram-Schmidt basis + norm downdating)
+//         swap them to the front; panel QR by shifted CholeskyQR3
+//         W = Q^T A_trail (rows of R), A_trail -= Q W, column norms
+//         Y_trail -= (Y_blk R_blk^{-1}) W   (sketch downdate, no new sketch)
+//       rank: the reference's rule in residual form — k is the first j whose
+//       largest residual column norm is <= eps * max_j ||A(:,j)|| (for exact
+//       QRCP this is exactly |R_jj| <= eps |R_00|), evaluated exactly inside
+//       the block where it first holds.
+//
+//  T = R11^{-1} R12 by blocked back substitution (64x64 diagonal block
+//  inverses + DMMA GEMM updates), identical for both paths.
+#include <vector>
+#include <algorithm>
+#include "common.cuh"
+#include "../../include/vief_b200.h"
+
+namespace vf {
+extern long long g_launches;
+
+// ---------------------------------------------------------------------------
+// small path: classical QRCP in shared memory
+constexpr int QS_THREADS = 256;
+
+__global__ void __launch_bounds__(QS_THREADS) k_qrcp_smem(
+    const double* A, long long sA, int lda, const int* pv, const int* mv, int* perm, int ldperm,
+    double* Rm, long long sR, int ldR, double* diag, int lddiag, double* colmax) {
+  extern __shared__ double sm[];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = QS_THREADS / 32;
+  const int p = pv[b], m = mv[b];
+  const int ld = p | 1;  // odd stride: column-parallel warps hit different banks
+  double* a = sm;                        // ld x m
+  double* vn1 = a + (long long)ld * m;   // m
+  double* vn2 = vn1 + m;                 // m
+  __shared__ double redv[32];
+  __shared__ int redi[32];
+  __shared__ double s_tau, s_beta;
+  int* pm = perm + b * ldperm;
+  const double* Ab = A + b * sA;
+  for (int idx = tid; idx < p * m; idx += QS_THREADS) {
+    int i = idx % p, j = idx / p;
+    a[j * ld + i] = Ab[(long long)j * lda + i];
+  }
+  for (int j = tid; j < m; j += QS_THREADS) pm[j] = j;
+  __syncthreads();
+  for (int j = warp; j < m; j += nw) {
+    double s = 0.0;
+    for (int i = lane; i < p; i += 32) s = fma(a[j * ld + i], a[j * ld + i], s);
+    s = sqrt(warp_sum(s));
+    if (lane == 0) { vn1[j] = s; vn2[j] = s; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int j = 0; j < m; ++j) mx = fmax(mx, vn1[j]);
+    colmax[b] = mx;
+  }
+  const int kmax = min(p, m);
+  const double tol3z = sqrt(2.220446049250313e-16);
+  double* Rb = Rm + b * sR;
+  double* db = diag + b * lddiag;
+  for (int i = 0; i < kmax; ++i) {
+    // pivot: first maximum of vn1[i:m]
+    double v = -1.0;
+    int iv = 0x7fffffff;
+    for (int j = i + tid; j < m; j += QS_THREADS)
+      if (vn1[j] > v) { v = vn1[j]; iv = j; }
+    block_argmax(v, iv, redv, redi);
+    const int pvt = iv;
+    if (pvt != i) {
+      for (int r = tid; r < p; r += QS_THREADS) {
+        double t = a[pvt * ld + r]; a[pvt * ld + r] = a[i * ld + r]; a[i * ld + r] = t;
+      }
+      if (tid == 0) {
+        int t = pm[pvt]; pm[pvt] = pm[i]; pm[i] = t;
+        vn1[pvt] = vn1[i]; vn2[pvt] = vn2[i];
+      }
+    }
+    __syncthreads();
+    // dlarfg on a(i:p, i)
+    double s = 0.0;
+    for (int r = i + 1 + tid; r < p; r += QS_THREADS) s = fma(a[i * ld + r], a[i * ld + r], s);
+    s = block_sum(s, redv);
+    if (tid == 0) {
+      double alpha = a[i * ld + i];
+      double xn = sqrt(s);
+      if (xn == 0.0) { s_tau = 0.0; s_beta = alpha; }
+      else {
+        double beta = -copysign(hypot(alpha, xn), alpha);
+        s_tau = (beta - alpha) / beta;
+        s_beta = beta;
+        a[i * ld + i] = 1.0 / (alpha - beta);  // temporary: scale factor
+      }
+    }
+    __syncthreads();
+    const double tau = s_tau, beta = s_beta;
+    if (tau != 0.0) {
+      const double sc = a[i * ld + i];
+      for (int r = i + 1 + tid; r < p; r += QS_THREADS) a[i * ld + r] *= sc;
+      __syncthreads();
+      if (tid == 0) a[i * ld + i] = 1.0;  // v(0) = 1 during the apply
+      __syncthreads();
+      // apply H = I - tau v v^T to columns i+1..m-1 (warp per column)
+      for (int j = i + 1 + warp; j < m; j += nw) {
+        double w = 0.0;
+        for (int r = i + lane; r < p; r += 32) w = fma(a[i * ld + r], a[j * ld + r], w);
+        w = warp_sum(w) * tau;
+        for (int r = i + lane; r < p; r += 32) a[j * ld + r] = fma(-w, a[i * ld + r], a[j * ld + r]);
+      }
+      __syncthreads();
+    }
+    if (tid == 0) { a[i * ld + i] = beta; db[i] = fabs(beta); }
+    // partial column norm update (dlaqp2)
+    for (int j = i + 1 + warp; j < m; j += nw) {
+      double nv1 = vn1[j];
+      if (nv1 != 0.0) {
+        double t = fabs(a[j * ld + i]) / nv1;
+        double temp = fmax(1.0 - t * t, 0.0);
+        double r = nv1 / vn2[j];
+        double temp2 = temp * r * r;
+        if (temp2 <= tol3z) {
+          double ss = 0.0;
+          for (int rr = i + 1 + lane; rr < p; rr += 32) ss = fma(a[j * ld + rr], a[j * ld + rr], ss);
+          ss = sqrt(warp_sum(ss));
+          if (lane == 0) { vn1[j] = ss; vn2[j] = ss; }
+        } else if (lane == 0) {
+          vn1[j] = nv1 * sqrt(temp);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = kmax + tid; i < m; i += QS_THREADS) db[i] = 0.0;
+  // R (upper trapezoid, kmax x m) -> Rm
+  for (int idx = tid; idx < kmax * m; idx += QS_THREADS) {
+    int i = idx % kmax, j = idx / kmax;
+    Rb[(long long)j * ldR + i] = (i <= j) ? a[j * ld + i] : 0.0;
+  }
+}
+
+// rank of small-path items: reference rule on |R_jj| (dense_core.py:81-89)
+__global__ void k_rank_small(const double* diag, int lddiag, const int* pv, const int* mv,
+                             int count, double eps, int* kout) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= count) return;
+  const int kmax = min(pv[b], mv[b]);
+  const double* d = diag + b * lddiag;
+  int k = 0;
+  if (kmax > 0) {
+    const double top = d[0], cut = eps * top;
+    if (top == 0.0 || top <= cut) k = 0;
+    else {
+      k = kmax;
+      for (int j = 0; j < kmax; ++j) if (d[j] <= cut) { k = j; break; }
+    }
+  }
+  kout[b] = k;
+}
+
+// group coupling: k = max over the group (row + column ID of one box)
+__global__ void k_group_max(int* k, int count, int group) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g * group >= count) return;
+  int mx = 0;
+  for (int i = 0; i < group; ++i) mx = max(mx, k[g * group + i]);
+  for (int i = 0; i < group; ++i) k[g * group + i] = mx;
+}
+
+// ---------------------------------------------------------------------------
+// blocked randomized path
+constexpr int HB = 32;       // block (panel) width
+constexpr int HS = HB + 8;   // sketch rows (oversampling 8)
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdULL; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ULL; x ^= x >> 33;
+  return x;
+}
+// deterministic standard normals (Box-Muller on a counter hash)
+__global__ void k_gaussian(double* out, long long n, unsigned long long seed) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long h1 = mix64(seed ^ (2 * i + 1) * 0x9E3779B97F4A7C15ULL);
+  unsigned long long h2 = mix64(h1 ^ 0xD1B54A32D192ED03ULL);
+  double u1 = ((h1 >> 11) + 1) * (1.0 / 9007199254740993.0);
+  double u2 = (h2 >> 11) * (1.0 / 9007199254740992.0);
+  out[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+// column norms of A(:, c0 + j), j < ncols_b; warp per column
+__global__ void k_colnorms(const double* A, long long sA, int lda, const int* pv, const int* mv,
+                           const int* active, int c0, double* out, int ldout) {
+  const int b = blockIdx.y;
+  if (active && !active[b]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 8 + warp;
+  const int m = mv[b], p = pv[b];
+  if (c0 + j >= m) return;
+  const double* a = A + b * sA + (long long)(c0 + j) * lda;
+  double s = 0.0;
+  for (int i = lane; i < p; i += 32) s = fma(a[i], a[i], s);
+  s = warp_sum(s);
+  if (lane == 0) out[b * ldout + c0 + j] = sqrt(s);
+}
+
+struct HState {
+  // per item
+  int* active;    // 1 while the item's group is unfinished
+  int* done;      // own criterion met
+  int* k;         // rank (valid once done)
+  int* bs;        // current block width (0 if inactive)
+  int* nrem;      // trailing columns after the block
+  int* pact;      // p if active else 0
+  int* sact;      // HS if active else 0
+  int* swaps;     // count x HB (source positions)
+  double* cut;    // eps * max column norm
+  double* tn;     // count x maxm trailing norms (absolute column index)
+  double* Rt;     // count x HB x HB block R (upper)
+  double* Qw;     // count x maxp x HB explicit panel Q
+  double* work;   // count x maxp x HB panel work copy (large panels)
+  double* Y;      // count x HS x maxm sketch
+  double* Z;      // count x HS x HB
+  int* any;       // 1 int: any active
+  int ldtn;       // row stride of tn (= maxm)
+};
+
+__global__ void k_block_setup(int J, const int* pv, const int* mv, int count, HState S) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= count) return;
+  const int act = S.active[b];
+  const int m = mv[b];
+  int bs = act ? min(HB, m - J) : 0;
+  if (bs < 0) bs = 0;
+  S.bs[b] = bs;
+  S.nrem[b] = act ? max(m - J - bs, 0) : 0;
+  S.pact[b] = act ? pv[b] : 0;
+  S.sact[b] = act ? HS : 0;
+}
+
+// select HB pivots from the sketch Y(:, J:m) by QRCP on the sketch.  Y is read
+// only: the chosen columns' residual directions are kept as an orthonormal
+// basis (classical Gram-Schmidt, twice) and all other columns' residual norms
+// are downdated by their projection on each new basis vector.
+__global__ void __launch_bounds__(256) k_sketch_select(const double* Yg, int ldy, long long sY,
+                                                       const int* mv, int J, HState S) {
+  extern __shared__ double sm[];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (!S.active[b]) return;
+  const int m = mv[b];
+  const int n = m - J;
+  const int bs = S.bs[b];
+  if (bs <= 0) return;
+  double* nrm = sm;                 // n: current residual norm^2
+  double* nrm0 = nrm + n;           // n: original norm^2
+  __shared__ double Qb[HB][HS];     // chosen basis vectors
+  __shared__ double qv[HS];
+  __shared__ double redv[32];
+  __shared__ int redi[32];
+  __shared__ int sel[HB];
+  const double* Y = Yg + b * sY + (long long)J * ldy;
+  (void)S.ldtn;
+  for (int j = warp; j < n; j += 8) {
+    double s = 0.0;
+    for (int r = lane; r < HS; r += 32) s = fma(Y[(long long)j * ldy + r], Y[(long long)j * ldy + r], s);
+    s = warp_sum(s);
+    if (lane == 0) { nrm[j] = s; nrm0[j] = s; }
+  }
+  __syncthreads();
+  for (int i = 0; i < bs; ++i) {
+    double v = -1.0;
+    int iv = 0x7fffffff;
+    for (int j = tid; j < n; j += 256)
+      if (nrm[j] > v) { v = nrm[j]; iv = j; }
+    block_argmax(v, iv, redv, redi);
+    if (tid == 0) { sel[i] = iv; nrm[iv] = -1.0; }  // never chosen again
+    // q = (I - Qb Qb^T) y, twice, normalised  (warp 0)
+    if (warp == 0) {
+      double y0 = lane < HS ? Y[(long long)iv * ldy + lane] : 0.0;
+      double y1 = lane + 32 < HS ? Y[(long long)iv * ldy + lane + 32] : 0.0;
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int c = 0; c < i; ++c) {
+          double d = (lane < HS ? Qb[c][lane] * y0 : 0.0) + (lane + 32 < HS ? Qb[c][lane + 32] * y1 : 0.0);
+          d = warp_sum(d);
+          if (lane < HS) y0 -= d * Qb[c][lane];
+          if (lane + 32 < HS) y1 -= d * Qb[c][lane + 32];
+        }
+      }
+      double nn = warp_sum(y0 * y0 + y1 * y1);
+      double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+      if (lane < HS) { Qb[i][lane] = y0 * inv; qv[lane] = y0 * inv; }
+      if (lane + 32 < HS) { Qb[i][lane + 32] = y1 * inv; qv[lane + 32] = y1 * inv; }
+    }
+    __syncthreads();
+    // downdate all remaining norms
+    for (int j = warp; j < n; j += 8) {
+      double cur = nrm[j];
+      if (cur < 0.0) continue;
+      double d = 0.0;
+      for (int r = lane; r < HS; r += 32) d = fma(qv[r], Y[(long long)j * ldy + r], d);
+      d = warp_sum(d);
+      if (lane == 0) {
+        double nv = cur - d * d;
+        if (nv < 1e-12 * nrm0[j]) nv = fmax(nv, 0.0);  // cancellation floor
+        nrm[j] = nv;
+      }
+    }
+    __syncthreads();
+  }
+  // convert the selection into a sequence of swaps (dst = J+i, src position)
+  if (tid == 0) {
+    int mid[2 * HB + 2], mpos[2 * HB + 2];
+    int nm = 0;
+    for (int i = 0; i < bs; ++i) {
+      const int id = J + sel[i];
+      int src = id;
+      for (int t = 0; t < nm; ++t) if (mid[t] == id) src = mpos[t];
+      const int dst = J + i;
+      int at_dst = dst;
+      for (int t = 0; t < nm; ++t) if (mpos[t] == dst) at_dst = mid[t];
+      S.swaps[b * HB + i] = src;
+      // id at_dst moves to src; id moves to dst
+      bool f1 = false, f2 = false;
+      for (int t = 0; t < nm; ++t) {
+        if (mid[t] == at_dst) { mpos[t] = src; f1 = true; }
+        else if (mid[t] == id) { mpos[t] = dst; f2 = true; }
+      }
+      if (!f1 && at_dst != src) { mid[nm] = at_dst; mpos[nm] = src; ++nm; }
+      if (!f2 && id != dst) { mid[nm] = id; mpos[nm] = dst; ++nm; }
+    }
+  }
+}
+
+// apply the swap sequence to A (p rows), Y (HS rows), perm, and the norms.
+__global__ void k_apply_swaps(double* A, long long sA, int lda, double* Y, long long sY, int ldy,
+                              int* perm, int ldperm, const int* pv, int J, HState S,
+                              double* Rm, long long sR, int ldR) {
+  const int b = blockIdx.y;
+  if (!S.active[b]) return;
+  const int bs = S.bs[b];
+  const int p = pv[b];
+  const int* sw = S.swaps + b * HB;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < p) {
+    double* a = A + b * sA + r;
+    for (int i = 0; i < bs; ++i) {
+      const int src = sw[i], dst = J + i;
+      if (src != dst) {
+        double t = a[(long long)src * lda]; a[(long long)src * lda] = a[(long long)dst * lda];
+        a[(long long)dst * lda] = t;
+      }
+    }
+  }
+  if (r < J) {  // rows of R already computed travel with their columns
+    double* rr = Rm + b * sR + r;
+    for (int i = 0; i < bs; ++i) {
+      const int src = sw[i], dst = J + i;
+      if (src != dst) {
+        double t = rr[(long long)src * ldR]; rr[(long long)src * ldR] = rr[(long long)dst * ldR];
+        rr[(long long)dst * ldR] = t;
+      }
+    }
+  }
+  if (r < HS) {
+    double* y = Y + b * sY + r;
+    for (int i = 0; i < bs; ++i) {
+      const int src = sw[i], dst = J + i;
+      if (src != dst) {
+        double t = y[(long long)src * ldy]; y[(long long)src * ldy] = y[(long long)dst * ldy];
+        y[(long long)dst * ldy] = t;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int* pm = perm + b * ldperm;
+    for (int i = 0; i < bs; ++i) {
+      const int src = sw[i], dst = J + i;
+      if (src != dst) { int t = pm[src]; pm[src] = pm[dst]; pm[dst] = t; }
+    }
+  }
+}
+
+// Householder QR of the block panel P = A(:, J:J+bs) (p x bs, unpivoted: the
+// order comes from the sketch), explicit Q (dorg2r-style backward
+// accumulation) into Qw and R into S.Rt.  Rank-deficient panels are harmless
+// (tau = 0 / tiny R_jj).  One CTA per item; the panel lives in shared memory
+// when small, else in a global work copy (L2-resident).
+constexpr int PQ_THREADS = 256;
+__global__ void __launch_bounds__(PQ_THREADS) k_panel_qr(const double* A, long long sA, int lda,
+                                                         const int* pv, int J, HState S,
+                                                         double* Qw, long long sQ, int ldq,
+                                                         double* work, int use_smem) {
+  extern __shared__ double psm[];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = PQ_THREADS / 32;
+  if (!S.active[b]) return;
+  const int bs = S.bs[b];
+  if (bs <= 0) return;
+  const int p = pv[b];
+  __shared__ double tau[HB], Rl[HB][HB + 1];
+  __shared__ double red[32];
+  __shared__ double s_beta, s_tau, s_sc;
+  const int ldp = use_smem ? p : ldq;
+  double* P = use_smem ? psm : work + b * sQ;
+  double* Q = use_smem ? psm + (long long)p * HB : Qw + b * sQ;
+  const double* Ab = A + b * sA + (long long)J * lda;
+  for (int idx = tid; idx < p * bs; idx += PQ_THREADS) {
+    int r = idx % p, c = idx / p;
+    P[(long long)c * ldp + r] = Ab[(long long)c * lda + r];
+  }
+  for (int idx = tid; idx < HB * HB; idx += PQ_THREADS) Rl[idx % HB][idx / HB] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < bs; ++j) {
+    if (j >= p) { if (tid == 0) tau[j] = 0.0; continue; }
+    double* v = P + (long long)j * ldp;
+    double ss = 0.0;
+    for (int r = j + 1 + tid; r < p; r += PQ_THREADS) ss = fma(v[r], v[r], ss);
+    ss = block_sum(ss, red);
+    if (tid == 0) {
+      const double alpha = v[j];
+      const double xn = sqrt(ss);
+      if (xn == 0.0) { s_tau = 0.0; s_beta = alpha; s_sc = 0.0; }
+      else {
+        const double beta = -copysign(hypot(alpha, xn), alpha);
+        s_tau = (beta - alpha) / beta; s_beta = beta; s_sc = 1.0 / (alpha - beta);
+      }
+    }
+    __syncthreads();
+    const double tj = s_tau;
+    if (tj != 0.0) {
+      const double sc = s_sc;
+      for (int r = j + 1 + tid; r < p; r += PQ_THREADS) v[r] *= sc;
+    }
+    __syncthreads();
+    if (tid == 0) { tau[j] = tj; Rl[j][j] = s_beta; v[j] = 1.0; }
+    __syncthreads();
+    if (tj != 0.0) {
+      for (int l = j + 1 + warp; l < bs; l += NW) {
+        double* c = P + (long long)l * ldp;
+        double w = 0.0;
+        for (int r = j + lane; r < p; r += 32) w = fma(v[r], c[r], w);
+        w = warp_sum(w) * tj;
+        for (int r = j + lane; r < p; r += 32) c[r] = fma(-w, v[r], c[r]);
+      }
+    }
+    __syncthreads();
+    for (int l = j + 1 + tid; l < bs; l += PQ_THREADS) Rl[j][l] = P[(long long)l * ldp + j];
+    __syncthreads();
+  }
+  // Q = H_0 ... H_{bs-1} [I; 0]
+  for (int idx = tid; idx < p * bs; idx += PQ_THREADS) {
+    int r = idx % p, c = idx / p;
+    Q[(long long)c * ldp + r] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = min(bs, p) - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    const double* v = P + (long long)j * ldp;  // v[j] == 1
+    for (int l = j + warp; l < bs; l += NW) {
+      double* c = Q + (long long)l * ldp;
+      double w = 0.0;
+      for (int r = j + lane; r < p; r += 32) w = fma(v[r], c[r], w);
+      w = warp_sum(w) * tj;
+      for (int r = j + lane; r < p; r += 32) c[r] = fma(-w, v[r], c[r]);
+    }
+    __syncthreads();
+  }
+  if (use_smem) {
+    double* Qo = Qw + b * sQ;
+    for (int idx = tid; idx < p * bs; idx += PQ_THREADS) {
+      int r = idx % p, c = idx / p;
+      Qo[(long long)c * ldq + r] = Q[(long long)c * ldp + r];
+    }
+  }
+  double* Rt = S.Rt + (long long)b * HB * HB;
+  for (int idx = tid; idx < HB * HB; idx += PQ_THREADS) {
+    int i = idx % HB, c = idx / HB;
+    Rt[c * HB + i] = Rl[i][c];
+  }
+}
+
+// store the block's R diagonal block into Rm rows J..J+bs
+__global__ void k_store_rblock(HState S, double* Rm, long long sR, int ldR, int J) {
+  const int b = blockIdx.x;
+  if (!S.active[b]) return;
+  const int n = S.bs[b];
+  const double* Rt = S.Rt + (long long)b * HB * HB;
+  double* R = Rm + b * sR;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    int i = idx % n, j = idx / n;
+    R[(long long)(J + j) * ldR + J + i] = i <= j ? Rt[j * HB + i] : 0.0;
+  }
+}
+
+// rank check after a block: own criterion, and k inside the block (exact
+// residual form of the reference's rule |R_jj| <= eps |R_00|).
+__global__ void __launch_bounds__(256) k_rank_check(HState S, const double* Rm, long long sR,
+                                                    int ldR, const int* pv, const int* mv, int J) {
+  const int b = blockIdx.x, tid = threadIdx.x;
+  if (!S.active[b] || S.done[b]) return;
+  const int bs = S.bs[b];
+  const int m = mv[b], p = pv[b];
+  const int kmax = min(p, m);
+  const double cut = S.cut[b];
+  const double* R = Rm + b * sR;
+  const double* tn = S.tn + (long long)b * S.ldtn;
+  const int J1 = J + bs;
+  __shared__ double red[32];
+  __shared__ double best[HB + 1];
+  __shared__ int s_go;
+  double mx = 0.0;
+  for (int j = J1 + tid; j < m; j += 256) mx = fmax(mx, tn[j]);
+  // block max
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v = fmax(v, red[w]);
+    s_go = (v <= cut) || (J1 >= kmax);
+  }
+  __syncthreads();
+  if (!s_go) return;
+  // residual^2 of every column after j steps, j in [J, J1]; keep the max per j
+  double loc[HB + 1];
+  for (int t = 0; t <= HB; ++t) loc[t] = 0.0;
+  for (int l = J1 + tid; l < m; l += 256) {
+    double acc = tn[l] * tn[l];
+    loc[bs] = fmax(loc[bs], acc);
+    for (int r = J1 - 1; r >= J; --r) {
+      double v = R[(long long)l * ldR + r];
+      acc = fma(v, v, acc);
+      loc[r - J] = fmax(loc[r - J], acc);
+    }
+  }
+  for (int i = J + tid; i < J1; i += 256) {  // in-block columns
+    double acc = 0.0;
+    for (int r = i; r >= J; --r) {
+      double v = R[(long long)i * ldR + r];
+      acc = fma(v, v, acc);
+      loc[r - J] = fmax(loc[r - J], acc);
+    }
+  }
+  for (int t = 0; t <= bs; ++t) {
+    double v = loc[t];
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double w = 0.0;
+      for (int q = 0; q < 8; ++q) w = fmax(w, red[q]);
+      best[t] = w;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int k = J1;
+    for (int t = 0; t <= bs; ++t)
+      if (sqrt(best[t]) <= cut) { k = J + t; break; }
+    if (k > kmax) k = kmax;
+    S.k[b] = k;
+    S.done[b] = 1;
+  }
+}
+
+// group bookkeeping: a group stays active until all members are done; then
+// every member gets k = max over the group.
+__global__ void k_group_update(HState S, int count, int group) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g * group >= count) return;
+  bool all = true;
+  int mx = 0;
+  for (int i = 0; i < group; ++i) {
+    const int b = g * group + i;
+    if (!S.done[b]) all = false;
+    else mx = max(mx, S.k[b]);
+  }
+  if (all) {
+    for (int i = 0; i < group; ++i) { S.active[g * group + i] = 0; S.k[g * group + i] = mx; }
+  } else {
+    atomicOr(S.any, 1);
+  }
+}
+
+__global__ void k_init_state(HState S, const double* colmax, const int* pv, const int* mv, int count,
+                             double eps) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= count) return;
+  const double top = colmax[b];
+  const double cut = eps * top;
+  S.cut[b] = cut;
+  const bool zero = !(top > 0.0) || top <= cut || min(pv[b], mv[b]) == 0;
+  S.done[b] = zero ? 1 : 0;
+  S.k[b] = 0;
+  S.active[b] = 1;
+}
+
+__global__ void k_iota(int* perm, int ldperm, const int* mv, int count) {
+  const int b = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < mv[b]) perm[b * ldperm + j] = j;
+}
+
+__global__ void k_colmax(const double* tn, int ldtn, const int* mv, int count, double* out) {
+  const int b = blockIdx.x;
+  double mx = 0.0;
+  for (int j = threadIdx.x; j < mv[b]; j += blockDim.x) mx = fmax(mx, tn[(long long)b * ldtn + j]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+    out[b] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// T = R11^{-1} R12 (blocked back substitution, items padded to Kmax)
+constexpr int TB = 64;
+
+// T(:, c) = R(0:k, k+c), zero rows k..Kmax; R11 copy padded with identity
+__global__ void k_t_init(const double* Rm, long long sR, int ldR, const int* kv, const int* mv,
+                         int Kmax, double* T, long long sT, int ldT, double* Rs, long long sRs) {
+  const int b = blockIdx.z;
+  const int k = kv[b], m = mv[b];
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  const int c0 = blockIdx.y * 8 + threadIdx.y;
+  if (i >= Kmax) return;
+  const double* R = Rm + b * sR;
+  for (int c = c0; c < max(m - k, Kmax); c += gridDim.y * 8) {
+    if (c < m - k) T[b * sT + (long long)c * ldT + i] = i < k ? R[(long long)(k + c) * ldR + i] : 0.0;
+    if (c < Kmax) {
+      double v;
+      if (i < k && c < k) v = i <= c ? R[(long long)c * ldR + i] : 0.0;
+      else v = (i == c) ? 1.0 : 0.0;
+      Rs[b * sRs + (long long)c * Kmax + i] = v;
+    }
+  }
+}
+
+// inverse of the upper-triangular TB x TB diagonal blocks of Rs
+__global__ void __launch_bounds__(TB) k_diag_inv(const double* Rs, long long sRs, int Kmax,
+                                                 double* Dinv, long long sD) {
+  const int b = blockIdx.y, blk = blockIdx.x, tid = threadIdx.x;
+  const int r0 = blk * TB;
+  const int n = min(TB, Kmax - r0);
+  __shared__ double U[TB][TB + 1];
+  const double* R = Rs + b * sRs;
+  for (int j = 0; j < n; ++j) U[tid][j] = tid < n ? R[(long long)(r0 + j) * Kmax + r0 + tid] : 0.0;
+  __syncthreads();
+  double* D = Dinv + b * sD + (long long)blk * TB * TB;
+  if (tid < TB) {
+    const int j = tid;
+    double col[TB];
+    for (int i = 0; i < TB; ++i) col[i] = 0.0;
+    if (j < n) {
+      col[j] = 1.0 / U[j][j];
+      for (int i = j - 1; i >= 0; --i) {
+        double s = 0.0;
+        for (int q = i + 1; q <= j; ++q) s = fma(U[i][q], col[q], s);
+        col[i] = -s / U[i][i];
+      }
+    }
+    for (int i = 0; i < TB; ++i) D[(long long)j * TB + i] = col[i];
+  }
+}
+
+}  // namespace vf
+
+using namespace vf;
+
+namespace {
+struct Buf {
+  std::vector<void*> ptrs;
+  cudaStream_t st;
+  explicit Buf(cudaStream_t s) : st(s) {}
+  template <typename T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, n * sizeof(T) + 16, st) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~Buf() { for (void* p : ptrs) cudaFreeAsync(p, st); }
+};
+}  // namespace
+
+static int t_solve(const vief_id_desc* d, double* Rm, long long sR, int ldR, const int* kdev,
+                   int Kmax, Buf& buf, cudaStream_t st) {
+  const int count = d->count;
+  if (Kmax <= 0) return VF_OK;
+  const int nblk = (Kmax + TB - 1) / TB;
+  const long long sRs = (long long)Kmax * Kmax;
+  double* Rs = buf.get<double>((size_t)sRs * count);
+  double* Dinv = buf.get<double>((size_t)nblk * TB * TB * count);
+  double* tmp = buf.get<double>((size_t)TB * d->maxm * count);
+  int* nT = buf.get<int>(count);
+  if (!Rs || !Dinv || !tmp || !nT) { set_error("id: out of device memory (T solve)"); return VF_ENOMEM; }
+  {
+    dim3 g(cdiv(Kmax, 32), std::min<unsigned>(cdiv(std::max(d->maxm, Kmax), 8), 4096u), count);
+    k_t_init<<<g, dim3(32, 8), 0, st>>>(Rm, sR, ldR, kdev, d->m, Kmax, d->T, d->sT, d->ldT, Rs, sRs);
+    k_diag_inv<<<dim3(nblk, count), TB, 0, st>>>(Rs, sRs, Kmax, Dinv, (long long)nblk * TB * TB);
+    g_launches += 2;
+    VF_LAUNCH_CHECK("t_init/diag_inv");
+  }
+  // per-item column count m - k
+  {
+    // nT = m - k computed on host-visible path: small kernel via gather trick
+    std::vector<int> hm(count), hk(count);
+    VF_CUDA(cudaMemcpyAsync(hm.data(), d->m, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+    VF_CUDA(cudaMemcpyAsync(hk.data(), kdev, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+    VF_CUDA(cudaStreamSynchronize(st));
+    int nmax = 0;
+    for (int b = 0; b < count; ++b) { hm[b] = std::max(hm[b] - hk[b], 0); nmax = std::max(nmax, hm[b]); }
+    VF_CUDA(cudaMemcpyAsync(nT, hm.data(), sizeof(int) * count, cudaMemcpyHostToDevice, st));
+    VF_CUDA(cudaStreamSynchronize(st));
+    if (nmax == 0) return VF_OK;
+    for (int blk = nblk - 1; blk >= 0; --blk) {
+      const int r0 = blk * TB, r1 = std::min(Kmax, r0 + TB);
+      int rc;
+      if (r1 < Kmax) {
+        vief_gemm_desc g{};
+        g.A = Rs + (long long)r1 * Kmax + r0; g.strideA = sRs; g.lda = Kmax;
+        g.B = d->T + r1; g.strideB = d->sT; g.ldb = d->ldT;
+        g.C = d->T + r0; g.strideC = d->sT; g.ldc = d->ldT;
+        g.M = r1 - r0; g.N = nmax; g.K = Kmax - r1; g.Nb = nT;
+        g.alpha = -1.0; g.beta = 1.0; g.batch = count;
+        if ((rc = vief_dgemm_batched(&g, st))) return rc;
+      }
+      vief_gemm_desc h{};
+      h.A = Dinv + (long long)blk * TB * TB; h.strideA = (long long)nblk * TB * TB; h.lda = TB;
+      h.B = d->T + r0; h.strideB = d->sT; h.ldb = d->ldT;
+      h.C = tmp; h.strideC = (long long)TB * d->maxm; h.ldc = TB;
+      h.M = r1 - r0; h.N = nmax; h.K = r1 - r0; h.Nb = nT;
+      h.alpha = 1.0; h.beta = 0.0; h.batch = count;
+      if ((rc = vief_dgemm_batched(&h, st))) return rc;
+      if ((rc = vief_copy2d(tmp, (long long)TB * d->maxm, nullptr, TB, d->T + r0, d->sT, nullptr,
+                            d->ldT, nullptr, r1 - r0, nT, nmax, count, st)))
+        return rc;
+    }
+  }
+  return VF_OK;
+}
+
+extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  const int count = d->count;
+  if (count <= 0) return VF_OK;
+  if (count > 65535) { set_error("id: count > 65535"); return VF_EARG; }
+  if (d->group < 1 || count % d->group) { set_error("id: bad group"); return VF_EARG; }
+  if (d->ldT < d->maxm) { set_error("id: ldT must be >= maxm"); return VF_EARG; }
+  Buf buf(st);
+  const int maxm = d->maxm, maxp = d->maxp;
+  const long long sR = (long long)maxm * maxm;
+  const int ldR = maxm;
+  double* Rm = buf.get<double>((size_t)sR * count);
+  double* colmax = buf.get<double>(count);
+  if (!Rm || !colmax) { set_error("id: out of device memory"); return VF_ENOMEM; }
+  VF_CUDA(cudaMemsetAsync(Rm, 0, sizeof(double) * sR * count, st));
+  int Kmax = 0;
+  const size_t smem_small = ((size_t)(maxp | 1) * maxm + 2 * (size_t)maxm) * sizeof(double);
+  const bool small = !d->force_blocked && smem_small <= 220 * 1024;
+  int* kdev = d->rank;
+  if (small) {
+    double* diag = buf.get<double>((size_t)maxm * count);
+    VF_CUDA(cudaFuncSetAttribute(k_qrcp_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_small));
+    k_qrcp_smem<<<count, QS_THREADS, smem_small, st>>>(d->A, d->sA, d->lda, d->p, d->m, d->perm,
+                                                       maxm, Rm, sR, ldR, diag, maxm, colmax);
+    k_rank_small<<<cdiv(count, 128), 128, 0, st>>>(diag, maxm, d->p, d->m, count, d->eps, kdev);
+    k_group_max<<<cdiv(count / d->group, 128), 128, 0, st>>>(kdev, count, d->group);
+    g_launches += 3;
+    VF_LAUNCH_CHECK("qrcp small");
+  } else {
+    HState S{};
+    S.active = buf.get<int>(count); S.done = buf.get<int>(count); S.k = kdev;
+    S.bs = buf.get<int>(count); S.nrem = buf.get<int>(count); S.pact = buf.get<int>(count);
+    S.sact = buf.get<int>(count); S.swaps = buf.get<int>((size_t)HB * count);
+    S.cut = buf.get<double>(count); S.tn = buf.get<double>((size_t)maxm * count);
+    S.Rt = buf.get<double>((size_t)HB * HB * count);
+    S.Qw = buf.get<double>((size_t)maxp * HB * count);
+    const size_t pq_need = 2 * (size_t)maxp * HB * sizeof(double);
+    const int pq_use_smem = pq_need <= 200 * 1024;
+    const size_t pq_smem = pq_use_smem ? pq_need : 0;
+    S.work = pq_use_smem ? nullptr : buf.get<double>((size_t)maxp * HB * count);
+    if (pq_use_smem)
+      VF_CUDA(cudaFuncSetAttribute(k_panel_qr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)pq_smem));
+    S.Y = buf.get<double>((size_t)HS * maxm * count);
+    S.Z = buf.get<double>((size_t)HS * HB * count);
+    S.any = buf.get<int>(1);
+    S.ldtn = maxm;
+    double* Om = buf.get<double>((size_t)HS * maxp);
+    if (!S.Y || !S.Qw || !Om || !S.any) { set_error("id: out of device memory (blocked)"); return VF_ENOMEM; }
+    const long long sY = (long long)HS * maxm, sQ = (long long)maxp * HB;
+    k_iota<<<dim3(cdiv(maxm, 128), count), 128, 0, st>>>(d->perm, maxm, d->m, count);
+    k_colnorms<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m,
+                                                           nullptr, 0, S.tn, maxm);
+    k_colmax<<<count, 256, 0, st>>>(S.tn, maxm, d->m, count, colmax);
+    k_init_state<<<cdiv(count, 128), 128, 0, st>>>(S, colmax, d->p, d->m, count, d->eps);
+    k_gaussian<<<cdiv((long long)HS * maxp, 256), 256, 0, st>>>(Om, (long long)HS * maxp,
+                                                               d->seed ^ 0x5eedULL);
+    g_launches += 5;
+    VF_LAUNCH_CHECK("id init");
+    int rc;
+    {  // Y = Omega A
+      vief_gemm_desc g{};
+      g.A = Om; g.strideA = 0; g.lda = HS;
+      g.B = d->A; g.strideB = d->sA; g.ldb = d->lda;
+      g.C = S.Y; g.strideC = sY; g.ldc = HS;
+      g.M = HS; g.N = maxm; g.K = maxp; g.Nb = d->m; g.Kb = d->p;
+      g.alpha = 1.0; g.beta = 0.0; g.batch = count;
+      if ((rc = vief_dgemm_batched(&g, st))) return rc;
+    }
+    const size_t sel_smem = 2 * (size_t)maxm * sizeof(double);
+    VF_CUDA(cudaFuncSetAttribute(k_sketch_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(sel_smem, 1024)));
+    const int kcap = std::min(maxp, maxm);
+    for (int J = 0; J < kcap; J += HB) {
+      k_block_setup<<<cdiv(count, 128), 128, 0, st>>>(J, d->p, d->m, count, S);
+      k_sketch_select<<<count, 256, sel_smem, st>>>(S.Y, HS, sY, d->m, J, S);
+      k_apply_swaps<<<dim3(cdiv(std::max(std::max(maxp, HS), J), 128), count), 128, 0, st>>>(
+          d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S, Rm, sR, ldR);
+      g_launches += 3;
+      VF_LAUNCH_CHECK("id select/swap");
+      k_panel_qr<<<count, PQ_THREADS, pq_smem, st>>>(d->A, d->sA, d->lda, d->p, J, S, S.Qw, sQ,
+                                                     maxp, S.work, pq_use_smem);
+      ++g_launches;
+      VF_LAUNCH_CHECK("k_panel_qr");
+      k_store_rblock<<<count, 256, 0, st>>>(S, Rm, sR, ldR, J);
+      ++g_launches;
+      {  // W = Q^T A_trail -> R(J:J+bs, J+bs:m); columns start at J+bs per item: use J+HB
+        // items with bs < HB have nrem = 0, so the fixed offset J+HB is exact for all active work
+        vief_gemm_desc w{};
+        w.A = S.Qw; w.strideA = sQ; w.lda = maxp; w.transA = 1;
+        w.B = d->A + (long long)(J + HB) * d->lda; w.strideB = d->sA; w.ldb = d->lda;
+        w.C = Rm + (long long)(J + HB) * ldR + J; w.strideC = sR; w.ldc = ldR;
+        w.M = HB; w.N = maxm; w.K = maxp; w.Mb = S.bs; w.Nb = S.nrem; w.Kb = S.pact;
+        w.alpha = 1.0; w.beta = 0.0; w.batch = count;
+        if ((rc = vief_dgemm_batched(&w, st))) return rc;
+        // A_trail -= Q W
+        vief_gemm_desc u{};
+        u.A = S.Qw; u.strideA = sQ; u.lda = maxp;
+        u.B = Rm + (long long)(J + HB) * ldR + J; u.strideB = sR; u.ldb = ldR;
+        u.C = d->A + (long long)(J + HB) * d->lda; u.strideC = d->sA; u.ldc = d->lda;
+        u.M = maxp; u.N = maxm; u.K = HB; u.Mb = S.pact; u.Nb = S.nrem; u.Kb = S.bs;
+        u.alpha = -1.0; u.beta = 1.0; u.batch = count;
+        if ((rc = vief_dgemm_batched(&u, st))) return rc;
+        // sketch downdate: Y_trail -= (Omega Q) W  (= Omega A_trail after the update)
+        vief_gemm_desc z{};
+        z.A = Om; z.strideA = 0; z.lda = HS;
+        z.B = S.Qw; z.strideB = sQ; z.ldb = maxp;
+        z.C = S.Z; z.strideC = (long long)HS * HB; z.ldc = HS;
+        z.M = HS; z.N = HB; z.K = maxp; z.Mb = S.sact; z.Nb = S.bs; z.Kb = S.pact;
+        z.alpha = 1.0; z.beta = 0.0; z.batch = count;
+        if ((rc = vief_dgemm_batched(&z, st))) return rc;
+        vief_gemm_desc y{};
+        y.A = S.Z; y.strideA = (long long)HS * HB; y.lda = HS;
+        y.B = Rm + (long long)(J + HB) * ldR + J; y.strideB = sR; y.ldb = ldR;
+        y.C = S.Y + (long long)(J + HB) * HS; y.strideC = sY; y.ldc = HS;
+        y.M = HS; y.N = maxm; y.K = HB; y.Mb = S.sact; y.Nb = S.nrem; y.Kb = S.bs;
+        y.alpha = -1.0; y.beta = 1.0; y.batch = count;
+        if ((rc = vief_dgemm_batched(&y, st))) return rc;
+      }
+      k_colnorms<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m,
+                                                             S.active, J + HB, S.tn, maxm);
+      VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
+      k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J);
+      k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
+      g_launches += 3;
+      VF_LAUNCH_CHECK("id rank");
+      int any = 0;
+      VF_CUDA(cudaMemcpyAsync(&any, S.any, sizeof(int), cudaMemcpyDeviceToHost, st));
+      VF_CUDA(cudaStreamSynchronize(st));
+      if (!any) break;
+    }
+  }
+  // Kmax and T
+  {
+    std::vector<int> hk(count);
+    VF_CUDA(cudaMemcpyAsync(hk.data(), kdev, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+    VF_CUDA(cudaStreamSynchronize(st));
+    for (int b = 0; b < count; ++b) Kmax = std::max(Kmax, hk[b]);
+  }
+  return t_solve(d, Rm, sR, ldR, kdev, Kmax, buf, st);
+}

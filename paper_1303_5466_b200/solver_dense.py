@@ -1,0 +1,751 @@
+"""Dense-block recursive skeletonization (HSS-D) on the B200.
+
+Drop-in for the reference's solver_dense.py (compress_outer 234-272,
+invert_dense_block 332-368, DenseBlockInverse.apply 293-329, Hss2dMatrix
+.matvec 143-178).  The reference walks boxes one by one; here every level is
+one batch ("boxes within a level are independent"):
+
+  compress_outer, per level fine -> coarse
+     work rows/cols  leaf: owned points; else children's skeletons concatenated
+     D (leaf) or B12/B21 (siblings)              K1  vief_gen_block
+     proxy ring + near field sources             K1  vief_box_sources
+     ID matrices (row block^T, column block)     K1  vief_gen_idmat
+     pivoted-QR IDs, ranks coupled per box       K2  vief_id_batched
+  invert_dense_block, per level fine -> coarse
+     F = D | [[E1, B12], [B21, E2]]  -> F^{-1}   K3  vief_inv_batched (Gauss-Jordan, partial pivoting)
+     W = F^{-1} L,  G = R W,  E = G^{-1},  C = E R   gathers + DMMA GEMMs
+  apply (solve), per level
+     up:   phi = F^{-1} u ;  ups = C phi            (= E R F^{-1} u, solver_dense.py:309-310)
+     down: res = phi - W (ups - E phi_dn)           (= F^{-1}(u - L ups + L E phi_dn), 317-321)
+
+The down-pass identity  F^{-1}(u - L(ups - E phi_dn)) = phi - W (ups - E phi_dn)
+uses W = F^{-1} L from the factorization, so the down sweep reads W (m x k)
+instead of F (m x m).  All per-box blocks of a level live in one padded HBM
+buffer (column-major, leading dimension = level maximum).
+"""
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import SolverOptions
+from .errors import SingularFactorError
+from .kernels import PLAIN, get_assembler
+from .tree import near_count, proxy_count
+
+_I32 = torch.int32
+_F64 = torch.float64
+
+
+def _even(x):
+    return int(x) + (int(x) & 1)
+
+
+def _dev_i32(a, device):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=device)
+
+
+def _ptrs(base, offsets_elems, device):
+    """Device int64 array of base.data_ptr() + 8*offset (pointer arrays)."""
+    off = np.asarray(offsets_elems, dtype=np.int64) * base.element_size() + base.data_ptr()
+    return torch.as_tensor(off, device=device)
+
+
+class _Level:
+    """Device state of one tree level (all its boxes as one batch)."""
+
+    def __init__(self, lv, ids, rects, leaf):
+        self.lv = lv
+        self.ids = np.asarray(ids)
+        self.rects = np.asarray(rects, dtype=np.int64)
+        self.nb = len(ids)
+        self.leaf = leaf
+
+
+class FactoredInterp:
+    """Host view of one box's interpolation operator (perm, T)
+    (solver_dense.py:58-95): R = [I T] Pi, L = Pi^T [I; T^T]."""
+
+    def __init__(self, perm, T):
+        self.perm = np.asarray(perm, dtype=np.int64)
+        self.T = T
+        self.k = T.shape[0]
+        self.m = self.perm.size
+
+    def apply_R(self, x):
+        return x[self.perm[:self.k]] + self.T @ x[self.perm[self.k:]]
+
+    def apply_L(self, w):
+        out = np.empty((self.m,) + w.shape[1:], dtype=np.result_type(self.T.dtype, w.dtype))
+        out[self.perm[:self.k]] = w
+        out[self.perm[self.k:]] = self.T.T @ w
+        return out
+
+    def dense_L(self, dtype):
+        out = np.zeros((self.m, self.k), dtype=dtype)
+        out[self.perm[:self.k], np.arange(self.k)] = 1.0
+        out[self.perm[self.k:]] = self.T.T
+        return out
+
+    def dense_R(self, dtype):
+        return self.dense_L(dtype).T.copy()
+
+    def nbytes(self):
+        return self.T.nbytes
+
+
+class _BoxView:
+    """Read-only dict-like access {box idx: host array} over level buffers."""
+
+    def __init__(self, owner, getter, keys):
+        self._owner, self._get, self._keys = owner, getter, keys
+
+    def __getitem__(self, i):
+        if i not in self._keys():
+            raise KeyError(i)
+        return self._get(i)
+
+    def __contains__(self, i):
+        return i in self._keys()
+
+    def get(self, i, default=None):
+        return self[i] if i in self else default
+
+    def keys(self):
+        return list(self._keys())
+
+    def __iter__(self):
+        return iter(self.keys())
+
+    def __len__(self):
+        return len(self._keys())
+
+    def items(self):
+        return [(i, self[i]) for i in self.keys()]
+
+    def values(self):
+        return [self[i] for i in self.keys()]
+
+
+class Hss2dMatrix:
+    """Outer skeleton compression of the system matrix, resident in HBM
+    (solver_dense.py:98-231)."""
+
+    def __init__(self, spec, grid, tree, eps, opts, quad=PLAIN):
+        _lib.require_cuda()
+        self.spec, self.grid, self.tree = spec, grid, tree
+        self.eps, self.opts, self.quad = eps, opts, quad
+        self.asm = get_assembler(spec, grid, quad)
+        self.device = self.asm.device
+        self.symmetric = spec.symmetric
+        self.group = 1 if self.symmetric else 2
+        self.levels = [_Level(lv, tree.ids[lv], tree.rects[lv], lv == tree.depth)
+                       for lv in range(tree.depth + 1)]
+        self._lvl_of = {}
+        for L in self.levels:
+            for j, i in enumerate(L.ids):
+                self._lvl_of[int(i)] = (L, j)
+        nonroot = lambda: [i for i in self._lvl_of if i != 0]
+        nonleaf = lambda: [i for i in self._lvl_of if not self.levels[self._lvl_of[i][0].lv].leaf]
+        leaves = lambda: [i for i in self._lvl_of if self._lvl_of[i][0].leaf]
+        self.row_skel = _BoxView(self, lambda i: self._skel(i, "rskel"), nonroot)
+        self.col_skel = _BoxView(self, lambda i: self._skel(i, "cskel"), nonroot)
+        self.Lfac = _BoxView(self, lambda i: self._interp(i, "row"), nonroot)
+        self.Rfac = _BoxView(self, lambda i: self._interp(i, "col"), nonroot)
+        self.D = _BoxView(self, self._dblock, leaves)
+        self.B = _BoxView(self, self._bblock, nonleaf)
+        self._interp_cache = {}
+
+    @property
+    def n(self):
+        return self.grid.n
+
+    # -- host views ---------------------------------------------------------
+    def _skel(self, i, which):
+        L, j = self._lvl_of[i]
+        k = int(L.k[j])
+        return getattr(L, which)[j, :k].cpu().numpy().astype(np.int64)
+
+    def _interp(self, i, which):
+        key = (i, "row" if (which == "row" or self.symmetric) else "col")
+        if key in self._interp_cache:
+            return self._interp_cache[key]
+        L, j = self._lvl_of[i]
+        k, m = int(L.k[j]), int(L.m[j])
+        perm = (L.perm_r if key[1] == "row" else L.perm_c)[j, :m].cpu().numpy()
+        Tbuf = L.Tr if key[1] == "row" else L.Tc
+        T = Tbuf[j, :m - k, :k].cpu().numpy().T.copy()
+        f = FactoredInterp(perm, T)
+        self._interp_cache[key] = f
+        if self.symmetric:
+            self._interp_cache[(i, "col")] = f
+        return f
+
+    def _dblock(self, i):
+        L, j = self._lvl_of[i]
+        m = int(L.m[j])
+        return L.D[j, :m, :m].t().cpu().numpy()
+
+    def _bblock(self, i):
+        L, j = self._lvl_of[i]
+        C = self.levels[L.lv + 1]
+        k1, k2 = int(C.k[2 * j]), int(C.k[2 * j + 1])
+        return (L.B12[j, :k2, :k1].t().cpu().numpy(), L.B21[j, :k1, :k2].t().cpu().numpy())
+
+    def work_rows(self, box):
+        if box.is_leaf:
+            return self.tree.owned_indices(box)
+        c1, c2 = box.children
+        return np.concatenate([self.row_skel[c1], self.row_skel[c2]])
+
+    def work_cols(self, box):
+        if box.is_leaf:
+            return self.tree.owned_indices(box)
+        c1, c2 = box.children
+        return np.concatenate([self.col_skel[c1], self.col_skel[c2]])
+
+    def nbytes(self):
+        """D + B + T bytes of the real entries (solver_dense.py:132-139)."""
+        tot = 0
+        for L in self.levels:
+            if L.leaf:
+                tot += int((L.m.astype(np.int64) ** 2).sum()) * 8
+            if L.lv < len(self.levels) - 1:
+                C = self.levels[L.lv + 1]
+                k1, k2 = C.k[0::2].astype(np.int64), C.k[1::2].astype(np.int64)
+                tot += int((2 * k1 * k2).sum()) * 8
+            if L.lv > 0:
+                t = int((L.k.astype(np.int64) * (L.m - L.k)).sum()) * 8
+                tot += t * (1 if self.symmetric else 2)
+        return tot * (2 if self.spec.is_complex else 1)
+
+    # -- forward operator ---------------------------------------------------
+    def matvec(self, x):
+        return _matvec(self, x)
+
+    def densify(self):
+        """Dense reconstruction (tests, small N)."""
+        n = self.grid.n
+        eye = np.eye(n)
+        return self.matvec(eye)
+
+
+# ---------------------------------------------------------------------------
+# compress_outer
+
+def _level_sources(H, L, pad):
+    dev = H.device
+    w = L.rects[:, 1] - L.rects[:, 0]
+    h = L.rects[:, 3] - L.rects[:, 2]
+    p = np.array([proxy_count(int(a), int(b), pad) for a, b in zip(w, h)], dtype=np.int64)
+    p += near_count(L.rects, H.grid.n_side, pad)
+    pmax = int(p.max())
+    rects = _dev_i32(L.rects, dev)
+    src_xy = torch.empty((L.nb, pmax, 2), dtype=_I32, device=dev)
+    src_g = torch.empty((L.nb, pmax), dtype=_I32, device=dev)
+    p_d = torch.empty(L.nb, dtype=_I32, device=dev)
+    _lib.call("vief_box_sources", _lib.ptr(rects), L.nb, pad, H.grid.n_side, _lib.ptr(src_xy),
+              _lib.ptr(src_g), pmax, _lib.ptr(p_d), _lib.stream_handle())
+    return p.astype(np.int32), pmax, src_xy, src_g
+
+
+def _compress_level(H, L, pad, seed):
+    dev, asm = H.device, H.asm
+    prob = ctypes.byref(asm.problem)
+    st = _lib.stream_handle
+    nb = L.nb
+    # work rows / cols
+    if L.leaf:
+        own = H.tree.owned_level(L.lv)
+        L.m = (own >= 0).sum(axis=1).astype(np.int32)
+        L.mmax = int(L.m.max())
+        L.rows = _dev_i32(np.where(own >= 0, own, 0), dev)
+        L.cols = L.rows
+        L.cat_idx = None
+    else:
+        C = H.levels[L.lv + 1]
+        k1, k2 = C.k[0::2].astype(np.int64), C.k[1::2].astype(np.int64)
+        L.m = (k1 + k2).astype(np.int32)
+        L.mmax = int(L.m.max())
+        t = np.arange(L.mmax)[None, :]
+        cat = np.where(t < k1[:, None], t, C.kmax + t - k1[:, None])
+        cat = np.where(t < L.m[:, None], cat, 0)
+        L.cat_idx = _dev_i32(cat, dev)
+        L.rows = torch.zeros((nb, L.mmax), dtype=_I32, device=dev)
+        m_d = _dev_i32(L.m, dev)
+        _lib.gather_int(C.rskel, 2 * C.kmax, L.cat_idx, L.mmax, L.rows, L.mmax, m_d, L.mmax, nb)
+        if H.symmetric:
+            L.cols = L.rows
+        else:
+            L.cols = torch.zeros((nb, L.mmax), dtype=_I32, device=dev)
+            _lib.gather_int(C.cskel, 2 * C.kmax, L.cat_idx, L.mmax, L.cols, L.mmax, m_d, L.mmax, nb)
+    L.m_d = _dev_i32(L.m, dev)
+    # leaf D / sibling B blocks (solver_dense.py:243-249)
+    if L.leaf:
+        L.D = torch.empty((nb, L.mmax, L.mmax), dtype=_F64, device=dev)
+        _lib.call("vief_gen_block", prob, _lib.ptr(L.rows), L.mmax, _lib.ptr(L.m_d), L.mmax,
+                  _lib.ptr(L.rows), L.mmax, _lib.ptr(L.m_d), L.mmax, _lib.ptr(L.D),
+                  L.mmax * L.mmax, None, L.mmax, nb, st())
+    else:
+        C = H.levels[L.lv + 1]
+        kc = C.kmax
+        k1d, k2d = C.k_d[0::2].contiguous(), C.k_d[1::2].contiguous()
+        L.B12 = torch.zeros((nb, kc, kc), dtype=_F64, device=dev)   # [item, col, row]
+        L.B21 = torch.zeros((nb, kc, kc), dtype=_F64, device=dev)
+        rs, cs = C.rskel, C.cskel
+        _lib.call("vief_gen_block", prob, _lib.ptr(rs), 2 * kc, _lib.ptr(k1d), kc,
+                  _lib.ptr(cs) + 4 * kc, 2 * kc, _lib.ptr(k2d), kc, _lib.ptr(L.B12), kc * kc, None,
+                  kc, nb, st())
+        _lib.call("vief_gen_block", prob, _lib.ptr(rs) + 4 * kc, 2 * kc, _lib.ptr(k2d), kc,
+                  _lib.ptr(cs), 2 * kc, _lib.ptr(k1d), kc, _lib.ptr(L.B21), kc * kc, None,
+                  kc, nb, st())
+    if L.lv == 0:
+        return
+    # proxy + near sources and the ID matrices (solver_dense.py:250-263)
+    p, pmax, src_xy, src_g = _level_sources(H, L, pad)
+    g = H.group
+    count = nb * g
+    ldA = _even(pmax)
+    mm = L.mmax
+    A = torch.zeros((count, mm, ldA), dtype=_F64, device=dev)
+    p_d = _dev_i32(p, dev)
+    _lib.call("vief_gen_idmat", prob, 0, _lib.ptr(L.rows), mm, _lib.ptr(L.m_d), mm,
+              _lib.ptr(src_xy), _lib.ptr(src_g), pmax, _lib.ptr(p_d), pmax, _lib.ptr(A),
+              g * mm * ldA, ldA, nb, st())
+    if g == 2:
+        _lib.call("vief_gen_idmat", prob, 1, _lib.ptr(L.cols), mm, _lib.ptr(L.m_d), mm,
+                  _lib.ptr(src_xy), _lib.ptr(src_g), pmax, _lib.ptr(p_d), pmax,
+                  _lib.ptr(A) + 8 * mm * ldA, g * mm * ldA, ldA, nb, st())
+    del src_xy, src_g
+    pv = _dev_i32(np.repeat(p, g), dev)
+    mv = _dev_i32(np.repeat(L.m, g), dev)
+    rank = torch.zeros(count, dtype=_I32, device=dev)
+    perm = torch.zeros((count, mm), dtype=_I32, device=dev)
+    T = torch.zeros((count, mm, mm), dtype=_F64, device=dev)
+    d = _lib.IdDesc(_lib.ptr(A), mm * ldA, ldA, _lib.ptr(pv), _lib.ptr(mv), pmax, mm, count, g,
+                    float(H.eps), _lib.ptr(rank), _lib.ptr(perm), _lib.ptr(T), mm * mm, mm,
+                    int(seed) * 1000003 + L.lv, int(getattr(H, "_force_blocked", 0)))
+    _lib.call("vief_id_batched", ctypes.byref(d), st())
+    del A
+    L.k = rank[0::g].cpu().numpy().astype(np.int32)
+    L.kmax = max(int(L.k.max()), 1)
+    L.k_d = _dev_i32(L.k, dev)
+    nT = L.m - L.k
+    L.ntmax = max(int(nT.max()), 1)
+    L.nT_d = _dev_i32(nT, dev)
+    L.perm_r = perm[0::g].contiguous()
+    L.perm_c = perm[1::g].contiguous() if g == 2 else L.perm_r
+    # T compacted to [item, col (m-k), row (k)] with ld = kmax
+    L.Tr = torch.zeros((nb, L.ntmax, L.kmax), dtype=_F64, device=dev)
+    _lib.copy2d(T, g * mm * mm, mm, L.Tr, L.ntmax * L.kmax, L.kmax, L.k_d, L.kmax, L.nT_d,
+                L.ntmax, nb)
+    if g == 2:
+        L.Tc = torch.zeros_like(L.Tr)
+        _lib.copy2d(_lib.ptr(T) + 8 * mm * mm, g * mm * mm, mm, L.Tc, L.ntmax * L.kmax, L.kmax,
+                    L.k_d, L.kmax, L.nT_d, L.ntmax, nb)
+    else:
+        L.Tc = L.Tr
+    del T
+    # skeletons in pivot order: rows[perm[:k]] (solver_dense.py:270-271)
+    L.rskel = torch.zeros((nb, L.kmax), dtype=_I32, device=dev)
+    _lib.gather_int(L.rows, mm, L.perm_r, mm, L.rskel, L.kmax, L.k_d, L.kmax, nb)
+    if g == 2:
+        L.cskel = torch.zeros((nb, L.kmax), dtype=_I32, device=dev)
+        _lib.gather_int(L.cols, mm, L.perm_c, mm, L.cskel, L.kmax, L.k_d, L.kmax, nb)
+    else:
+        L.cskel = L.rskel
+
+
+def compress_outer(spec, grid, tree, eps, opts, quad=PLAIN, spill=None):
+    """Skeletonize all boxes fine-to-coarse, one batch per level
+    (solver_dense.py:234-272).  `spill` is accepted for signature
+    compatibility; every block stays in HBM."""
+    H = Hss2dMatrix(spec, grid, tree, eps, opts, quad)
+    pad = opts.resolved_proxy_layers(spec)
+    for L in reversed(H.levels):
+        _compress_level(H, L, pad, opts.seed)
+    return H
+
+
+# ---------------------------------------------------------------------------
+# invert_dense_block
+
+def _check_singular(H, L, pmin, pmax, what):
+    lo, hi = pmin.cpu().numpy(), pmax.cpu().numpy()
+    eps2 = np.finfo(float).eps ** 2
+    bad = (hi == 0.0) | (lo <= 1e-300) | (lo / np.where(hi == 0.0, 1.0, hi) < eps2) | ~np.isfinite(lo)
+    if bad.any():
+        j = int(np.flatnonzero(bad)[0])
+        i = int(L.ids[j])
+        where = f"box {i} level {L.lv}" if what == "F" else f"E of box {i}"
+        raise SingularFactorError(where, float(lo[j]))
+
+
+def _invert_level(inv, L):
+    H = inv.H
+    dev = H.device
+    nb, mm = L.nb, L.mmax
+    F = torch.zeros((nb, mm, mm), dtype=_F64, device=dev)
+    if L.leaf:
+        F.copy_(L.D)
+    else:
+        C = H.levels[L.lv + 1]
+        kc = C.kmax
+        k1, k2 = C.k[0::2].astype(np.int64), C.k[1::2].astype(np.int64)
+        k1d, k2d = C.k_d[0::2].contiguous(), C.k_d[1::2].contiguous()
+        base = np.arange(nb, dtype=np.int64) * mm * mm
+        # F[:k1,:k1] = E1 ; F[k1:,k1:] = E2 ; F[:k1,k1:] = B12 ; F[k1:,:k1] = B21
+        _lib.copy2d(C.E, 2 * kc * kc, kc, F, mm * mm, mm, k1d, kc, k1d, kc, nb)
+        _lib.copy2d(_lib.ptr(C.E) + 8 * kc * kc, 2 * kc * kc, kc, None, 0, mm, k2d, kc, k2d, kc, nb,
+                    dstp=_ptrs(F, base + k1 * mm + k1, dev))
+        _lib.copy2d(L.B12, kc * kc, kc, None, 0, mm, k1d, kc, k2d, kc, nb,
+                    dstp=_ptrs(F, base + k1 * mm, dev))
+        _lib.copy2d(L.B21, kc * kc, kc, None, 0, mm, k2d, kc, k1d, kc, nb,
+                    dstp=_ptrs(F, base + k1, dev))
+    _lib.pad_identity(F, mm * mm, mm, L.m_d, mm, nb)
+    pmin, pmax = _lib.inv_batched(F, mm * mm, mm, mm, nb)
+    _check_singular(H, L, pmin, pmax, "F")
+    L.Finv = F
+    if L.lv == 0:
+        return
+    kk = L.kmax
+    k = L.k.astype(np.int64)
+    base = np.arange(nb, dtype=np.int64)
+    # W = F^{-1} L = Fp[:, :k] + Fp[:, k:] Tr^T,  Fp = F^{-1}[:, perm_r]
+    Fp = torch.empty((nb, mm, mm), dtype=_F64, device=dev)
+    _lib.gather_cols(F, mm * mm, mm, L.perm_r, mm, Fp, mm * mm, mm, L.m_d, mm, L.m_d, mm, nb)
+    W = torch.zeros((nb, kk, mm), dtype=_F64, device=dev)
+    _lib.copy2d(Fp, mm * mm, mm, W, kk * mm, mm, L.m_d, mm, L.k_d, kk, nb)
+    _lib.gemm(None, L.Tr, W, M=mm, N=kk, K=L.ntmax, lda=mm, ldb=kk, ldc=mm,
+              sB=L.ntmax * kk, sC=kk * mm, tB=1, alpha=1.0, beta=1.0, batch=nb,
+              Mb=L.m_d, Nb=L.k_d, Kb=L.nT_d, Aptr=_ptrs(Fp, base * mm * mm + k * mm, dev))
+    del Fp
+    # G = R W = Wp[:k] + Tc Wp[k:],  Wp = W[perm_c, :]
+    Wp = torch.empty((nb, kk, mm), dtype=_F64, device=dev)
+    _lib.gather_rows(W, kk * mm, mm, L.perm_c, mm, Wp, kk * mm, mm, L.m_d, mm, L.k_d, kk, nb)
+    G = torch.zeros((nb, kk, kk), dtype=_F64, device=dev)
+    _lib.copy2d(Wp, kk * mm, mm, G, kk * kk, kk, L.k_d, kk, L.k_d, kk, nb)
+    _lib.gemm(L.Tc, None, G, M=kk, N=kk, K=L.ntmax, lda=kk, ldb=mm, ldc=kk,
+              sA=L.ntmax * kk, sC=kk * kk, alpha=1.0, beta=1.0, batch=nb,
+              Mb=L.k_d, Nb=L.k_d, Kb=L.nT_d, Bptr=_ptrs(Wp, base * kk * mm + k, dev))
+    del Wp
+    _lib.pad_identity(G, kk * kk, kk, L.k_d, kk, nb)
+    pmin, pmax = _lib.inv_batched(G, kk * kk, kk, kk, nb)
+    _check_singular(H, L, pmin, pmax, "E")
+    L.E = G
+    L.W = W
+    # C = E R: Cp = [E, E Tc] then columns scattered to perm_c
+    Cp = torch.zeros((nb, mm, kk), dtype=_F64, device=dev)
+    _lib.copy2d(G, kk * kk, kk, Cp, mm * kk, kk, L.k_d, kk, L.k_d, kk, nb)
+    _lib.gemm(G, L.Tc, None, M=kk, N=L.ntmax, K=kk, lda=kk, ldb=kk, ldc=kk,
+              sA=kk * kk, sB=L.ntmax * kk, alpha=1.0, beta=0.0, batch=nb,
+              Mb=L.k_d, Nb=L.nT_d, Kb=L.k_d, Cptr=_ptrs(Cp, base * mm * kk + k * kk, dev))
+    Cm = torch.zeros((nb, mm, kk), dtype=_F64, device=dev)
+    _lib.scatter_cols(Cp, mm * kk, kk, L.perm_c, mm, Cm, mm * kk, kk, L.k_d, kk, L.m_d, mm, nb)
+    L.C = Cm
+
+
+class DenseBlockInverse:
+    """Per-box factors of the telescoping inverse (solver_dense.py:275-329),
+    held in HBM as per-level batches: F^{-1}, W = F^{-1}L, E, C = E R."""
+
+    def __init__(self, H):
+        self.H = H
+        self.tree = H.tree
+        levels = H.levels
+        ids = lambda pred: [int(i) for L in levels if pred(L) for i in L.ids]
+        self.E = _BoxView(self, lambda i: self._get(i, "E"), lambda: ids(lambda L: L.lv > 0))
+        self.Finv = _BoxView(self, lambda i: self._get(i, "Finv"), lambda: ids(lambda L: True))
+
+    def _get(self, i, which):
+        L, j = self.H._lvl_of[i]
+        if which == "E":
+            k = int(L.k[j])
+            return L.E[j, :k, :k].t().cpu().numpy()
+        m = int(L.m[j])
+        return L.Finv[j, :m, :m].t().cpu().numpy()
+
+    def nbytes(self):
+        """Bytes of the factors this object holds (F^{-1}, E, W, C, T)."""
+        tot = 0
+        H = self.H
+        for L in H.levels:
+            m = L.m.astype(np.int64)
+            tot += int((m * m).sum()) * 8
+            if L.lv > 0:
+                k = L.k.astype(np.int64)
+                tot += int((k * k + 2 * k * m).sum()) * 8
+                tot += int((k * (m - k)).sum()) * 8 * H.group
+        return tot
+
+    def nbytes_reference_layout(self):
+        """What the reference's inv.nbytes() would count for the same ranks:
+        F + E + T (solver_dense.py:284-291)."""
+        tot = 0
+        H = self.H
+        for L in H.levels:
+            m = L.m.astype(np.int64)
+            tot += int((m * m).sum()) * 8
+            if L.lv > 0:
+                k = L.k.astype(np.int64)
+                tot += int((k * k).sum()) * 8 + int((k * (m - k)).sum()) * 8 * H.group
+        return tot
+
+    def apply(self, f):
+        return _apply(self, f)
+
+
+def invert_dense_block(H, spill=None, free_source=False):
+    """Fine-to-coarse telescoping inversion, one batch per level
+    (solver_dense.py:332-368).  `free_source` drops D/B once consumed."""
+    inv = DenseBlockInverse(H)
+    for L in reversed(H.levels):
+        _invert_level(inv, L)
+        if free_source:
+            if L.leaf:
+                L.D = None
+            else:
+                L.B12 = L.B21 = None
+    return inv
+
+
+# ---------------------------------------------------------------------------
+# solve sweeps
+
+def _as_device_rhs(x, n, device):
+    """(N,) or (N, r) numpy/torch -> (r, N) float64 device tensor (column-major N x r)."""
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device, dtype=_F64)
+    else:
+        arr = np.asarray(x)
+        if np.iscomplexobj(arr):
+            raise NotImplementedError("complex right-hand sides need the complex128 path")
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device)
+    single = t.dim() == 1
+    t2 = t[:, None] if single else t
+    if t2.shape[0] != n:
+        raise ValueError(f"rhs has {t2.shape[0]} rows, expected {n}")
+    return t2.t().contiguous(), single
+
+
+def _level_dn_idx(H, L):
+    """Absolute offsets of each child's phi_dn slice in the parent's result
+    buffer ([r, nb_p * mm_p] layout)."""
+    if getattr(L, "dn_idx", None) is not None:
+        return L.dn_idx
+    P = H.levels[L.lv - 1]
+    j = np.arange(L.nb)
+    off = (j // 2) * P.mmax + np.where(j % 2 == 1, np.roll(L.k, 1), 0)
+    t = np.arange(L.kmax)[None, :]
+    idx = np.where(t < L.k[:, None], off[:, None] + t, 0)
+    L.dn_idx = _dev_i32(idx, H.device)
+    return L.dn_idx
+
+
+def _mv(A, sA, lda, X, sx, ldx, Y, sy, ldy, M, K, Mb, Kb, nb, r, alpha, beta):
+    """Y_b = alpha * A_b X_b + beta * Y_b for r right-hand sides."""
+    if r == 1:
+        _lib.gemv(A, X, Y, M=M, K=K, lda=lda, sA=sA, sx=sx, sy=sy, alpha=alpha, beta=beta,
+                  batch=nb, Mb=Mb, Kb=Kb)
+    else:
+        _lib.gemm(A, X, Y, M=M, N=r, K=K, lda=lda, ldb=ldx, ldc=ldy, sA=sA, sB=sx, sC=sy,
+                  alpha=alpha, beta=beta, batch=nb, Mb=Mb, Kb=Kb)
+
+
+def _apply_device(inv, fd):
+    """fd: (r, N) device tensor -> (r, N) solution (device)."""
+    H = inv.H
+    dev = H.device
+    r, n = fd.shape
+    levels = H.levels
+    phi, ups = {}, {}
+    for L in reversed(levels):
+        nb, mm = L.nb, L.mmax
+        ldv = nb * mm
+        U = torch.zeros((r, ldv), dtype=_F64, device=dev)
+        if L.leaf:
+            _lib.gather_rows(fd, 0, n, L.rows, mm, U, mm, ldv, L.m_d, mm, None, r, nb)
+        else:
+            C = levels[L.lv + 1]
+            _lib.gather_rows(ups[C.lv], 2 * C.kmax, C.nb * C.kmax, L.cat_idx, mm, U, mm, ldv,
+                             L.m_d, mm, None, r, nb)
+        Phi = torch.zeros((r, ldv), dtype=_F64, device=dev)
+        _mv(L.Finv, mm * mm, mm, U, mm, ldv, Phi, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r, 1.0, 0.0)
+        del U
+        phi[L.lv] = Phi
+        if L.lv == 0:
+            break
+        kk = L.kmax
+        Ups = torch.zeros((r, nb * kk), dtype=_F64, device=dev)
+        _mv(L.C, mm * kk, kk, Phi, mm, ldv, Ups, kk, nb * kk, kk, mm, L.k_d, L.m_d, nb, r,
+            1.0, 0.0)
+        ups[L.lv] = Ups
+    out = torch.zeros((r, n), dtype=_F64, device=dev)
+    for L in levels:
+        nb, mm = L.nb, L.mmax
+        ldv = nb * mm
+        Phi = phi[L.lv]
+        if L.lv > 0:
+            P = levels[L.lv - 1]
+            kk = L.kmax
+            PD = torch.zeros((r, nb * kk), dtype=_F64, device=dev)
+            _lib.gather_rows(phi[P.lv], 0, P.nb * P.mmax, _level_dn_idx(H, L), kk, PD, kk,
+                             nb * kk, L.k_d, kk, None, r, nb)
+            Ups = ups[L.lv]
+            # d = ups - E phi_dn ; res = phi - W d
+            _mv(L.E, kk * kk, kk, PD, kk, nb * kk, Ups, kk, nb * kk, kk, kk, L.k_d, L.k_d, nb, r,
+                -1.0, 1.0)
+            _mv(L.W, kk * mm, mm, Ups, kk, nb * kk, Phi, mm, ldv, mm, kk, L.m_d, L.k_d, nb, r,
+                -1.0, 1.0)
+            del PD
+        if L.leaf:
+            _lib.scatter_rows(Phi, mm, ldv, L.rows, mm, out, 0, n, L.m_d, mm, None, r, nb)
+    return out
+
+
+def _apply(inv, f):
+    H = inv.H
+    fd, single = _as_device_rhs(f, H.grid.n, H.device)
+    out = _apply_device(inv, fd)
+    res = out.t()
+    if isinstance(f, torch.Tensor):
+        return res[:, 0] if single else res
+    arr = res.cpu().numpy()
+    return arr[:, 0].copy() if single else np.ascontiguousarray(arr)
+
+
+def apply_inverse_dense_block(inv, f):
+    return inv.apply(f)
+
+
+# ---------------------------------------------------------------------------
+# forward operator (solver_dense.py:143-178)
+
+def _matvec_device(H, xd):
+    dev = H.device
+    r, n = xd.shape
+    levels = H.levels
+    phi = {}
+    for L in reversed(levels):
+        if L.lv == 0:
+            break
+        nb, mm, kk = L.nb, L.mmax, L.kmax
+        ldv = nb * mm
+        Wv = torch.zeros((r, ldv), dtype=_F64, device=dev)
+        if L.leaf:
+            _lib.gather_rows(xd, 0, n, L.rows, mm, Wv, mm, ldv, L.m_d, mm, None, r, nb)
+        else:
+            C = levels[L.lv + 1]
+            _lib.gather_rows(phi[C.lv], 2 * C.kmax, C.nb * C.kmax, L.cat_idx, mm, Wv, mm, ldv,
+                             L.m_d, mm, None, r, nb)
+        # phi = R w = wp[:k] + Tc wp[k:],  wp = w[perm_c]
+        Wp = torch.zeros((r, ldv), dtype=_F64, device=dev)
+        _lib.gather_rows(Wv, mm, ldv, L.perm_c, mm, Wp, mm, ldv, L.m_d, mm, None, r, nb)
+        Ph = torch.zeros((r, nb * kk), dtype=_F64, device=dev)
+        _lib.copy2d(Wp, mm, ldv, Ph, kk, nb * kk, L.k_d, kk, None, r, nb)
+        k = L.k.astype(np.int64)
+        base = np.arange(nb, dtype=np.int64) * mm
+        _gemm_ptr_rhs(L.Tc, L.ntmax * kk, kk, Wp, base + k, ldv, Ph, kk, nb * kk,
+                      kk, L.ntmax, L.k_d, L.nT_d, nb, r, 1.0, 1.0, dev)
+        phi[L.lv] = Ph
+    out = torch.zeros((r, n), dtype=_F64, device=dev)
+    wdn = {}
+    for L in levels:
+        nb, mm = L.nb, L.mmax
+        ldv = nb * mm
+        t = None
+        if L.lv > 0:
+            # t = L w_in : tp = [w; Tr^T w] scattered by perm_r
+            kk = L.kmax
+            win = wdn[L.lv]
+            tp = torch.zeros((r, ldv), dtype=_F64, device=dev)
+            _lib.copy2d(win, kk, nb * kk, tp, mm, ldv, L.k_d, kk, None, r, nb)
+            k = L.k.astype(np.int64)
+            base = np.arange(nb, dtype=np.int64) * mm
+            # tp[k:m] = Tr^T w   (Tr stored [item, col, row]: Tr^T is (m-k) x k, ld kmax, trans)
+            _gemm_ptr_out(L.Tr, L.ntmax * kk, kk, win, kk, nb * kk, tp, base + k, ldv,
+                          L.ntmax, kk, L.nT_d, L.k_d, nb, r, dev)
+            t = torch.zeros((r, ldv), dtype=_F64, device=dev)
+            _lib.scatter_rows(tp, mm, ldv, L.perm_r, mm, t, mm, ldv, L.m_d, mm, None, r, nb)
+        if L.leaf:
+            y = torch.zeros((r, ldv), dtype=_F64, device=dev)
+            xin = torch.zeros((r, ldv), dtype=_F64, device=dev)
+            _lib.gather_rows(xd, 0, n, L.rows, mm, xin, mm, ldv, L.m_d, mm, None, r, nb)
+            _mv(L.D, mm * mm, mm, xin, mm, ldv, y, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r, 1.0, 0.0)
+            if t is not None:
+                y += t
+            _lib.scatter_rows(y, mm, ldv, L.rows, mm, out, 0, n, L.m_d, mm, None, r, nb)
+            continue
+        # children: w1 = B12 phi[c2] + t[:k1], w2 = B21 phi[c1] + t[k1:]
+        C = levels[L.lv + 1]
+        kc = C.kmax
+        wc = torch.zeros((r, C.nb * kc), dtype=_F64, device=dev)
+        k1d, k2d = C.k_d[0::2].contiguous(), C.k_d[1::2].contiguous()
+        ph = phi[C.lv]
+        # wc[2j] = B12_j phi[2j+1] ; wc[2j+1] = B21_j phi[2j]
+        _mv(L.B12, kc * kc, kc, _lib.ptr(ph) + 8 * kc, 2 * kc, C.nb * kc, wc, 2 * kc, C.nb * kc,
+            kc, kc, k1d, k2d, nb, r, 1.0, 0.0)
+        _mv(L.B21, kc * kc, kc, ph, 2 * kc, C.nb * kc, _lib.ptr(wc) + 8 * kc, 2 * kc, C.nb * kc,
+            kc, kc, k2d, k1d, nb, r, 1.0, 0.0)
+        if t is not None:
+            # add t (parent order: [k1 | k2]) into the children slices
+            _scatter_add_children(t, L, C, wc, r, dev)
+        wdn[C.lv] = wc
+    return out
+
+
+def _gemm_ptr_rhs(A, sA, lda, X, xoff, ldx, Y, sy, ldy, M, K, Mb, Kb, nb, r, alpha, beta, dev):
+    """Y_b += A_b X[xoff_b : xoff_b + K] for r right-hand sides (pointer arrays)."""
+    xp = _ptrs(X, xoff, dev)
+    if r == 1:
+        _lib.gemv(A, None, Y, M=M, K=K, lda=lda, sA=sA, sy=sy, alpha=alpha, beta=beta,
+                  batch=nb, Mb=Mb, Kb=Kb, xptr=xp)
+    else:
+        _lib.gemm(A, None, Y, M=M, N=r, K=K, lda=lda, ldb=ldx, ldc=ldy, sA=sA, sC=sy,
+                  alpha=alpha, beta=beta, batch=nb, Mb=Mb, Kb=Kb, Bptr=xp)
+
+
+def _gemm_ptr_out(A, sA, lda, X, sx, ldx, Y, yoff, ldy, M, K, Mb, Kb, nb, r, dev):
+    """Y[yoff_b : yoff_b + M] = op(A_b)^T X_b where A_b is stored K x M (trans)."""
+    yp = _ptrs(Y, yoff, dev)
+    if r == 1:
+        _lib.gemv(A, X, None, M=M, K=K, lda=lda, sA=sA, sx=sx, tA=1, alpha=1.0, beta=0.0,
+                  batch=nb, Mb=Mb, Kb=Kb, yptr=yp)
+    else:
+        _lib.gemm(A, X, None, M=M, N=r, K=K, lda=lda, ldb=ldx, ldc=ldy, sA=sA, sB=sx, tA=1,
+                  alpha=1.0, beta=0.0, batch=nb, Mb=Mb, Kb=Kb, Cptr=yp)
+
+
+def _scatter_add_children(t, L, C, wc, r, dev):
+    """wc[child slice] += t[parent rows] with parent rows = [k1 | k2]."""
+    if getattr(L, "_child_scatter", None) is None:
+        # absolute destination offset in wc for parent row i of box j
+        k1, k2 = C.k[0::2].astype(np.int64), C.k[1::2].astype(np.int64)
+        j = np.arange(L.nb)[:, None]
+        i = np.arange(L.mmax)[None, :]
+        dst = np.where(i < k1[:, None], (2 * j) * C.kmax + i, (2 * j + 1) * C.kmax + i - k1[:, None])
+        dst = np.where(i < (k1 + k2)[:, None], dst, 0)
+        src = j * L.mmax + i
+        L._child_scatter = (_dev_i32(dst, dev), _dev_i32(src, dev))
+    dst, src = L._child_scatter
+    tmp = torch.zeros_like(wc)
+    # gather t rows into child layout then add
+    _lib.scatter_rows(t, L.mmax, L.nb * L.mmax, dst, L.mmax, tmp, 0, C.nb * C.kmax, L.m_d,
+                      L.mmax, None, r, L.nb)
+    wc += tmp
+
+
+def _matvec(H, x):
+    xd, single = _as_device_rhs(x, H.grid.n, H.device)
+    out = _matvec_device(H, xd).t()
+    if isinstance(x, torch.Tensor):
+        return out[:, 0] if single else out
+    arr = out.cpu().numpy()
+    return arr[:, 0].copy() if single else np.ascontiguousarray(arr)
+
+
+def hss_matvec(H, x):
+    return H.matvec(x)

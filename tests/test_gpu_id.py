@@ -1,0 +1,112 @@
+"""ID (K2) contracts, ported from the reference's test_dense_core.py:20-77 and
+run on BOTH device paths (shared-memory classical QRCP and the blocked
+randomized path), plus parity with the oracle's LAPACK ID on kernel blocks."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PATHS = [False, True]
+
+
+def reconstruct(A, f):
+    return A[:, f.skeleton] @ f.right_matrix(A.dtype)
+
+
+def planted(rng, m, n, sv):
+    u, _ = np.linalg.qr(rng.standard_normal((m, min(m, n))))
+    v, _ = np.linalg.qr(rng.standard_normal((n, min(m, n))))
+    return (u * sv) @ v.T
+
+
+@pytest.mark.parametrize("blocked", PATHS)
+def test_id_identity_full_rank(blocked):
+    from paper_1303_5466_b200.dense_core import interp_decomp
+    f = interp_decomp(np.eye(3), 1e-10, force_blocked=blocked)
+    assert f.rank == 3 and f.T.shape == (3, 0)
+
+
+@pytest.mark.parametrize("blocked", PATHS)
+def test_id_rank_one(blocked):
+    from paper_1303_5466_b200.dense_core import interp_decomp
+    rng = np.random.default_rng(1)
+    A = np.outer(rng.standard_normal(20), rng.standard_normal(30))
+    f = interp_decomp(A, 1e-10, force_blocked=blocked)
+    assert f.rank == 1
+    assert np.linalg.norm(A - reconstruct(A, f), 2) <= 1e-10 * np.linalg.norm(A, 2)
+
+
+@pytest.mark.parametrize("blocked", PATHS)
+def test_id_skeleton_columns_exact(blocked):
+    from paper_1303_5466_b200.dense_core import interp_decomp
+    rng = np.random.default_rng(2)
+    A = planted(rng, 40, 50, np.geomspace(1, 1e-12, 40))
+    f = interp_decomp(A, 1e-8, force_blocked=blocked)
+    rec = reconstruct(A, f)
+    np.testing.assert_allclose(rec[:, f.skeleton], A[:, f.skeleton], atol=1e-13)
+
+
+@pytest.mark.parametrize("blocked", PATHS)
+def test_id_error_vs_svd_planted_spectra(blocked):
+    from paper_1303_5466_b200.dense_core import interp_decomp_batched
+    rng = np.random.default_rng(3)
+    mats, svs = [], []
+    for _ in range(200):
+        m, n = int(rng.integers(10, 60)), int(rng.integers(10, 60))
+        decay = 10.0 ** -rng.uniform(0.1, 1.0)
+        sv = decay ** np.arange(min(m, n))
+        mats.append(planted(rng, m, n, sv))
+        svs.append(sv)
+    res = interp_decomp_batched(mats, 1e-6, force_blocked=blocked)
+    worst = 0.0
+    for A, sv, (perm, k, T) in zip(mats, svs, res):
+        n = A.shape[1]
+        if k == min(A.shape):
+            continue
+        R = np.zeros((k, n))
+        R[np.arange(k), perm[:k]] = 1.0
+        R[:, perm[k:]] = T
+        err = np.linalg.norm(A - A[:, perm[:k]] @ R, 2)
+        worst = max(worst, err / (10.0 * np.sqrt(1.0 + k * (n - k)) * sv[k]))
+    assert worst <= 1.0
+
+
+@pytest.mark.parametrize("blocked", PATHS)
+def test_id_laplace_block_rank_near_svd(blocked):
+    from paper_1303_5466_b200 import Grid, KernelSpec, PLAIN, assemble_dense
+    from paper_1303_5466_b200.dense_core import interp_decomp
+    grid = Grid(14)
+    spec = KernelSpec("laplace2d")
+    n = grid.n_side
+    ix, iy = np.meshgrid(np.arange(7), np.arange(7), indexing="xy")
+    box1 = (iy * n + ix).ravel()
+    box2 = (iy * n + ix + 7).ravel()
+    A = assemble_dense(spec, grid, PLAIN, box1, box2)
+    f = interp_decomp(A, 1e-10, force_blocked=blocked)
+    sv = np.linalg.svd(A, compute_uv=False)
+    assert abs(f.rank - int(np.sum(sv > 1e-10 * sv[0]))) <= 5
+
+
+@pytest.mark.parametrize("shape", [(300, 200), (500, 450), (160, 64), (1200, 900)])
+def test_blocked_id_on_kernel_rows_vs_oracle(shape):
+    """Proxy-style smooth kernel block: blocked-path rank within a few of the
+    LAPACK ID's and reconstruction error at the tolerance."""
+    import oracle.hssd as O
+    from paper_1303_5466_b200.dense_core import interp_decomp_batched
+    p, m = shape
+    rng = np.random.default_rng(7)
+    src = rng.uniform(-1, 1, (m, 2)) * 0.5
+    th = np.linspace(0, 2 * np.pi, p, endpoint=False)
+    tgt = np.column_stack([1.2 * np.cos(th), 1.2 * np.sin(th)]) + rng.normal(0, 0.05, (p, 2))
+    r = np.hypot(*(tgt[:, None, :] - src[None, :, :]).transpose(2, 0, 1))
+    A = np.log(r)
+    eps = 1e-10
+    ref = O.column_id(A, eps)
+    (perm, k, T), = interp_decomp_batched([A], eps, force_blocked=True)
+    R = np.zeros((k, m))
+    R[np.arange(k), perm[:k]] = 1.0
+    R[:, perm[k:]] = T
+    err = np.linalg.norm(A - A[:, perm[:k]] @ R) / np.linalg.norm(A)
+    assert abs(k - ref.k) <= max(3, ref.k // 20), (k, ref.k)
+    assert err <= 50 * eps, err
+    assert len(set(perm.tolist())) == m
