@@ -37,6 +37,10 @@ int vief_version(void);
 const char* vief_last_error(void);
 /* number of kernel launches issued by this library since load (bench evidence) */
 long long vief_launch_count(void);
+/* phase profiler: CUDA-event totals per orchestration phase (synchronising; off by default) */
+void vief_prof_enable(int on);
+void vief_prof_prefix(const char* prefix);  /* tag subsequent phases (e.g. level) */
+int vief_prof_report(char* buf, int len);
 
 /* ---- problem description (kernels.py:216-302 Assembler state) ----------- */
 typedef struct {

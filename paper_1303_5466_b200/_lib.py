@@ -48,6 +48,9 @@ _SIGS = {
     "vief_version": [],
     "vief_last_error": [],
     "vief_launch_count": [],
+    "vief_prof_enable": [c_int],
+    "vief_prof_prefix": [ctypes.c_char_p],
+    "vief_prof_report": [ctypes.c_char_p, c_int],
     "vief_gen_block": [c_vp, c_vp, c_ll, c_vp, c_int, c_vp, c_ll, c_vp, c_int,
                        c_vp, c_ll, c_vp, c_int, c_int, c_vp],
     "vief_box_sources": [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_ll, c_vp, c_vp],
@@ -70,7 +73,7 @@ _SIGS = {
                     c_vp, c_int, c_vp, c_int, c_int, c_vp],
     "vief_pad_identity": [c_vp, c_ll, c_int, c_vp, c_int, c_int, c_vp],
 }
-_RET = {"vief_last_error": ctypes.c_char_p, "vief_launch_count": c_ll}
+_RET = {"vief_last_error": ctypes.c_char_p, "vief_launch_count": c_ll, "vief_prof_enable": None, "vief_prof_prefix": None}
 
 _lib = None
 
@@ -119,6 +122,16 @@ def call(name, *args):
         msg = lib.vief_last_error().decode(errors="replace")
         raise LibraryError(f"{name} failed (code {rc}): {msg}")
     return rc
+
+
+def prof_enable(on=True):
+    load().vief_prof_enable(int(on))
+
+
+def prof_report():
+    buf = ctypes.create_string_buffer(1 << 16)
+    load().vief_prof_report(buf, len(buf))
+    return buf.value.decode()
 
 
 def launch_count():
@@ -198,3 +211,7 @@ def inv_batched(A, sA, lda, n, batch):
     pmax = torch.empty(batch, dtype=torch.float64, device=A.device)
     call("vief_inv_batched", ptr(A), sA, lda, n, batch, ptr(pmin), ptr(pmax), stream_handle())
     return pmin, pmax
+
+
+def prof_prefix(tag):
+    load().vief_prof_prefix(tag.encode())

@@ -93,3 +93,17 @@ __device__ __forceinline__ void block_argmax(double& v, int& i, double* redv, in
 inline unsigned cdiv(long long a, long long b) { return static_cast<unsigned>((a + b - 1) / b); }
 
 }  // namespace vf
+
+// ---------------------------------------------------------------------------
+// optional phase profiler (vief_prof_enable): CUDA events around orchestration
+// phases, accumulated per phase name when the owning call finishes.
+namespace vf {
+bool prof_on();
+void prof_push(cudaStream_t st, const char* name);   // closes the previous phase, opens `name`
+void prof_flush(cudaStream_t st);                    // closes the open phase, syncs, accumulates
+}  // namespace vf
+namespace vf {
+// keep freed cudaMallocAsync blocks cached in the device pool (no OS round trip
+// per call); idempotent
+void ensure_pool();
+}  // namespace vf

@@ -3,8 +3,8 @@
 // (dense_core.py:222-230, solver_dense.py:361-367).
 //
 // Step s over block column [c0, c0+nb):
-//   1. k_gj_panel   (1 CTA / item): LU with partial pivoting of the panel rows
-//      c0..n-1 (a copy; shared memory when it fits), pivot rows, |U_jj| min/max
+//   1. lu_panel     (cluster of CTAs / item, panels.cu): LU with partial pivoting of the panel rows
+//      c0..n-1 (a copy in distributed shared memory), pivot rows, |U_jj| min/max
 //      (the reference's singularity test reads the same U diagonal), and
 //      A11^{-1} = U11^{-1} L11^{-1}.
 //   2. k_gj_swap    apply the nb row interchanges to all n columns.
@@ -16,101 +16,13 @@
 // partial-pivoting pivots of getrf (the trailing Schur complements coincide).
 #include <vector>
 #include "common.cuh"
+#include "panels.cuh"
 #include "../../include/vief_b200.h"
 
 namespace vf {
 extern long long g_launches;
 
 constexpr int GJ_NB = 32;
-
-__global__ void __launch_bounds__(256) k_gj_panel(const double* A, long long sA, int lda, int n,
-                                                  int c0, int nbs, double* Pg, long long sP,
-                                                  int* ipiv, long long sPiv, double* Ainv,
-                                                  long long sAi, double* pivmin, double* pivmax,
-                                                  int use_smem) {
-  extern __shared__ double dsm[];
-  __shared__ double rowj[GJ_NB];
-  __shared__ double M[GJ_NB][GJ_NB + 1], Li[GJ_NB][GJ_NB + 1], Ui[GJ_NB][GJ_NB + 1];
-  __shared__ double redv[32];
-  __shared__ int redi[32];
-  __shared__ double pmin, pmax;
-  const int b = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
-  const double* Ab = A + b * sA;
-  const int R = n - c0;
-  const int ldp = use_smem ? R : n;
-  double* P = use_smem ? dsm : Pg + b * sP;
-  for (int idx = tid; idx < R * nbs; idx += bd) {
-    int i = idx % R, j = idx / R;
-    P[j * ldp + i] = Ab[(long long)(c0 + j) * lda + c0 + i];
-  }
-  if (tid == 0) { pmin = pivmin[b]; pmax = pivmax[b]; }
-  __syncthreads();
-  for (int j = 0; j < nbs; ++j) {
-    double v = -1.0;
-    int iv = 0x7fffffff;
-    for (int i = j + tid; i < R; i += bd) {
-      double a = fabs(P[j * ldp + i]);
-      if (a > v) { v = a; iv = i; }
-    }
-    block_argmax(v, iv, redv, redi);
-    const int piv = iv;
-    if (tid == 0) {
-      ipiv[b * sPiv + c0 + j] = c0 + piv;
-      pmin = fmin(pmin, v);
-      pmax = fmax(pmax, v);
-    }
-    if (piv != j)
-      for (int l = tid; l < nbs; l += bd) {
-        double t = P[l * ldp + j];
-        P[l * ldp + j] = P[l * ldp + piv];
-        P[l * ldp + piv] = t;
-      }
-    __syncthreads();
-    if (tid < nbs) rowj[tid] = P[tid * ldp + j];
-    __syncthreads();
-    const double pv = rowj[j];
-    for (int i = j + 1 + tid; i < R; i += bd) {
-      double lij = P[j * ldp + i];
-      if (pv != 0.0) lij = lij / pv;
-      P[j * ldp + i] = lij;
-      for (int l = j + 1; l < nbs; ++l) P[l * ldp + i] = fma(-lij, rowj[l], P[l * ldp + i]);
-    }
-    __syncthreads();
-  }
-  // A11^{-1} = U11^{-1} L11^{-1}
-  for (int idx = tid; idx < nbs * nbs; idx += bd) {
-    int i = idx % nbs, j = idx / nbs;
-    M[i][j] = P[j * ldp + i];
-  }
-  __syncthreads();
-  if (tid < nbs) {
-    const int j = tid;
-    // column j of L^{-1} (unit lower)
-    for (int i = 0; i < nbs; ++i) Li[i][j] = (i == j) ? 1.0 : 0.0;
-    for (int i = j + 1; i < nbs; ++i) {
-      double s = 0.0;
-      for (int k = j; k < i; ++k) s = fma(M[i][k], Li[k][j], s);
-      Li[i][j] = -s;
-    }
-    // column j of U^{-1}
-    for (int i = 0; i < nbs; ++i) Ui[i][j] = 0.0;
-    Ui[j][j] = 1.0 / M[j][j];
-    for (int i = j - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int k = i + 1; k <= j; ++k) s = fma(M[i][k], Ui[k][j], s);
-      Ui[i][j] = -s / M[i][i];
-    }
-  }
-  __syncthreads();
-  double* Ai = Ainv + b * sAi;
-  for (int idx = tid; idx < nbs * nbs; idx += bd) {
-    int i = idx % nbs, j = idx / nbs;
-    double s = 0.0;
-    for (int k = i; k < nbs; ++k) s = fma(Ui[i][k], Li[k][j], s);
-    Ai[j * GJ_NB + i] = s;
-  }
-  if (tid == 0) { pivmin[b] = pmin; pivmax[b] = pmax; }
-}
 
 __global__ void k_gj_swap(double* A, long long sA, int lda, int n, int c0, int nbs,
                           const int* ipiv, long long sPiv) {
@@ -169,18 +81,11 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
   if (batch <= 0 || n <= 0) return VF_OK;
   if (batch > 65535) { set_error("inv_batched: batch too large"); return VF_EARG; }
   cudaStream_t st = (cudaStream_t)stream_;
+  ensure_pool();
   const int nb = GJ_NB;
-  double *Pg = nullptr, *Pw = nullptr, *Rw = nullptr, *Ai = nullptr;
+  double *Pw = nullptr, *Rw = nullptr, *Ai = nullptr;
   int* ipiv = nullptr;
   const long long sPw = (long long)n * nb;
-  const size_t smem_need = (size_t)n * nb * sizeof(double);
-  const int use_smem = smem_need <= 160 * 1024;
-  if (use_smem) {
-    VF_CUDA(cudaFuncSetAttribute(k_gj_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem_need));
-  } else {
-    VF_CUDA(cudaMallocAsync(&Pg, sizeof(double) * sPw * batch, st));
-  }
   VF_CUDA(cudaMallocAsync(&Pw, sizeof(double) * sPw * batch, st));
   VF_CUDA(cudaMallocAsync(&Rw, sizeof(double) * sPw * batch, st));
   VF_CUDA(cudaMallocAsync(&Ai, sizeof(double) * nb * nb * batch, st));
@@ -191,14 +96,16 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
   int rc = VF_OK;
   for (int c0 = 0; c0 < n && rc == VF_OK; c0 += nb) {
     const int nbs = n - c0 < nb ? n - c0 : nb;
-    size_t sm = use_smem ? (size_t)(n - c0) * nbs * sizeof(double) : 0;
-    k_gj_panel<<<batch, 256, sm, st>>>(A, sA, lda, n, c0, nbs, Pg, sPw, ipiv, n, Ai, nb * nb,
-                                       pivmin, pivmax, use_smem);
+    prof_push(st, "gj.panel");
+    rc = lu_panel(A, sA, lda, n, c0, nbs, batch, ipiv, n, Ai, nb * nb, pivmin, pivmax, st);
+    if (rc) break;
+    prof_push(st, "gj.swap+prep");
     k_gj_swap<<<dim3(cdiv(n, 128), batch), 128, 0, st>>>(A, sA, lda, n, c0, nbs, ipiv, n);
     k_gj_prep<<<dim3(cdiv(n, 32), cdiv(nbs, 8), batch), dim3(32, 8), 0, st>>>(A, sA, lda, n, c0,
                                                                                nbs, Pw, sPw);
     g_launches += 3;
     VF_LAUNCH_CHECK("gj panel/swap/prep");
+    prof_push(st, "gj.gemm_rw");
     vief_gemm_desc g{};
     // Rw (nbs x n, ld nb) = Ainv (nbs x nbs) * A[c0:c0+nbs, :]
     g.A = Ai; g.strideA = nb * nb; g.lda = nb;
@@ -208,6 +115,7 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
     rc = vief_dgemm_batched(&g, st);
     if (rc) break;
     // A -= Pw (n x nbs, ld n) * Rw (nbs x n, ld nb)
+    prof_push(st, "gj.gemm_update");
     vief_gemm_desc u{};
     u.A = Pw; u.strideA = sPw; u.lda = n;
     u.B = Rw; u.strideB = sPw; u.ldb = nb;
@@ -215,15 +123,17 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
     u.M = n; u.N = n; u.K = nbs; u.alpha = -1.0; u.beta = 1.0; u.batch = batch;
     rc = vief_dgemm_batched(&u, st);
     if (rc) break;
+    prof_push(st, "gj.copy");
     rc = vief_copy2d(Rw, sPw, nullptr, nb, A + c0, sA, nullptr, lda, nullptr, nbs, nullptr, n,
                      batch, st);
   }
+  prof_push(st, "gj.colswap");
   if (rc == VF_OK) {
     k_gj_colswap<<<dim3(cdiv(n, 128), batch), 128, 0, st>>>(A, sA, lda, n, ipiv, n);
     ++g_launches;
     VF_LAUNCH_CHECK("k_gj_colswap");
   }
-  if (Pg) cudaFreeAsync(Pg, st);
+  prof_flush(st);
   cudaFreeAsync(Pw, st);
   cudaFreeAsync(Rw, st);
   cudaFreeAsync(Ai, st);

@@ -4,6 +4,9 @@
 // Plus library-global error state.
 #include <cstdarg>
 #include <cstring>
+#include <map>
+#include <string>
+#include <vector>
 #include "common.cuh"
 #include "../../include/vief_b200.h"
 
@@ -104,9 +107,70 @@ __global__ void k_pad_identity(double* A, long long sA, int lda, const int* nb, 
   A[b * sA + (long long)j * lda + i] = (i == j) ? 1.0 : 0.0;
 }
 
+static bool g_prof = false;
+static std::map<std::string, std::pair<double, long long>> g_prof_acc;
+struct ProfEv { std::string name; cudaEvent_t e0, e1; };
+static std::vector<ProfEv> g_prof_pending;
+static int g_prof_open = -1;
+
+bool prof_on() { return g_prof; }
+static std::string g_prof_prefix;
+void prof_push(cudaStream_t st, const char* name) {
+  if (!g_prof) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  if (g_prof_open >= 0) g_prof_pending[g_prof_open].e1 = e;
+  ProfEv pe{g_prof_prefix + name, e, nullptr};
+  cudaEvent_t e2;
+  cudaEventCreate(&e2);
+  cudaEventRecord(e2, st);
+  pe.e0 = e2;
+  g_prof_pending.push_back(pe);
+  g_prof_open = (int)g_prof_pending.size() - 1;
+}
+void prof_flush(cudaStream_t st) {
+  if (!g_prof) return;
+  if (g_prof_open >= 0) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    g_prof_pending[g_prof_open].e1 = e;
+  }
+  cudaStreamSynchronize(st);
+  for (auto& pe : g_prof_pending) {
+    float ms = 0.f;
+    if (pe.e1) cudaEventElapsedTime(&ms, pe.e0, pe.e1);
+    auto& a = g_prof_acc[pe.name];
+    a.first += ms;
+    a.second += 1;
+    cudaEventDestroy(pe.e0);
+    if (pe.e1) cudaEventDestroy(pe.e1);
+  }
+  g_prof_pending.clear();
+  g_prof_open = -1;
+}
+
 }  // namespace vf
 
 using namespace vf;
+
+extern "C" void vief_prof_prefix(const char* p) { g_prof_prefix = p ? p : ""; }
+extern "C" void vief_prof_enable(int on) {
+  g_prof = on != 0;
+  g_prof_acc.clear();
+}
+extern "C" int vief_prof_report(char* buf, int len) {
+  std::string s;
+  char line[256];
+  for (auto& kv : g_prof_acc) {
+    snprintf(line, sizeof(line), "%-28s %10.3f ms  (%lld)\n", kv.first.c_str(), kv.second.first,
+             kv.second.second);
+    s += line;
+  }
+  snprintf(buf, len, "%s", s.c_str());
+  return (int)s.size();
+}
 
 extern "C" int vief_version(void) { return 1; }
 extern "C" const char* vief_last_error(void) { return g_err; }
@@ -197,3 +261,18 @@ extern "C" int vief_pad_identity(double* A, long long sA, int lda, const int* nb
   VF_LAUNCH_CHECK("k_pad_identity");
   return VF_OK;
 }
+
+namespace vf {
+void ensure_pool() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done = true;
+}
+}  // namespace vf

@@ -1,0 +1,18 @@
+// Cluster-parallel panel kernels (see panels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <algorithm>
+
+namespace vf {
+constexpr int PNB = 32;       // panel width (GJ block, ID block)
+constexpr int HSK = PNB + 8;  // sketch rows
+
+int lu_panel(const double* A, long long sA, int lda, int n, int c0, int nbs, int batch, int* ipiv,
+             long long sPiv, double* Ainv, long long sAi, double* pivmin, double* pivmax,
+             cudaStream_t st);
+int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* active,
+             const int* bsv, int J, int maxp, int count, double* Qw, long long sQ, int ldq,
+             double* Rt, cudaStream_t st);
+int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const int* active,
+                  const int* bsv, int J, int maxm, int count, int* swaps, cudaStream_t st);
+}  // namespace vf

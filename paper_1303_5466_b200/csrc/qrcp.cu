@@ -16,11 +16,12 @@
 //    pass over the trailing matrix per column:
 //       Y = Omega A (sketch, s = b+8 rows)
 //       per block of b = 32 columns:
-//         select b pivots by QRCP on the sketch (CTA per item, Y read-only,
-//            Gram-Schmidt basis + norm downdating)
-//         swap them to the front; panel QR by shifted CholeskyQR3
+//         select b pivots by QRCP on the sketch (cluster of CTAs per item,
+//            Y read-only, Gram-Schmidt basis + norm downdating; panels.cu)
+//         swap them to the front; Householder QR of the panel with explicit
+//            Q (cluster of CTAs per item, DSMEM reductions; panels.cu)
 //         W = Q^T A_trail (rows of R), A_trail -= Q W, column norms
-//         Y_trail -= (Y_blk R_blk^{-1}) W   (sketch downdate, no new sketch)
+//         Y_trail -= (Omega Q) W   (sketch downdate, no new sketch, no R^{-1})
 //       rank: the reference's rule in residual form — k is the first j whose
 //       largest residual column norm is <= eps * max_j ||A(:,j)|| (for exact
 //       QRCP this is exactly |R_jj| <= eps |R_00|), evaluated exactly inside
@@ -31,6 +32,7 @@
 #include <vector>
 #include <algorithm>
 #include "common.cuh"
+#include "panels.cuh"
 #include "../../include/vief_b200.h"
 
 namespace vf {
@@ -189,6 +191,7 @@ __global__ void k_group_max(int* k, int count, int group) {
 // blocked randomized path
 constexpr int HB = 32;       // block (panel) width
 constexpr int HS = HB + 8;   // sketch rows (oversampling 8)
+static_assert(HB == PNB && HS == HSK, "panel sizes must agree with panels.cuh");
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
   x ^= x >> 33; x *= 0xff51afd7ed558ccdULL; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ULL; x ^= x >> 33;
@@ -255,99 +258,6 @@ __global__ void k_block_setup(int J, const int* pv, const int* mv, int count, HS
   S.sact[b] = act ? HS : 0;
 }
 
-// select HB pivots from the sketch Y(:, J:m) by QRCP on the sketch.  Y is read
-// only: the chosen columns' residual directions are kept as an orthonormal
-// basis (classical Gram-Schmidt, twice) and all other columns' residual norms
-// are downdated by their projection on each new basis vector.
-__global__ void __launch_bounds__(256) k_sketch_select(const double* Yg, int ldy, long long sY,
-                                                       const int* mv, int J, HState S) {
-  extern __shared__ double sm[];
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (!S.active[b]) return;
-  const int m = mv[b];
-  const int n = m - J;
-  const int bs = S.bs[b];
-  if (bs <= 0) return;
-  double* nrm = sm;                 // n: current residual norm^2
-  double* nrm0 = nrm + n;           // n: original norm^2
-  __shared__ double Qb[HB][HS];     // chosen basis vectors
-  __shared__ double qv[HS];
-  __shared__ double redv[32];
-  __shared__ int redi[32];
-  __shared__ int sel[HB];
-  const double* Y = Yg + b * sY + (long long)J * ldy;
-  (void)S.ldtn;
-  for (int j = warp; j < n; j += 8) {
-    double s = 0.0;
-    for (int r = lane; r < HS; r += 32) s = fma(Y[(long long)j * ldy + r], Y[(long long)j * ldy + r], s);
-    s = warp_sum(s);
-    if (lane == 0) { nrm[j] = s; nrm0[j] = s; }
-  }
-  __syncthreads();
-  for (int i = 0; i < bs; ++i) {
-    double v = -1.0;
-    int iv = 0x7fffffff;
-    for (int j = tid; j < n; j += 256)
-      if (nrm[j] > v) { v = nrm[j]; iv = j; }
-    block_argmax(v, iv, redv, redi);
-    if (tid == 0) { sel[i] = iv; nrm[iv] = -1.0; }  // never chosen again
-    // q = (I - Qb Qb^T) y, twice, normalised  (warp 0)
-    if (warp == 0) {
-      double y0 = lane < HS ? Y[(long long)iv * ldy + lane] : 0.0;
-      double y1 = lane + 32 < HS ? Y[(long long)iv * ldy + lane + 32] : 0.0;
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int c = 0; c < i; ++c) {
-          double d = (lane < HS ? Qb[c][lane] * y0 : 0.0) + (lane + 32 < HS ? Qb[c][lane + 32] * y1 : 0.0);
-          d = warp_sum(d);
-          if (lane < HS) y0 -= d * Qb[c][lane];
-          if (lane + 32 < HS) y1 -= d * Qb[c][lane + 32];
-        }
-      }
-      double nn = warp_sum(y0 * y0 + y1 * y1);
-      double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-      if (lane < HS) { Qb[i][lane] = y0 * inv; qv[lane] = y0 * inv; }
-      if (lane + 32 < HS) { Qb[i][lane + 32] = y1 * inv; qv[lane + 32] = y1 * inv; }
-    }
-    __syncthreads();
-    // downdate all remaining norms
-    for (int j = warp; j < n; j += 8) {
-      double cur = nrm[j];
-      if (cur < 0.0) continue;
-      double d = 0.0;
-      for (int r = lane; r < HS; r += 32) d = fma(qv[r], Y[(long long)j * ldy + r], d);
-      d = warp_sum(d);
-      if (lane == 0) {
-        double nv = cur - d * d;
-        if (nv < 1e-12 * nrm0[j]) nv = fmax(nv, 0.0);  // cancellation floor
-        nrm[j] = nv;
-      }
-    }
-    __syncthreads();
-  }
-  // convert the selection into a sequence of swaps (dst = J+i, src position)
-  if (tid == 0) {
-    int mid[2 * HB + 2], mpos[2 * HB + 2];
-    int nm = 0;
-    for (int i = 0; i < bs; ++i) {
-      const int id = J + sel[i];
-      int src = id;
-      for (int t = 0; t < nm; ++t) if (mid[t] == id) src = mpos[t];
-      const int dst = J + i;
-      int at_dst = dst;
-      for (int t = 0; t < nm; ++t) if (mpos[t] == dst) at_dst = mid[t];
-      S.swaps[b * HB + i] = src;
-      // id at_dst moves to src; id moves to dst
-      bool f1 = false, f2 = false;
-      for (int t = 0; t < nm; ++t) {
-        if (mid[t] == at_dst) { mpos[t] = src; f1 = true; }
-        else if (mid[t] == id) { mpos[t] = dst; f2 = true; }
-      }
-      if (!f1 && at_dst != src) { mid[nm] = at_dst; mpos[nm] = src; ++nm; }
-      if (!f2 && id != dst) { mid[nm] = id; mpos[nm] = dst; ++nm; }
-    }
-  }
-}
-
 // apply the swap sequence to A (p rows), Y (HS rows), perm, and the norms.
 __global__ void k_apply_swaps(double* A, long long sA, int lda, double* Y, long long sY, int ldy,
                               int* perm, int ldperm, const int* pv, int J, HState S,
@@ -394,106 +304,6 @@ __global__ void k_apply_swaps(double* A, long long sA, int lda, double* Y, long 
       const int src = sw[i], dst = J + i;
       if (src != dst) { int t = pm[src]; pm[src] = pm[dst]; pm[dst] = t; }
     }
-  }
-}
-
-// Householder QR of the block panel P = A(:, J:J+bs) (p x bs, unpivoted: the
-// order comes from the sketch), explicit Q (dorg2r-style backward
-// accumulation) into Qw and R into S.Rt.  Rank-deficient panels are harmless
-// (tau = 0 / tiny R_jj).  One CTA per item; the panel lives in shared memory
-// when small, else in a global work copy (L2-resident).
-constexpr int PQ_THREADS = 256;
-__global__ void __launch_bounds__(PQ_THREADS) k_panel_qr(const double* A, long long sA, int lda,
-                                                         const int* pv, int J, HState S,
-                                                         double* Qw, long long sQ, int ldq,
-                                                         double* work, int use_smem) {
-  extern __shared__ double psm[];
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = PQ_THREADS / 32;
-  if (!S.active[b]) return;
-  const int bs = S.bs[b];
-  if (bs <= 0) return;
-  const int p = pv[b];
-  __shared__ double tau[HB], Rl[HB][HB + 1];
-  __shared__ double red[32];
-  __shared__ double s_beta, s_tau, s_sc;
-  const int ldp = use_smem ? p : ldq;
-  double* P = use_smem ? psm : work + b * sQ;
-  double* Q = use_smem ? psm + (long long)p * HB : Qw + b * sQ;
-  const double* Ab = A + b * sA + (long long)J * lda;
-  for (int idx = tid; idx < p * bs; idx += PQ_THREADS) {
-    int r = idx % p, c = idx / p;
-    P[(long long)c * ldp + r] = Ab[(long long)c * lda + r];
-  }
-  for (int idx = tid; idx < HB * HB; idx += PQ_THREADS) Rl[idx % HB][idx / HB] = 0.0;
-  __syncthreads();
-  for (int j = 0; j < bs; ++j) {
-    if (j >= p) { if (tid == 0) tau[j] = 0.0; continue; }
-    double* v = P + (long long)j * ldp;
-    double ss = 0.0;
-    for (int r = j + 1 + tid; r < p; r += PQ_THREADS) ss = fma(v[r], v[r], ss);
-    ss = block_sum(ss, red);
-    if (tid == 0) {
-      const double alpha = v[j];
-      const double xn = sqrt(ss);
-      if (xn == 0.0) { s_tau = 0.0; s_beta = alpha; s_sc = 0.0; }
-      else {
-        const double beta = -copysign(hypot(alpha, xn), alpha);
-        s_tau = (beta - alpha) / beta; s_beta = beta; s_sc = 1.0 / (alpha - beta);
-      }
-    }
-    __syncthreads();
-    const double tj = s_tau;
-    if (tj != 0.0) {
-      const double sc = s_sc;
-      for (int r = j + 1 + tid; r < p; r += PQ_THREADS) v[r] *= sc;
-    }
-    __syncthreads();
-    if (tid == 0) { tau[j] = tj; Rl[j][j] = s_beta; v[j] = 1.0; }
-    __syncthreads();
-    if (tj != 0.0) {
-      for (int l = j + 1 + warp; l < bs; l += NW) {
-        double* c = P + (long long)l * ldp;
-        double w = 0.0;
-        for (int r = j + lane; r < p; r += 32) w = fma(v[r], c[r], w);
-        w = warp_sum(w) * tj;
-        for (int r = j + lane; r < p; r += 32) c[r] = fma(-w, v[r], c[r]);
-      }
-    }
-    __syncthreads();
-    for (int l = j + 1 + tid; l < bs; l += PQ_THREADS) Rl[j][l] = P[(long long)l * ldp + j];
-    __syncthreads();
-  }
-  // Q = H_0 ... H_{bs-1} [I; 0]
-  for (int idx = tid; idx < p * bs; idx += PQ_THREADS) {
-    int r = idx % p, c = idx / p;
-    Q[(long long)c * ldp + r] = (r == c) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  for (int j = min(bs, p) - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj == 0.0) continue;
-    const double* v = P + (long long)j * ldp;  // v[j] == 1
-    for (int l = j + warp; l < bs; l += NW) {
-      double* c = Q + (long long)l * ldp;
-      double w = 0.0;
-      for (int r = j + lane; r < p; r += 32) w = fma(v[r], c[r], w);
-      w = warp_sum(w) * tj;
-      for (int r = j + lane; r < p; r += 32) c[r] = fma(-w, v[r], c[r]);
-    }
-    __syncthreads();
-  }
-  if (use_smem) {
-    double* Qo = Qw + b * sQ;
-    for (int idx = tid; idx < p * bs; idx += PQ_THREADS) {
-      int r = idx % p, c = idx / p;
-      Qo[(long long)c * ldq + r] = Q[(long long)c * ldp + r];
-    }
-  }
-  double* Rt = S.Rt + (long long)b * HB * HB;
-  for (int idx = tid; idx < HB * HB; idx += PQ_THREADS) {
-    int i = idx % HB, c = idx / HB;
-    Rt[c * HB + i] = Rl[i][c];
   }
 }
 
@@ -736,35 +546,46 @@ static int t_solve(const vief_id_desc* d, double* Rm, long long sR, int ldR, con
     VF_CUDA(cudaMemcpyAsync(nT, hm.data(), sizeof(int) * count, cudaMemcpyHostToDevice, st));
     VF_CUDA(cudaStreamSynchronize(st));
     if (nmax == 0) return VF_OK;
-    for (int blk = nblk - 1; blk >= 0; --blk) {
-      const int r0 = blk * TB, r1 = std::min(Kmax, r0 + TB);
-      int rc;
-      if (r1 < Kmax) {
+    // recursive back substitution over block rows [r0, r1): solve the lower
+    // half first, one large GEMM update of the upper half, then recurse on it
+    struct Rec {
+      const vief_id_desc* d; double* Rs; long long sRs; int Kmax; double* Dinv; int nblk;
+      double* tmp; int* nT; int nmax; cudaStream_t st;
+      int run(int b0, int b1) {  // block indices [b0, b1)
+        int rc;
+        const int r0 = b0 * TB, r1 = std::min(Kmax, b1 * TB);
+        if (b1 - b0 == 1) {
+          vief_gemm_desc h{};
+          h.A = Dinv + (long long)b0 * TB * TB; h.strideA = (long long)nblk * TB * TB; h.lda = TB;
+          h.B = d->T + r0; h.strideB = d->sT; h.ldb = d->ldT;
+          h.C = tmp; h.strideC = (long long)TB * d->maxm; h.ldc = TB;
+          h.M = r1 - r0; h.N = nmax; h.K = r1 - r0; h.Nb = nT;
+          h.alpha = 1.0; h.beta = 0.0; h.batch = d->count;
+          if ((rc = vief_dgemm_batched(&h, st))) return rc;
+          return vief_copy2d(tmp, (long long)TB * d->maxm, nullptr, TB, d->T + r0, d->sT, nullptr,
+                             d->ldT, nullptr, r1 - r0, nT, nmax, d->count, st);
+        }
+        const int bm = b0 + (b1 - b0) / 2, rm = bm * TB;
+        if ((rc = run(bm, b1))) return rc;
         vief_gemm_desc g{};
-        g.A = Rs + (long long)r1 * Kmax + r0; g.strideA = sRs; g.lda = Kmax;
-        g.B = d->T + r1; g.strideB = d->sT; g.ldb = d->ldT;
+        g.A = Rs + (long long)rm * Kmax + r0; g.strideA = sRs; g.lda = Kmax;
+        g.B = d->T + rm; g.strideB = d->sT; g.ldb = d->ldT;
         g.C = d->T + r0; g.strideC = d->sT; g.ldc = d->ldT;
-        g.M = r1 - r0; g.N = nmax; g.K = Kmax - r1; g.Nb = nT;
-        g.alpha = -1.0; g.beta = 1.0; g.batch = count;
+        g.M = rm - r0; g.N = nmax; g.K = r1 - rm; g.Nb = nT;
+        g.alpha = -1.0; g.beta = 1.0; g.batch = d->count;
         if ((rc = vief_dgemm_batched(&g, st))) return rc;
+        return run(b0, bm);
       }
-      vief_gemm_desc h{};
-      h.A = Dinv + (long long)blk * TB * TB; h.strideA = (long long)nblk * TB * TB; h.lda = TB;
-      h.B = d->T + r0; h.strideB = d->sT; h.ldb = d->ldT;
-      h.C = tmp; h.strideC = (long long)TB * d->maxm; h.ldc = TB;
-      h.M = r1 - r0; h.N = nmax; h.K = r1 - r0; h.Nb = nT;
-      h.alpha = 1.0; h.beta = 0.0; h.batch = count;
-      if ((rc = vief_dgemm_batched(&h, st))) return rc;
-      if ((rc = vief_copy2d(tmp, (long long)TB * d->maxm, nullptr, TB, d->T + r0, d->sT, nullptr,
-                            d->ldT, nullptr, r1 - r0, nT, nmax, count, st)))
-        return rc;
-    }
+    } rec{d, Rs, sRs, Kmax, Dinv, nblk, tmp, nT, nmax, st};
+    int rc = rec.run(0, nblk);
+    if (rc) return rc;
   }
   return VF_OK;
 }
 
 extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
+  ensure_pool();
   const int count = d->count;
   if (count <= 0) return VF_OK;
   if (count > 65535) { set_error("id: count > 65535"); return VF_EARG; }
@@ -783,6 +604,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   const bool small = !d->force_blocked && smem_small <= 220 * 1024;
   int* kdev = d->rank;
   if (small) {
+    prof_push(st, "id.small_qrcp");
     double* diag = buf.get<double>((size_t)maxm * count);
     VF_CUDA(cudaFuncSetAttribute(k_qrcp_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_small));
@@ -800,19 +622,14 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.cut = buf.get<double>(count); S.tn = buf.get<double>((size_t)maxm * count);
     S.Rt = buf.get<double>((size_t)HB * HB * count);
     S.Qw = buf.get<double>((size_t)maxp * HB * count);
-    const size_t pq_need = 2 * (size_t)maxp * HB * sizeof(double);
-    const int pq_use_smem = pq_need <= 200 * 1024;
-    const size_t pq_smem = pq_use_smem ? pq_need : 0;
-    S.work = pq_use_smem ? nullptr : buf.get<double>((size_t)maxp * HB * count);
-    if (pq_use_smem)
-      VF_CUDA(cudaFuncSetAttribute(k_panel_qr, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)pq_smem));
+    S.work = nullptr;
     S.Y = buf.get<double>((size_t)HS * maxm * count);
     S.Z = buf.get<double>((size_t)HS * HB * count);
     S.any = buf.get<int>(1);
     S.ldtn = maxm;
     double* Om = buf.get<double>((size_t)HS * maxp);
     if (!S.Y || !S.Qw || !Om || !S.any) { set_error("id: out of device memory (blocked)"); return VF_ENOMEM; }
+    prof_push(st, "id.init+sketch");
     const long long sY = (long long)HS * maxm, sQ = (long long)maxp * HB;
     k_iota<<<dim3(cdiv(maxm, 128), count), 128, 0, st>>>(d->perm, maxm, d->m, count);
     k_colnorms<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m,
@@ -833,25 +650,27 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       g.alpha = 1.0; g.beta = 0.0; g.batch = count;
       if ((rc = vief_dgemm_batched(&g, st))) return rc;
     }
-    const size_t sel_smem = 2 * (size_t)maxm * sizeof(double);
-    VF_CUDA(cudaFuncSetAttribute(k_sketch_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(sel_smem, 1024)));
     const int kcap = std::min(maxp, maxm);
     for (int J = 0; J < kcap; J += HB) {
+      prof_push(st, "id.setup+select");
       k_block_setup<<<cdiv(count, 128), 128, 0, st>>>(J, d->p, d->m, count, S);
-      k_sketch_select<<<count, 256, sel_smem, st>>>(S.Y, HS, sY, d->m, J, S);
+      ++g_launches;
+      if ((rc = sketch_select(S.Y, HS, sY, d->m, S.active, S.bs, J, maxm, count, S.swaps, st)))
+        return rc;
+      prof_push(st, "id.swaps");
       k_apply_swaps<<<dim3(cdiv(std::max(std::max(maxp, HS), J), 128), count), 128, 0, st>>>(
           d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S, Rm, sR, ldR);
       g_launches += 3;
       VF_LAUNCH_CHECK("id select/swap");
-      k_panel_qr<<<count, PQ_THREADS, pq_smem, st>>>(d->A, d->sA, d->lda, d->p, J, S, S.Qw, sQ,
-                                                     maxp, S.work, pq_use_smem);
-      ++g_launches;
-      VF_LAUNCH_CHECK("k_panel_qr");
+      prof_push(st, "id.panel_qr");
+      if ((rc = qr_panel(d->A, d->sA, d->lda, d->p, S.active, S.bs, J, maxp, count, S.Qw, sQ,
+                         maxp, S.Rt, st)))
+        return rc;
       k_store_rblock<<<count, 256, 0, st>>>(S, Rm, sR, ldR, J);
       ++g_launches;
       {  // W = Q^T A_trail -> R(J:J+bs, J+bs:m); columns start at J+bs per item: use J+HB
         // items with bs < HB have nrem = 0, so the fixed offset J+HB is exact for all active work
+        prof_push(st, "id.gemm_W");
         vief_gemm_desc w{};
         w.A = S.Qw; w.strideA = sQ; w.lda = maxp; w.transA = 1;
         w.B = d->A + (long long)(J + HB) * d->lda; w.strideB = d->sA; w.ldb = d->lda;
@@ -860,6 +679,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         w.alpha = 1.0; w.beta = 0.0; w.batch = count;
         if ((rc = vief_dgemm_batched(&w, st))) return rc;
         // A_trail -= Q W
+        prof_push(st, "id.gemm_update");
         vief_gemm_desc u{};
         u.A = S.Qw; u.strideA = sQ; u.lda = maxp;
         u.B = Rm + (long long)(J + HB) * ldR + J; u.strideB = sR; u.ldb = ldR;
@@ -868,6 +688,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         u.alpha = -1.0; u.beta = 1.0; u.batch = count;
         if ((rc = vief_dgemm_batched(&u, st))) return rc;
         // sketch downdate: Y_trail -= (Omega Q) W  (= Omega A_trail after the update)
+        prof_push(st, "id.sketch_downdate");
         vief_gemm_desc z{};
         z.A = Om; z.strideA = 0; z.lda = HS;
         z.B = S.Qw; z.strideB = sQ; z.ldb = maxp;
@@ -883,6 +704,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         y.alpha = -1.0; y.beta = 1.0; y.batch = count;
         if ((rc = vief_dgemm_batched(&y, st))) return rc;
       }
+      prof_push(st, "id.norms+rank");
       k_colnorms<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m,
                                                              S.active, J + HB, S.tn, maxm);
       VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
@@ -890,6 +712,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
       g_launches += 3;
       VF_LAUNCH_CHECK("id rank");
+      prof_push(st, "id.hostsync");
       int any = 0;
       VF_CUDA(cudaMemcpyAsync(&any, S.any, sizeof(int), cudaMemcpyDeviceToHost, st));
       VF_CUDA(cudaStreamSynchronize(st));
@@ -903,5 +726,8 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     VF_CUDA(cudaStreamSynchronize(st));
     for (int b = 0; b < count; ++b) Kmax = std::max(Kmax, hk[b]);
   }
-  return t_solve(d, Rm, sR, ldR, kdev, Kmax, buf, st);
+  prof_push(st, "id.tsolve");
+  int rct = t_solve(d, Rm, sR, ldR, kdev, Kmax, buf, st);
+  prof_flush(st);
+  return rct;
 }

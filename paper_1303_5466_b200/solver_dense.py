@@ -40,6 +40,34 @@ _I32 = torch.int32
 _F64 = torch.float64
 
 
+class StageTimer:
+    """Optional per-(stage, level) CUDA-event timing of the factor/solve
+    sweeps (set solver_dense.TIMER = StageTimer() to enable)."""
+
+    def __init__(self):
+        self.events = []
+
+    def mark(self, tag):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.events.append((tag, e))
+
+    def report(self):
+        torch.cuda.synchronize()
+        out = []
+        for (t0, e0), (t1, e1) in zip(self.events, self.events[1:]):
+            out.append((t1, e0.elapsed_time(e1)))
+        return out
+
+
+TIMER = None
+
+
+def _mark(tag):
+    if TIMER is not None:
+        TIMER.mark(tag)
+
+
 def _even(x):
     return int(x) + (int(x) & 1)
 
@@ -365,8 +393,11 @@ def compress_outer(spec, grid, tree, eps, opts, quad=PLAIN, spill=None):
     compatibility; every block stays in HBM."""
     H = Hss2dMatrix(spec, grid, tree, eps, opts, quad)
     pad = opts.resolved_proxy_layers(spec)
+    _mark("compress:start")
     for L in reversed(H.levels):
+        _lib.prof_prefix(f"L{L.lv:02d}.")
         _compress_level(H, L, pad, opts.seed)
+        _mark(f"compress:{L.lv}")
     return H
 
 
@@ -502,8 +533,11 @@ def invert_dense_block(H, spill=None, free_source=False):
     """Fine-to-coarse telescoping inversion, one batch per level
     (solver_dense.py:332-368).  `free_source` drops D/B once consumed."""
     inv = DenseBlockInverse(H)
+    _mark("invert:start")
     for L in reversed(H.levels):
+        _lib.prof_prefix(f"L{L.lv:02d}.")
         _invert_level(inv, L)
+        _mark(f"invert:{L.lv}")
         if free_source:
             if L.leaf:
                 L.D = None
