@@ -1,0 +1,366 @@
+"""Benchmark: dense-block recursive-skeletonization factor + solve at N = 1024^2.
+
+Metric (BASELINE.json): factor & solve unknowns/sec at N=1024^2, tol 1e-10.
+One step = build_tree + compress_outer + invert_dense_block (the factor) and a
+256-RHS solve, on config 4 (Laplace log-kernel VIE, float64, leaf 64,
+eps 1e-10, BASELINE bump on the rows, cell-integral diagonal; synthetic
+seeded N(0,1) right-hand sides).  value = N / step time, RHS resident in HBM.
+e2e = the same step through the public API (compress_inverse + apply) with the
+256 RHS copied from pinned host memory and the solution copied back.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the CPU oracle port (oracle/hssd.py: the reference's
+algorithm on scipy/OpenBLAS, all host threads) on a bounded sample of the same
+workload (the 128^2 member of the family, factor + 256-RHS solve per step).
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "factor & solve unknowns/sec at N=1024^2, tol 1e-10"
+UNIT = "unknowns/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--nrhs", type=int, default=256)
+    ap.add_argument("--cpu-n", type=int, default=128, help="oracle sample grid side")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def _config(n, nrhs, world):
+    return {"workload": f"c4: Laplace log-kernel VIE {n}x{n} (N={n*n}), float64, leaf 64, "
+                        f"eps 1e-10, factor + {nrhs}-RHS solve",
+            "n_side": n, "N": n * n, "nrhs": nrhs, "leaf": 64, "eps": 1e-10,
+            "kernel": "laplace2d (1/2pi) log r on [-1,1]^2, b = (pi/2)(1+0.5 exp(-|x|^2/0.08)) "
+                      "rows, c = 1, cell-integral diagonal",
+            "l2": "inputs and factors (~60 GB) far exceed the 126 MB L2 between steps",
+            "parallelism": "replicas" if world > 1 else "single GPU"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU oracle port)
+
+def _oracle_step(n, nrhs, seed=0):
+    import oracle.hssd as O
+    P = O.Problem(n, "laplace2d", 0.0, ("one", ()), ("centre_bump", (("scale", math.pi / 2),)),
+                  ("one", ()), "cell")
+    rng = np.random.default_rng(seed)
+    f = rng.standard_normal((n * n, nrhs))
+    t0 = time.perf_counter()
+    tree = O.make_tree(n, 64)
+    H = O.compress(P, tree, 1e-10, 2)
+    inv = O.invert(H)
+    x = O.apply_inverse(inv, f)
+    t1 = time.perf_counter()
+    return t1 - t0, x
+
+
+def _cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(a):
+    rank, world, _ = _dist()
+    if rank != 0:
+        return
+    cores = _cpu_threads()
+    for _ in range(a.warmup):
+        _oracle_step(a.cpu_n, a.nrhs)
+    times = [_oracle_step(a.cpu_n, a.nrhs)[0] for _ in range(a.steps)]
+    t = sum(times) / len(times)
+    v = a.cpu_n ** 2 / t
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": _config(a.n, a.nrhs, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"oracle/hssd.py (reference algorithm on scipy "
+                                       f"{__import__('scipy').__version__}/OpenBLAS, "
+                                       f"{cores} threads) full factor + {a.nrhs}-RHS solve of "
+                                       f"the {a.cpu_n}^2 member of the same problem family per "
+                                       f"step; unknowns/s falls as N^-1/2 with size, so this "
+                                       f"overstates the CPU at 1024^2"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+class Clocks:
+    def __init__(self, gpu):
+        self.path = f"/tmp/vief_clocks_{os.getpid()}.csv"
+        self.proc = None
+        self.gpu = gpu
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def _algorithmic_work(H):
+    """SURVEY §8(d) per-box formulas evaluated with this run's m, k, p."""
+    id_fl = lu_fl = 0.0
+    solve_bytes = 0.0
+    solve_fl = 0.0
+    sym = H.symmetric
+    for L in H.levels:
+        m = L.m.astype(np.float64)
+        if L.lv == 0:
+            lu_fl += float(((2.0 / 3.0) * m ** 3).sum())
+            solve_bytes += float((8.0 * m * m).sum())
+            solve_fl += float((2.0 * m * m).sum())
+            continue
+        k = L.k.astype(np.float64)
+        p = L.p.astype(np.float64)
+        one = 4 * p * m * k - 2 * (p + m) * k * k + (4.0 / 3.0) * k ** 3 + k * k * (m - k)
+        id_fl += float(one.sum()) * (1 if sym else 2)
+        lu_fl += float(((2.0 / 3.0) * m ** 3 + 2 * m * m * k + 2 * k * k * (m - k)
+                        + (2.0 / 3.0) * k ** 3 + 2 * k ** 3).sum())
+        solve_bytes += float((8.0 * (2 * m * m + 2 * k * k + 2 * k * (m - k))).sum())
+        solve_fl += float((4 * m * m + 4 * k * k + 6 * k * (m - k)).sum())
+    return id_fl, lu_fl, solve_bytes, solve_fl
+
+
+def run_ours(a):
+    import torch
+    rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    from paper_1303_5466_b200 import (CELL, Grid, KernelSpec, SolverOptions, build_tree,
+                                      make_field, _lib)
+    from paper_1303_5466_b200 import solver_dense as sd
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+
+    n, nrhs = a.n, a.nrhs
+    N = n * n
+    spec = KernelSpec("laplace2d", b_field=make_field("centre_bump", scale=math.pi / 2),
+                      c_field=make_field("one"))
+    grid = Grid(n)
+    opts = SolverOptions(eps=1e-10, leaf_size=64, k_cut=None)
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    F = torch.randn((N, nrhs), dtype=torch.float64, device="cuda", generator=gen)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    stage = {}
+
+    def step(record=False):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        tree = build_tree(grid, 64)
+        H = sd.compress_outer(spec, grid, tree, 1e-10, opts, CELL)
+        ev[1].record()
+        inv = sd.invert_dense_block(H)
+        ev[2].record()
+        X = inv.apply(F)
+        ev[3].record()
+        if record:
+            torch.cuda.synchronize()
+            stage.setdefault("compress", []).append(ev[0].elapsed_time(ev[1]))
+            stage.setdefault("invert", []).append(ev[1].elapsed_time(ev[2]))
+            stage.setdefault("solve", []).append(ev[2].elapsed_time(ev[3]))
+        return H, inv, X
+
+    for _ in range(a.warmup):
+        H, inv, X = step()
+        del H, inv, X
+    barrier()
+    L0 = _lib.launch_count()
+    with Clocks(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record()
+        for _ in range(a.steps):
+            H, inv, X = step(record=True)
+            if _ < a.steps - 1:
+                del H, inv, X
+        e1.record()
+        barrier()
+    launches = _lib.launch_count() - L0
+    ms = e0.elapsed_time(e1) / a.steps
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * N / (ms / 1e3)
+
+    # residual check of the last step (approximate residual of the paper, E)
+    v = F[:, :4]
+    r = (v - H.matvec(X[:, :4])).norm() / v.norm()
+    id_fl, lu_fl, sbytes, sfl = _algorithmic_work(H)
+    t_c = statistics.mean(stage["compress"]) / 1e3
+    t_i = statistics.mean(stage["invert"]) / 1e3
+    t_s = statistics.mean(stage["solve"]) / 1e3
+    peak_fp64 = 37.1e12   # measured DMMA issue rate (profiles/r01_fp64_peak.txt)
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm = float(peaks["hbm_gbs"]) * 1e9
+    except Exception:
+        hbm = 6.65e12
+    sfl_all = sfl * nrhs
+    roof_solve = max(sbytes / hbm, sfl_all / peak_fp64)
+    stages = {
+        "id (compress_outer)": {"bound": "tensor", "achieved": id_fl / t_c / 1e12,
+                                "peak": peak_fp64 / 1e12, "unit": "TFLOP/s",
+                                "frac": id_fl / t_c / peak_fp64, "algorithmic_flops": id_fl,
+                                "seconds": t_c},
+        "lu_schur (invert_dense_block)": {"bound": "tensor", "achieved": lu_fl / t_i / 1e12,
+                                          "peak": peak_fp64 / 1e12, "unit": "TFLOP/s",
+                                          "frac": lu_fl / t_i / peak_fp64,
+                                          "algorithmic_flops": lu_fl, "seconds": t_i},
+        f"solve ({nrhs} rhs)": {"bound": "tensor" if sfl_all / peak_fp64 > sbytes / hbm else "hbm",
+                                "achieved": sfl_all / t_s / 1e12, "peak": peak_fp64 / 1e12,
+                                "unit": "TFLOP/s", "frac": roof_solve / t_s,
+                                "algorithmic_flops": sfl_all, "factor_bytes": sbytes,
+                                "seconds": t_s},
+    }
+    dom = max(stages, key=lambda s: stages[s]["seconds"])
+    roof = dict(stages[dom])
+    roof = {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
+            "unit": roof["unit"], "frac": roof["frac"], "traffic": None, "stage": dom,
+            "peak_source": "measured DMMA mma.sync.m8n8k4.f64 issue rate 37.1 TFLOP/s "
+                           "(cuBLAS DGEMM 35.5); MEASURED_PEAKS.json has no FP64 entry"}
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": _config(n, nrhs, world),
+           "factor_s": t_c + t_i, "solve_s": t_s,
+           "factor_unknowns_per_s": N / (t_c + t_i),
+           "solve_unknown_rhs_per_s": N * nrhs / t_s,
+           "approx_residual_E": float(r), "max_rank": int(max(L.kmax for L in H.levels if L.lv)),
+           "factor_bytes": inv.nbytes(), "roofline": roof, "roofline_stages": stages,
+           "gpu_launches": int(launches)}
+    del H, inv, X
+    torch.cuda.empty_cache()
+    out["clocks"] = clk.summary()
+
+    # e2e through the public API with host buffers
+    if not a.no_e2e:
+        Fh = F.cpu().pin_memory()
+        Xh = torch.empty_like(Fh).pin_memory()
+
+        def e2e_step():
+            inv2 = compress_inverse(spec, grid, eps=1e-10, opts=opts, quad=CELL)
+            Xd = inv2.apply(Fh.to("cuda", non_blocking=True))
+            Xh.copy_(Xd, non_blocking=True)
+            torch.cuda.synchronize()
+            del inv2, Xd
+
+        for _ in range(a.warmup):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            e2e_step()
+        barrier()
+        te = (time.perf_counter() - t0) / a.steps
+        if dist is not None:
+            t = torch.tensor([te], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        out["e2e"] = {"value": world * N / te, "unit": UNIT, "h2d_bytes_per_step": int(N * nrhs * 8),
+                      "d2h_bytes_per_step": int(N * nrhs * 8), "ms_per_step": te * 1e3,
+                      "api": "solver_compressed.compress_inverse(k_cut=None) + .apply(pinned host "
+                             "RHS -> device) + device->pinned host copy of the solution"}
+
+    # CPU baseline (oracle port), rank 0, single GPU only
+    if rank == 0 and world == 1 and not a.no_cpu:
+        t, _ = _oracle_step(a.cpu_n, a.nrhs)
+        cores = _cpu_threads()
+        out["cpu_baseline"] = {"value": a.cpu_n ** 2 / t, "unit": UNIT, "cores": cores,
+                               "kind": "port",
+                               "sample": f"oracle/hssd.py at {a.cpu_n}^2 (same problem family, "
+                                         f"leaf 64, eps 1e-10), factor + {nrhs}-RHS solve, "
+                                         f"{t:.1f} s on {cores} threads; CPU unknowns/s falls "
+                                         f"as N^-1/2, so this overstates the CPU at 1024^2"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

@@ -2,16 +2,22 @@
 // Gauss-Jordan), replacing lu_factor_checked + lu_solve(., I)
 // (dense_core.py:222-230, solver_dense.py:361-367).
 //
-// Step s over block column [c0, c0+nb):
-//   1. lu_panel     (cluster of CTAs / item, panels.cu): LU with partial pivoting of the panel rows
-//      c0..n-1 (a copy in distributed shared memory), pivot rows, |U_jj| min/max
-//      (the reference's singularity test reads the same U diagonal), and
-//      A11^{-1} = U11^{-1} L11^{-1}.
-//   2. k_gj_swap    apply the nb row interchanges to all n columns.
-//   3. k_gj_prep    Pw = panel with pivot rows zeroed; panel := [0; I; 0].
-//   4. DMMA GEMM    Rw = A11^{-1} * A[pivot rows, :]
-//   5. DMMA GEMM    A -= Pw * Rw           (the 2 n^2 nb flops of the step)
-//   6. copy         A[pivot rows, :] = Rw
+// Two-level blocking.  Outer block columns of NBO = 128; inside each, inner
+// panels of 32:
+//   inner step on [c0, c0+32) (restricted to the outer block's columns):
+//     1. lu_panel  (cluster of CTAs per item, panels.cu): partial-pivoting LU
+//        of rows c0..n-1 -> pivots, |U_jj| min/max (the reference's
+//        singularity test reads the same U diagonal), A11^{-1}
+//     2. swap the 32 pivot rows inside the outer block columns
+//     3. Pw = panel with pivot rows zeroed; panel := [0; I; 0]
+//     4. Rw = A11^{-1} * A[pivot rows, block cols]            (DMMA GEMM)
+//     5. A[:, block cols] -= Pw * Rw                           (DMMA GEMM)
+//     6. A[pivot rows, block cols] = Rw
+//   outer step: the block columns now hold X = [.. -P A11^{-1} ..; A11^{-1}]
+//     (128 x 128 pivot block inverse).  Apply the 128 row swaps to the other
+//     columns, save their pivot rows R and zero them, then
+//        A[:, other] += X * R                (DMMA GEMM, K = 128)
+//     which is the Gauss-Jordan update of all other columns at once.
 // Finally columns are interchanged in reverse pivot order.  The pivots are the
 // partial-pivoting pivots of getrf (the trailing Schur complements coincide).
 #include <vector>
@@ -22,18 +28,20 @@
 namespace vf {
 extern long long g_launches;
 
-constexpr int GJ_NB = 32;
+constexpr int GJ_NB = 32;    // inner panel
+constexpr int GJ_NBO = 128;  // outer block
 
-__global__ void k_gj_swap(double* A, long long sA, int lda, int n, int c0, int nbs,
+// apply row interchanges ipiv[s0..s1) (in order) to columns [col0, col1) of A
+__global__ void k_gj_swap(double* A, long long sA, int lda, int col0, int col1, int s0, int s1,
                           const int* ipiv, long long sPiv) {
   const int b = blockIdx.y;
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= n) return;
+  const int col = col0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= col1) return;
   double* a = A + b * sA + (long long)col * lda;
   const int* pv = ipiv + b * sPiv;
-  for (int s = 0; s < nbs; ++s) {
-    int r = pv[c0 + s];
-    if (r != c0 + s) { double t = a[c0 + s]; a[c0 + s] = a[r]; a[r] = t; }
+  for (int s = s0; s < s1; ++s) {
+    int r = pv[s];
+    if (r != s) { double t = a[s]; a[s] = a[r]; a[r] = t; }
   }
 }
 
@@ -48,6 +56,20 @@ __global__ void k_gj_prep(double* A, long long sA, int lda, int n, int c0, int n
   const double v = *a;
   Pw[b * sP + (long long)j * n + i] = pivrow ? 0.0 : v;
   *a = pivrow ? ((i - c0 == j) ? 1.0 : 0.0) : 0.0;
+}
+
+// outer prep: R(r, j) = A(C0 + r, j) for r < NB, columns outside [C0, C0+NB)
+// (zero inside), and zero those pivot-row entries of A
+__global__ void k_gj_outer_prep(double* A, long long sA, int lda, int n, int C0, int NB, double* R,
+                                long long sR, int ldr) {
+  const int b = blockIdx.z;
+  const int r = blockIdx.x * 32 + threadIdx.x;
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  if (r >= NB || j >= n) return;
+  double* a = A + b * sA + (long long)j * lda + C0 + r;
+  const bool inblock = j >= C0 && j < C0 + NB;
+  R[b * sR + (long long)j * ldr + r] = inblock ? 0.0 : *a;
+  if (!inblock) *a = 0.0;
 }
 
 __global__ void k_gj_colswap(double* A, long long sA, int lda, int n, const int* ipiv,
@@ -82,50 +104,81 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
   if (batch > 65535) { set_error("inv_batched: batch too large"); return VF_EARG; }
   cudaStream_t st = (cudaStream_t)stream_;
   ensure_pool();
-  const int nb = GJ_NB;
-  double *Pw = nullptr, *Rw = nullptr, *Ai = nullptr;
+  const int nb = GJ_NB, NBO = GJ_NBO;
+  double *Pw = nullptr, *Rw = nullptr, *Ai = nullptr, *Xw = nullptr, *Ro = nullptr;
   int* ipiv = nullptr;
   const long long sPw = (long long)n * nb;
+  const long long sRw = (long long)nb * NBO;
+  const long long sX = (long long)n * NBO;
   VF_CUDA(cudaMallocAsync(&Pw, sizeof(double) * sPw * batch, st));
-  VF_CUDA(cudaMallocAsync(&Rw, sizeof(double) * sPw * batch, st));
+  VF_CUDA(cudaMallocAsync(&Rw, sizeof(double) * sRw * batch, st));
   VF_CUDA(cudaMallocAsync(&Ai, sizeof(double) * nb * nb * batch, st));
+  VF_CUDA(cudaMallocAsync(&Xw, sizeof(double) * sX * batch, st));
+  VF_CUDA(cudaMallocAsync(&Ro, sizeof(double) * sX * batch, st));
   VF_CUDA(cudaMallocAsync(&ipiv, sizeof(int) * n * batch, st));
   k_fill<<<cdiv(batch, 256), 256, 0, st>>>(pivmin, batch, INFINITY);
   k_fill<<<cdiv(batch, 256), 256, 0, st>>>(pivmax, batch, 0.0);
   g_launches += 2;
   int rc = VF_OK;
-  for (int c0 = 0; c0 < n && rc == VF_OK; c0 += nb) {
-    const int nbs = n - c0 < nb ? n - c0 : nb;
-    prof_push(st, "gj.panel");
-    rc = lu_panel(A, sA, lda, n, c0, nbs, batch, ipiv, n, Ai, nb * nb, pivmin, pivmax, st);
+  for (int C0 = 0; C0 < n && rc == VF_OK; C0 += NBO) {
+    const int NB = n - C0 < NBO ? n - C0 : NBO;
+    // ---- inner steps restricted to block columns [C0, C0+NB)
+    for (int c0 = C0; c0 < C0 + NB && rc == VF_OK; c0 += nb) {
+      const int nbs = C0 + NB - c0 < nb ? C0 + NB - c0 : nb;
+      prof_push(st, "gj.panel");
+      rc = lu_panel(A, sA, lda, n, c0, nbs, batch, ipiv, n, Ai, nb * nb, pivmin, pivmax, st);
+      if (rc) break;
+      prof_push(st, "gj.inner");
+      k_gj_swap<<<dim3(cdiv(NB, 128), batch), 128, 0, st>>>(A, sA, lda, C0, C0 + NB, c0, c0 + nbs,
+                                                            ipiv, n);
+      k_gj_prep<<<dim3(cdiv(n, 32), cdiv(nbs, 8), batch), dim3(32, 8), 0, st>>>(A, sA, lda, n, c0,
+                                                                                 nbs, Pw, sPw);
+      g_launches += 2;
+      VF_LAUNCH_CHECK("gj swap/prep");
+      vief_gemm_desc g{};  // Rw (nbs x NB, ld nb) = Ainv * A[c0:c0+nbs, C0:C0+NB]
+      g.A = Ai; g.strideA = nb * nb; g.lda = nb;
+      g.B = A + (long long)C0 * lda + c0; g.strideB = sA; g.ldb = lda;
+      g.C = Rw; g.strideC = sRw; g.ldc = nb;
+      g.M = nbs; g.N = NB; g.K = nbs; g.alpha = 1.0; g.beta = 0.0; g.batch = batch;
+      if ((rc = vief_dgemm_batched(&g, st))) break;
+      vief_gemm_desc u{};  // A[:, C0:C0+NB] -= Pw * Rw
+      u.A = Pw; u.strideA = sPw; u.lda = n;
+      u.B = Rw; u.strideB = sRw; u.ldb = nb;
+      u.C = A + (long long)C0 * lda; u.strideC = sA; u.ldc = lda;
+      u.M = n; u.N = NB; u.K = nbs; u.alpha = -1.0; u.beta = 1.0; u.batch = batch;
+      if ((rc = vief_dgemm_batched(&u, st))) break;
+      rc = vief_copy2d(Rw, sRw, nullptr, nb, A + (long long)C0 * lda + c0, sA, nullptr, lda,
+                       nullptr, nbs, nullptr, NB, batch, st);
+    }
     if (rc) break;
-    prof_push(st, "gj.swap+prep");
-    k_gj_swap<<<dim3(cdiv(n, 128), batch), 128, 0, st>>>(A, sA, lda, n, c0, nbs, ipiv, n);
-    k_gj_prep<<<dim3(cdiv(n, 32), cdiv(nbs, 8), batch), dim3(32, 8), 0, st>>>(A, sA, lda, n, c0,
-                                                                               nbs, Pw, sPw);
+    if (NB == n) continue;  // single block: nothing outside it
+    // ---- outer update of all other columns
+    prof_push(st, "gj.outer_prep");
+    if (C0 > 0)
+      k_gj_swap<<<dim3(cdiv(C0, 128), batch), 128, 0, st>>>(A, sA, lda, 0, C0, C0, C0 + NB, ipiv,
+                                                            n);
+    if (n - C0 - NB > 0)
+      k_gj_swap<<<dim3(cdiv(n - C0 - NB, 128), batch), 128, 0, st>>>(A, sA, lda, C0 + NB, n, C0,
+                                                                     C0 + NB, ipiv, n);
+    k_gj_outer_prep<<<dim3(cdiv(NB, 32), cdiv(n, 8), batch), dim3(32, 8), 0, st>>>(
+        A, sA, lda, n, C0, NB, Ro, sX, NBO);
     g_launches += 3;
-    VF_LAUNCH_CHECK("gj panel/swap/prep");
-    prof_push(st, "gj.gemm_rw");
-    vief_gemm_desc g{};
-    // Rw (nbs x n, ld nb) = Ainv (nbs x nbs) * A[c0:c0+nbs, :]
-    g.A = Ai; g.strideA = nb * nb; g.lda = nb;
-    g.B = A + c0; g.strideB = sA; g.ldb = lda;
-    g.C = Rw; g.strideC = sPw; g.ldc = nb;
-    g.M = nbs; g.N = n; g.K = nbs; g.alpha = 1.0; g.beta = 0.0; g.batch = batch;
-    rc = vief_dgemm_batched(&g, st);
-    if (rc) break;
-    // A -= Pw (n x nbs, ld n) * Rw (nbs x n, ld nb)
+    VF_LAUNCH_CHECK("gj outer prep");
+    if ((rc = vief_copy2d(A + (long long)C0 * lda, sA, nullptr, lda, Xw, sX, nullptr, n, nullptr,
+                          n, nullptr, NB, batch, st)))
+      break;
     prof_push(st, "gj.gemm_update");
-    vief_gemm_desc u{};
-    u.A = Pw; u.strideA = sPw; u.lda = n;
-    u.B = Rw; u.strideB = sPw; u.ldb = nb;
-    u.C = A; u.strideC = sA; u.ldc = lda;
-    u.M = n; u.N = n; u.K = nbs; u.alpha = -1.0; u.beta = 1.0; u.batch = batch;
-    rc = vief_dgemm_batched(&u, st);
-    if (rc) break;
-    prof_push(st, "gj.copy");
-    rc = vief_copy2d(Rw, sPw, nullptr, nb, A + c0, sA, nullptr, lda, nullptr, nbs, nullptr, n,
-                     batch, st);
+    for (int side = 0; side < 2; ++side) {
+      const int j0 = side == 0 ? 0 : C0 + NB;
+      const int nj = side == 0 ? C0 : n - C0 - NB;
+      if (nj <= 0) continue;
+      vief_gemm_desc u{};  // A[:, j0:j0+nj] += Xw * Ro[:, j0:j0+nj]
+      u.A = Xw; u.strideA = sX; u.lda = n;
+      u.B = Ro + (long long)j0 * NBO; u.strideB = sX; u.ldb = NBO;
+      u.C = A + (long long)j0 * lda; u.strideC = sA; u.ldc = lda;
+      u.M = n; u.N = nj; u.K = NB; u.alpha = 1.0; u.beta = 1.0; u.batch = batch;
+      if ((rc = vief_dgemm_batched(&u, st))) break;
+    }
   }
   prof_push(st, "gj.colswap");
   if (rc == VF_OK) {
@@ -137,6 +190,8 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
   cudaFreeAsync(Pw, st);
   cudaFreeAsync(Rw, st);
   cudaFreeAsync(Ai, st);
+  cudaFreeAsync(Xw, st);
+  cudaFreeAsync(Ro, st);
   cudaFreeAsync(ipiv, st);
   return rc;
 }

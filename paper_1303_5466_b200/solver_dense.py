@@ -334,6 +334,7 @@ def _compress_level(H, L, pad, seed):
         return
     # proxy + near sources and the ID matrices (solver_dense.py:250-263)
     p, pmax, src_xy, src_g = _level_sources(H, L, pad)
+    L.p = p
     g = H.group
     count = nb * g
     ldA = _even(pmax)
