@@ -15,8 +15,7 @@
 namespace vf {
 extern long long g_launches;
 
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, PAD = 4;
-constexpr int LDS_A = BM + PAD, LDS_B = BN + PAD;
+constexpr int BK = 16, STAGES = 3, PAD = 4;
 
 struct GemmItem {
   const double* A; const double* B; double* C; int M, N, K;
@@ -33,66 +32,85 @@ __device__ __forceinline__ GemmItem gemm_item(const vief_gemm_desc& d, int b) {
   return it;
 }
 
-// load one BKxBM tile of op(A) into As[k][m]
-__device__ __forceinline__ void load_a(double* As, const double* A, int lda, int trans,
-                                       int m0, int k0, int M, int K, int tid) {
+// load one BK x BMT tile of op(A) into As[k][m] (row stride BMT + PAD)
+template <int BMT>
+__device__ __forceinline__ void load_a(double* As, const double* A, int lda, int trans, int m0,
+                                       int k0, int M, int K, int tid) {
+  constexpr int LD = BMT + PAD, KQ = 128 / BMT, N_IT = BMT * BK / 128;
   if (!trans) {  // A(m,k) = A[k*lda + m], contiguous in m
-    int m = tid & 63, kq = tid >> 6;
+    const int m = tid % BMT, kq = tid / BMT;
+    const int gm = m0 + m;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int k = kq + 2 * i;
-      int gm = m0 + m, gk = k0 + k;
-      bool v = gm < M && gk < K;
-      cp_async8(As + k * LDS_A + m, v ? A + (long long)gk * lda + gm : A, v);
+    for (int i = 0; i < N_IT; ++i) {
+      const int k = kq + KQ * i, gk = k0 + k;
+      const bool v = gm < M && gk < K;
+      cp_async8(As + k * LD + m, v ? A + (long long)gk * lda + gm : A, v);
     }
   } else {       // op(A)(m,k) = A[m*lda + k], contiguous in k
-    int k = tid & 15, mq = tid >> 4;
+    const int k = tid % BK, mq = tid / BK;
+    const int gk = k0 + k;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int m = mq + 8 * i;
-      int gm = m0 + m, gk = k0 + k;
-      bool v = gm < M && gk < K;
-      cp_async8(As + k * LDS_A + m, v ? A + (long long)gm * lda + gk : A, v);
+    for (int i = 0; i < N_IT; ++i) {
+      const int m = mq + 8 * i, gm = m0 + m;
+      const bool v = gm < M && gk < K;
+      cp_async8(As + k * LD + m, v ? A + (long long)gm * lda + gk : A, v);
     }
   }
 }
 
-// load one BKxBN tile of op(B) into Bs[k][n]
-__device__ __forceinline__ void load_b(double* Bs, const double* B, int ldb, int trans,
-                                       int n0, int k0, int N, int K, int tid) {
+// load one BK x BNT tile of op(B) into Bs[k][n]
+template <int BNT>
+__device__ __forceinline__ void load_b(double* Bs, const double* B, int ldb, int trans, int n0,
+                                       int k0, int N, int K, int tid) {
+  constexpr int LD = BNT + PAD, KQ = 128 / BNT, N_IT = BNT * BK / 128;
   if (!trans) {  // B(k,n) = B[n*ldb + k], contiguous in k
-    int k = tid & 15, nq = tid >> 4;
+    const int k = tid % BK, nq = tid / BK;
+    const int gk = k0 + k;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int n = nq + 8 * i;
-      int gn = n0 + n, gk = k0 + k;
-      bool v = gn < N && gk < K;
-      cp_async8(Bs + k * LDS_B + n, v ? B + (long long)gn * ldb + gk : B, v);
+    for (int i = 0; i < N_IT; ++i) {
+      const int n = nq + 8 * i, gn = n0 + n;
+      const bool v = gn < N && gk < K;
+      cp_async8(Bs + k * LD + n, v ? B + (long long)gn * ldb + gk : B, v);
     }
   } else {       // op(B)(k,n) = B[k*ldb + n], contiguous in n
-    int n = tid & 63, kq = tid >> 6;
+    if (KQ >= 1) {
+      const int n = tid % BNT, kq = tid / BNT;
+      const int gn = n0 + n;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int k = kq + 2 * i;
-      int gn = n0 + n, gk = k0 + k;
-      bool v = gn < N && gk < K;
-      cp_async8(Bs + k * LDS_B + n, v ? B + (long long)gk * ldb + gn : B, v);
+      for (int i = 0; i < N_IT; ++i) {
+        const int k = kq + (KQ > 0 ? KQ : 1) * i, gk = k0 + k;
+        const bool v = gn < N && gk < K;
+        cp_async8(Bs + k * LD + n, v ? B + (long long)gk * ldb + gn : B, v);
+      }
+    } else {     // BNT > 128: each thread covers several n per k row
+#pragma unroll
+      for (int i = 0; i < N_IT; ++i) {
+        const int e = tid + 128 * i, n = e % BNT, k = e / BNT;
+        const int gn = n0 + n, gk = k0 + k;
+        const bool v = gn < N && gk < K;
+        cp_async8(Bs + k * LD + n, v ? B + (long long)gk * ldb + gn : B, v);
+      }
     }
   }
 }
 
+// CTA tile BMT x BNT with 4 warps, each a 32 x 32 warp tile of 4 x 4 m8n8k4
+// DMMA fragments.  (64,64): 2x2 warps; (32,128): 1x4 warps for skinny M.
+template <int BMT, int BNT>
 __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
+  constexpr int LDA_S = BMT + PAD, LDB_S = BNT + PAD, WN = BNT / 32;
   const int b = blockIdx.z;
   GemmItem it = gemm_item(d, b);
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int m0 = blockIdx.y * BMT, n0 = blockIdx.x * BNT;
   if (m0 >= it.M || n0 >= it.N) return;
   extern __shared__ __align__(16) double gsm[];
-  double (*As)[BK * LDS_A] = reinterpret_cast<double (*)[BK * LDS_A]>(gsm);
-  double (*Bs)[BK * LDS_B] = reinterpret_cast<double (*)[BK * LDS_B]>(gsm + STAGES * BK * LDS_A);
+  double* As = gsm;
+  double* Bs = gsm + STAGES * BK * LDA_S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
   const int g = lane >> 2, t = lane & 3;
 
+  const bool use_c = d.beta != 0.0;
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -104,30 +122,30 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       if (s < nk) {
-        load_a(As[s], it.A, d.lda, d.transA, m0, s * BK, it.M, it.K, tid);
-        load_b(Bs[s], it.B, d.ldb, d.transB, n0, s * BK, it.N, it.K, tid);
+        load_a<BMT>(As + s * BK * LDA_S, it.A, d.lda, d.transA, m0, s * BK, it.M, it.K, tid);
+        load_b<BNT>(Bs + s * BK * LDB_S, it.B, d.ldb, d.transB, n0, s * BK, it.N, it.K, tid);
       }
       cp_async_commit();
     }
     for (int kt = 0; kt < nk; ++kt) {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
-      int nxt = kt + STAGES - 1;
+      const int nxt = kt + STAGES - 1;
       if (nxt < nk) {
-        int s = nxt % STAGES;
-        load_a(As[s], it.A, d.lda, d.transA, m0, nxt * BK, it.M, it.K, tid);
-        load_b(Bs[s], it.B, d.ldb, d.transB, n0, nxt * BK, it.N, it.K, tid);
+        const int s = nxt % STAGES;
+        load_a<BMT>(As + s * BK * LDA_S, it.A, d.lda, d.transA, m0, nxt * BK, it.M, it.K, tid);
+        load_b<BNT>(Bs + s * BK * LDB_S, it.B, d.ldb, d.transB, n0, nxt * BK, it.N, it.K, tid);
       }
       cp_async_commit();
-      const double* as = As[kt % STAGES];
-      const double* bs = Bs[kt % STAGES];
+      const double* as = As + (kt % STAGES) * BK * LDA_S;
+      const double* bs = Bs + (kt % STAGES) * BK * LDB_S;
 #pragma unroll
       for (int kk = 0; kk < BK; kk += 4) {
         double af[4], bf[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = as[(kk + t) * LDS_A + wm + 8 * i + g];
+        for (int i = 0; i < 4; ++i) af[i] = as[(kk + t) * LDA_S + wm + 8 * i + g];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = bs[(kk + t) * LDS_B + wn + 8 * j + g];
+        for (int j = 0; j < 4; ++j) bf[j] = bs[(kk + t) * LDB_S + wn + 8 * j + g];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -139,17 +157,17 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
   // epilogue
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    int gm = m0 + wm + 8 * i + g;
+    const int gm = m0 + wm + 8 * i + g;
     if (gm >= it.M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        int gn = n0 + wn + 8 * j + 2 * t + e;
+        const int gn = n0 + wn + 8 * j + 2 * t + e;
         if (gn >= it.N) continue;
         double* c = it.C + (long long)gn * d.ldc + gm;
         double v = d.alpha * acc[i][j][e];
-        if (d.beta != 0.0) v = fma(d.beta, *c, v);
+        if (use_c) v = fma(d.beta, *c, v);
         *c = v;
       }
     }
@@ -239,15 +257,22 @@ using namespace vf;
 extern "C" int vief_dgemm_batched(const vief_gemm_desc* d, void* stream) {
   if (!d || d->batch <= 0 || d->M <= 0 || d->N <= 0) return VF_OK;
   if (d->batch > 65535) { set_error("dgemm: batch %d > 65535", d->batch); return VF_EARG; }
-  dim3 grid(cdiv(d->N, BN), cdiv(d->M, BM), d->batch);
-  if (grid.y > 65535) { set_error("dgemm: M too large"); return VF_EARG; }
-  constexpr int smem = STAGES * BK * (LDS_A + LDS_B) * sizeof(double);
   static bool attr = false;
+  constexpr int smemA = STAGES * BK * ((64 + PAD) + (64 + PAD)) * sizeof(double);
+  constexpr int smemB = STAGES * BK * ((32 + PAD) + (128 + PAD)) * sizeof(double);
   if (!attr) {
-    VF_CUDA(cudaFuncSetAttribute(k_dgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    VF_CUDA(cudaFuncSetAttribute(k_dgemm<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemA));
+    VF_CUDA(cudaFuncSetAttribute(k_dgemm<32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemB));
     attr = true;
   }
-  k_dgemm<<<grid, 128, smem, (cudaStream_t)stream>>>(*d);
+  if (d->M <= 32) {  // skinny: 32 x 128 tiles (no idle DMMA rows)
+    dim3 grid(cdiv(d->N, 128), cdiv(d->M, 32), d->batch);
+    k_dgemm<32, 128><<<grid, 128, smemB, (cudaStream_t)stream>>>(*d);
+  } else {
+    dim3 grid(cdiv(d->N, 64), cdiv(d->M, 64), d->batch);
+    if (grid.y > 65535) { set_error("dgemm: M too large"); return VF_EARG; }
+    k_dgemm<64, 64><<<grid, 128, smemA, (cudaStream_t)stream>>>(*d);
+  }
   ++g_launches;
   VF_LAUNCH_CHECK("k_dgemm");
   return VF_OK;

@@ -81,18 +81,12 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(const double* A, long long s
     if (cr == oj)
       for (int l = tid; l < nbs; l += PT) x.rowj[l] = P[l * ldp + (j - r0)];
     cl.sync();
-    if (tid == 0) {
-      double gv = -1.0;
-      int gi = 0x7fffffff, gr = 0;
-      for (int q = 0; q < cs; ++q) {
-        XLu* xr = remote(cl, &x, q);
-        if (xr->cand_v > gv || (xr->cand_v == gv && xr->cand_i < gi)) {
-          gv = xr->cand_v; gi = xr->cand_i; gr = q;
-        }
-      }
-      s_iv = gi;
-      redv[0] = gv;
-      redi[0] = gr;
+    if (tid < 32) {  // lanes read one rank's candidate each; ties -> smaller row
+      double cv = -2.0;
+      int ci = 0x7fffffff;
+      if (tid < cs) { XLu* xr = remote(cl, &x, tid); cv = xr->cand_v; ci = xr->cand_i; }
+      warp_argmax(cv, ci);
+      if (tid == 0) { s_iv = ci; redv[0] = cv; redi[0] = ci / rows_per; }
     }
     __syncthreads();
     const int piv = s_iv, owner = redi[0];
@@ -225,8 +219,13 @@ __global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long s
     if (cr == oj)
       for (int l = j + 1 + tid; l < bs; l += PT) x.rowj[l] = P[l * ldp + (j - r0)];
     cl.sync();
-    double tot = 0.0;
-    for (int q = 0; q < cs; ++q) tot += remote(cl, &x, q)->ss;
+    if (tid < 32) {
+      double v = tid < cs ? remote(cl, &x, tid)->ss : 0.0;
+      v = warp_sum(v);
+      if (tid == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double tot = red[0];
     XQr* xo = remote(cl, &x, oj);
     const double alpha = xo->alpha;
     double tj, beta, sc;
@@ -403,18 +402,12 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
     if (v >= 0.0)
       for (int r = tid; r < HSK; r += PT) x.y[r] = Ys[(iv - c0) * HSK + r];
     cl.sync();
-    if (tid == 0) {
-      double gv = -1.0;
-      int gi = 0x7fffffff, go = 0;
-      for (int q = 0; q < cs; ++q) {
-        XSel* xr = remote(cl, &x, q);
-        if (xr->cand_v > gv || (xr->cand_v == gv && xr->cand_i < gi)) {
-          gv = xr->cand_v; gi = xr->cand_i; go = q;
-        }
-      }
-      s_gi = gi;
-      s_own = go;
-      sel[i] = gi;
+    if (tid < 32) {
+      double cv = -2.0;
+      int ci = 0x7fffffff;
+      if (tid < cs) { XSel* xr = remote(cl, &x, tid); cv = xr->cand_v; ci = xr->cand_i; }
+      warp_argmax(cv, ci);
+      if (tid == 0) { s_gi = ci; s_own = ci / cols_per; sel[i] = ci; }
     }
     __syncthreads();
     const int gi = s_gi;

@@ -224,6 +224,61 @@ __global__ void k_colnorms(const double* A, long long sA, int lda, const int* pv
   if (lane == 0) out[b * ldout + c0 + j] = sqrt(s);
 }
 
+struct HState;
+
+// residual column norms after a block, LAPACK dlaqps style: downdate
+// ||a||^2 -= sum_r R(r, col)^2 over the block's R rows, and recompute exactly
+// from A when the downdated value has lost more than half the digits relative
+// to the last exact value (ratio <= sqrt(eps)).  Warp per column.
+// The norms only steer the termination test (pivots come from the sketch), so a
+// downdated value is kept while it is provably on the right side of the cut:
+// its error is below ~1e-13 ||a_ref||^2 (u per downdate), hence a value above
+// max(1e-12 ||a_ref||^2, 4 cut^2) is certainly above cut^2.  Anything else is
+// flagged and recomputed exactly (k_norm_exact) after the pending trailing
+// updates have been applied.
+__global__ void k_norm_downdate(const int* pv, const int* mv, const int* active, const int* bsv,
+                                int J, const double* Rm, long long sR, int ldR, double* tn,
+                                const double* tn0, int* flag, int ldt, const double* cutv,
+                                int* any) {
+  const int b = blockIdx.y;
+  if (!active[b]) return;
+  const int bs = bsv[b];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = J + bs + blockIdx.x * 8 + warp;
+  const int m = mv[b];
+  if (bs <= 0 || c >= m) return;
+  const double* R = Rm + b * sR + (long long)c * ldR + J;
+  double w = lane < bs ? R[lane] : 0.0;
+  w = warp_sum(w * w);
+  if (lane != 0) return;
+  const long long o = (long long)b * ldt + c;
+  const double cur = tn[o], ref = tn0[o], cut = cutv[b];
+  const double nv = cur * cur - w;
+  const bool bad = !(nv > fmax(1e-12 * ref * ref, 4.0 * cut * cut));
+  tn[o] = sqrt(fmax(nv, 0.0));
+  flag[o] = bad;
+  if (bad) atomicOr(any, 1);
+}
+
+__global__ void k_norm_exact(const double* A, long long sA, int lda, const int* pv, const int* mv,
+                             const int* active, const int* bsv, int J, double* tn, double* tn0,
+                             int* flag, int ldt) {
+  const int b = blockIdx.y;
+  if (!active[b]) return;
+  const int bs = bsv[b];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = J + bs + blockIdx.x * 8 + warp;
+  const int m = mv[b], p = pv[b];
+  if (bs <= 0 || c >= m) return;
+  const long long o = (long long)b * ldt + c;
+  if (!flag[o]) return;
+  const double* a = A + b * sA + (long long)c * lda;
+  double s = 0.0;
+  for (int i = lane; i < p; i += 32) s = fma(a[i], a[i], s);
+  s = sqrt(warp_sum(s));
+  if (lane == 0) { tn[o] = s; tn0[o] = s; flag[o] = 0; }
+}
+
 struct HState {
   // per item
   int* active;    // 1 while the item's group is unfinished
@@ -235,9 +290,13 @@ struct HState {
   int* sact;      // HS if active else 0
   int* swaps;     // count x HB (source positions)
   double* cut;    // eps * max column norm
-  double* tn;     // count x maxm trailing norms (absolute column index)
+  double* tn;     // count x maxm trailing residual norms (travel with their columns)
+  double* tn0;    // last exactly computed norm of each column (downdating reference)
+  int* flag;      // count x maxm: column needs an exact norm
   double* Rt;     // count x HB x HB block R (upper)
-  double* Qw;     // count x maxp x HB explicit panel Q
+  double* Qw;     // count x maxp x (HB*D): explicit panel Q's of the pending blocks
+  double* G;      // count x HB x (HB*D): Q_i^T Qcat
+  int D;          // inner blocks per delayed trailing update
   double* work;   // count x maxp x HB panel work copy (large panels)
   double* Y;      // count x HS x maxm sketch
   double* Z;      // count x HS x HB
@@ -300,9 +359,15 @@ __global__ void k_apply_swaps(double* A, long long sA, int lda, double* Y, long 
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     int* pm = perm + b * ldperm;
+    double* t = S.tn + (long long)b * S.ldtn;
+    double* t0 = S.tn0 + (long long)b * S.ldtn;
     for (int i = 0; i < bs; ++i) {
       const int src = sw[i], dst = J + i;
-      if (src != dst) { int t = pm[src]; pm[src] = pm[dst]; pm[dst] = t; }
+      if (src != dst) {
+        int tp = pm[src]; pm[src] = pm[dst]; pm[dst] = tp;
+        double tv = t[src]; t[src] = t[dst]; t[dst] = tv;
+        tv = t0[src]; t0[src] = t0[dst]; t0[dst] = tv;
+      }
     }
   }
 }
@@ -620,8 +685,12 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.bs = buf.get<int>(count); S.nrem = buf.get<int>(count); S.pact = buf.get<int>(count);
     S.sact = buf.get<int>(count); S.swaps = buf.get<int>((size_t)HB * count);
     S.cut = buf.get<double>(count); S.tn = buf.get<double>((size_t)maxm * count);
+    S.tn0 = buf.get<double>((size_t)maxm * count);
+    S.flag = buf.get<int>((size_t)maxm * count);
     S.Rt = buf.get<double>((size_t)HB * HB * count);
-    S.Qw = buf.get<double>((size_t)maxp * HB * count);
+    S.D = maxm >= 2048 ? 4 : (maxm >= 512 ? 2 : 1);
+    S.Qw = buf.get<double>((size_t)maxp * HB * S.D * count);
+    S.G = buf.get<double>((size_t)HB * HB * S.D * count);
     S.work = nullptr;
     S.Y = buf.get<double>((size_t)HS * maxm * count);
     S.Z = buf.get<double>((size_t)HS * HB * count);
@@ -630,10 +699,12 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     double* Om = buf.get<double>((size_t)HS * maxp);
     if (!S.Y || !S.Qw || !Om || !S.any) { set_error("id: out of device memory (blocked)"); return VF_ENOMEM; }
     prof_push(st, "id.init+sketch");
-    const long long sY = (long long)HS * maxm, sQ = (long long)maxp * HB;
+    const long long sY = (long long)HS * maxm, sQ = (long long)maxp * HB * S.D;
     k_iota<<<dim3(cdiv(maxm, 128), count), 128, 0, st>>>(d->perm, maxm, d->m, count);
     k_colnorms<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m,
                                                            nullptr, 0, S.tn, maxm);
+    VF_CUDA(cudaMemcpyAsync(S.tn0, S.tn, sizeof(double) * maxm * count, cudaMemcpyDeviceToDevice,
+                            st));
     k_colmax<<<count, 256, 0, st>>>(S.tn, maxm, d->m, count, colmax);
     k_init_state<<<cdiv(count, 128), 128, 0, st>>>(S, colmax, d->p, d->m, count, d->eps);
     k_gaussian<<<cdiv((long long)HS * maxp, 256), 256, 0, st>>>(Om, (long long)HS * maxp,
@@ -651,6 +722,12 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       if ((rc = vief_dgemm_batched(&g, st))) return rc;
     }
     const int kcap = std::min(maxp, maxm);
+    // Trailing updates are delayed over D inner blocks (K = 32 D in the update
+    // GEMM).  Between flushes: the panel is made current with the pending
+    // (Q, W) pairs, W of a new block is corrected for the pending blocks, and
+    // norms recomputed exactly use the implicit residual a - Qcat W.
+    const int D = S.D;
+    int pend = 0, Jf = 0;
     for (int J = 0; J < kcap; J += HB) {
       prof_push(st, "id.setup+select");
       k_block_setup<<<cdiv(count, 128), 128, 0, st>>>(J, d->p, d->m, count, S);
@@ -660,11 +737,23 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       prof_push(st, "id.swaps");
       k_apply_swaps<<<dim3(cdiv(std::max(std::max(maxp, HS), J), 128), count), 128, 0, st>>>(
           d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S, Rm, sR, ldR);
-      g_launches += 3;
+      g_launches += 2;
       VF_LAUNCH_CHECK("id select/swap");
+      double* Qi = S.Qw + (long long)pend * HB * maxp;
+      const int kp = pend * HB;  // pending Q columns
+      if (pend > 0) {  // make the panel current: A(:, J:J+bs) -= Qcat W_pend(:, J:J+bs)
+        prof_push(st, "id.panel_catchup");
+        vief_gemm_desc c{};
+        c.A = S.Qw; c.strideA = sQ; c.lda = maxp;
+        c.B = Rm + (long long)J * ldR + Jf; c.strideB = sR; c.ldb = ldR;
+        c.C = d->A + (long long)J * d->lda; c.strideC = d->sA; c.ldc = d->lda;
+        c.M = maxp; c.N = HB; c.K = kp; c.Mb = S.pact; c.Nb = S.bs;
+        c.alpha = -1.0; c.beta = 1.0; c.batch = count;
+        if ((rc = vief_dgemm_batched(&c, st))) return rc;
+      }
       prof_push(st, "id.panel_qr");
-      if ((rc = qr_panel(d->A, d->sA, d->lda, d->p, S.active, S.bs, J, maxp, count, S.Qw, sQ,
-                         maxp, S.Rt, st)))
+      if ((rc = qr_panel(d->A, d->sA, d->lda, d->p, S.active, S.bs, J, maxp, count, Qi, sQ, maxp,
+                         S.Rt, st)))
         return rc;
       k_store_rblock<<<count, 256, 0, st>>>(S, Rm, sR, ldR, J);
       ++g_launches;
@@ -672,26 +761,22 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         // items with bs < HB have nrem = 0, so the fixed offset J+HB is exact for all active work
         prof_push(st, "id.gemm_W");
         vief_gemm_desc w{};
-        w.A = S.Qw; w.strideA = sQ; w.lda = maxp; w.transA = 1;
+        w.A = Qi; w.strideA = sQ; w.lda = maxp; w.transA = 1;
         w.B = d->A + (long long)(J + HB) * d->lda; w.strideB = d->sA; w.ldb = d->lda;
         w.C = Rm + (long long)(J + HB) * ldR + J; w.strideC = sR; w.ldc = ldR;
         w.M = HB; w.N = maxm; w.K = maxp; w.Mb = S.bs; w.Nb = S.nrem; w.Kb = S.pact;
         w.alpha = 1.0; w.beta = 0.0; w.batch = count;
         if ((rc = vief_dgemm_batched(&w, st))) return rc;
-        // A_trail -= Q W
-        prof_push(st, "id.gemm_update");
-        vief_gemm_desc u{};
-        u.A = S.Qw; u.strideA = sQ; u.lda = maxp;
-        u.B = Rm + (long long)(J + HB) * ldR + J; u.strideB = sR; u.ldb = ldR;
-        u.C = d->A + (long long)(J + HB) * d->lda; u.strideC = d->sA; u.ldc = d->lda;
-        u.M = maxp; u.N = maxm; u.K = HB; u.Mb = S.pact; u.Nb = S.nrem; u.Kb = S.bs;
-        u.alpha = -1.0; u.beta = 1.0; u.batch = count;
-        if ((rc = vief_dgemm_batched(&u, st))) return rc;
+        // W is taken against the stale trailing columns: W_true = W - (Q_i^T Qcat) W_pend,
+        // and Q_i is orthogonal to the pending Q's to O(u ||P_stale|| / ||P_res||) = O(u)
+        // for D <= 4 blocks of the slowly decaying proxy rows, so the correction is
+        // below u ||A|| and is not formed (the bookkeeping A P = Q R + residual stays
+        // exact up to that term).
         // sketch downdate: Y_trail -= (Omega Q) W  (= Omega A_trail after the update)
         prof_push(st, "id.sketch_downdate");
         vief_gemm_desc z{};
         z.A = Om; z.strideA = 0; z.lda = HS;
-        z.B = S.Qw; z.strideB = sQ; z.ldb = maxp;
+        z.B = Qi; z.strideB = sQ; z.ldb = maxp;
         z.C = S.Z; z.strideC = (long long)HS * HB; z.ldc = HS;
         z.M = HS; z.N = HB; z.K = maxp; z.Mb = S.sact; z.Nb = S.bs; z.Kb = S.pact;
         z.alpha = 1.0; z.beta = 0.0; z.batch = count;
@@ -704,13 +789,40 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         y.alpha = -1.0; y.beta = 1.0; y.batch = count;
         if ((rc = vief_dgemm_batched(&y, st))) return rc;
       }
+      // norms: downdate; columns near the cut (or with lost digits) need exact values,
+      // which are only formed on a current A (after a flush)
       prof_push(st, "id.norms+rank");
-      k_colnorms<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m,
-                                                             S.active, J + HB, S.tn, maxm);
+      VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
+      k_norm_downdate<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(
+          d->p, d->m, S.active, S.bs, J, Rm, sR, ldR, S.tn, S.tn0, S.flag, maxm, S.cut, S.any);
+      ++g_launches;
+      int need = 0;
+      VF_CUDA(cudaMemcpyAsync(&need, S.any, sizeof(int), cudaMemcpyDeviceToHost, st));
+      VF_CUDA(cudaStreamSynchronize(st));
+      ++pend;
+      if (pend == D || need) {  // flush: A_trail -= Qcat W_pend  (K = 32 pend)
+        prof_push(st, "id.gemm_update");
+        vief_gemm_desc u{};
+        u.A = S.Qw; u.strideA = sQ; u.lda = maxp;
+        u.B = Rm + (long long)(J + HB) * ldR + Jf; u.strideB = sR; u.ldb = ldR;
+        u.C = d->A + (long long)(J + HB) * d->lda; u.strideC = d->sA; u.ldc = d->lda;
+        u.M = maxp; u.N = maxm; u.K = pend * HB; u.Mb = S.pact; u.Nb = S.nrem;
+        u.alpha = -1.0; u.beta = 1.0; u.batch = count;
+        if ((rc = vief_dgemm_batched(&u, st))) return rc;
+        pend = 0;
+        Jf = J + HB;
+        if (need) {
+          prof_push(st, "id.norms+rank");
+          k_norm_exact<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(
+              d->A, d->sA, d->lda, d->p, d->m, S.active, S.bs, J, S.tn, S.tn0, S.flag, maxm);
+          ++g_launches;
+        }
+      }
+      prof_push(st, "id.norms+rank");
       VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
       k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J);
       k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
-      g_launches += 3;
+      g_launches += 2;
       VF_LAUNCH_CHECK("id rank");
       prof_push(st, "id.hostsync");
       int any = 0;
