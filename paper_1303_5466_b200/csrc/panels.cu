@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(const double* A, long long s
     int iv = 0x7fffffff;
     for (int i = max(j - r0, 0) + tid; i < nr; i += PT) {
       double a = fabs(P[j * ldp + i]);
+      if (a != a) a = INFINITY;  // NaN (from an earlier singular pivot) stays selectable
       if (a > v) { v = a; iv = r0 + i; }
     }
     block_argmax(v, iv, redv, redi);
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(const double* A, long long s
       int ci = 0x7fffffff;
       if (tid < cs) { XLu* xr = remote(cl, &x, tid); cv = xr->cand_v; ci = xr->cand_i; }
       warp_argmax(cv, ci);
+      if (ci < j || ci >= R) { ci = j; cv = 0.0; }  // defensive: always a valid owner rank
       if (tid == 0) { s_iv = ci; redv[0] = cv; redi[0] = ci / rows_per; }
     }
     __syncthreads();
@@ -407,6 +409,7 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
       int ci = 0x7fffffff;
       if (tid < cs) { XSel* xr = remote(cl, &x, tid); cv = xr->cand_v; ci = xr->cand_i; }
       warp_argmax(cv, ci);
+      if (ci < 0 || ci >= n) ci = min(i, n - 1);  // defensive (NaN data): stay in range
       if (tid == 0) { s_gi = ci; s_own = ci / cols_per; sel[i] = ci; }
     }
     __syncthreads();
