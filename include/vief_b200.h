@@ -40,6 +40,8 @@ long long vief_launch_count(void);
 /* phase profiler: CUDA-event totals per orchestration phase (synchronising; off by default) */
 void vief_prof_enable(int on);
 void vief_prof_prefix(const char* prefix);  /* tag subsequent phases (e.g. level) */
+void vief_prof_mark(const char* name, void* stream);  /* open a host-marked phase */
+void vief_prof_flush(void* stream);                   /* close, sync, accumulate */
 int vief_prof_report(char* buf, int len);
 
 /* ---- problem description (kernels.py:216-302 Assembler state) ----------- */
@@ -53,6 +55,9 @@ typedef struct {
   int is_complex;        /* 0: float64 entries, 1: complex128 (helmholtz2d) */
   double hh;             /* h*h */
   double corr_re, corr_im; /* diagonal correction corr0 (kernels.py:196-203) */
+  int realify;           /* complex only: index lists hold real unknowns u = 2*point + (0 re | 1 im)
+                            and entries are the real 2x2 blocks [[Re,-Im],[Im,Re]]; ID matrices
+                            get 2p rows (source, component) */
 } vief_problem;
 
 /* K1a: A[I_b, J_b] with the diagonal rule — replaces Assembler.block

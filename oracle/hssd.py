@@ -411,10 +411,12 @@ class Compressed:
         return t
 
 
-def compress(P, tree, eps, pad):
-    """Fine-to-coarse proxy-reduced skeletonization (solver_dense.py:234-272)."""
-    H = Compressed(P, tree, {}, {}, {}, {}, {}, {})
-    for b in tree.fine_to_coarse():
+def compress(P, tree, eps, pad, boxes=None, H=None):
+    """Fine-to-coarse proxy-reduced skeletonization (solver_dense.py:234-272).
+    `boxes` (fine-to-coarse order) restricts the sweep to a subtree, adding to
+    an existing `H` (used by the distributed tests)."""
+    H = H or Compressed(P, tree, {}, {}, {}, {}, {}, {})
+    for b in (tree.fine_to_coarse() if boxes is None else boxes):
         rows = H.rows(b)
         if tree.is_leaf(b):
             H.D[b] = entries(P, rows, rows)
@@ -457,12 +459,12 @@ class Inverse:
         return t
 
 
-def invert(H):
+def invert(H, boxes=None, inv=None):
     """F = D | [[E1,B12],[B21,E2]]; LU(F); E = (R F^-1 L)^-1
-    (solver_dense.py:332-368)."""
+    (solver_dense.py:332-368); `boxes` restricts to a subtree."""
     tree, dt = H.tree, H.P.dtype
-    inv = Inverse(H, {}, {})
-    for b in tree.fine_to_coarse():
+    inv = inv or Inverse(H, {}, {})
+    for b in (tree.fine_to_coarse() if boxes is None else boxes):
         if tree.is_leaf(b):
             F = np.array(H.D[b], dtype=dt)
         else:
@@ -478,6 +480,39 @@ def invert(H):
     return inv
 
 
+def apply_up(inv, f2, boxes, ups, uin):
+    """Up sweep over `boxes` (fine to coarse): phi = F^-1 u, ups = E R phi
+    (solver_dense.py:303-310)."""
+    H, tree = inv.H, inv.H.tree
+    for b in boxes:
+        u = f2[tree.owned(b)] if tree.is_leaf(b) else np.vstack([ups[c] for c in tree.kids[b]])
+        uin[b] = u
+        if b == 0:
+            continue
+        phi = sla.lu_solve(inv.Flu[b], u, check_finite=False)
+        ups[b] = inv.E[b] @ interp_R_apply(H.Rf[b], phi)
+
+
+def apply_down(inv, boxes, ups, uin, dn, out):
+    """Down sweep over `boxes` (coarse to fine) (solver_dense.py:312-328)."""
+    H, tree = inv.H, inv.H.tree
+    for b in boxes:
+        u = uin[b]
+        if b == 0:
+            res = sla.lu_solve(inv.Flu[0], u, check_finite=False)
+        else:
+            nu = u - interp_L_apply(H.Lf[b], ups[b])
+            if dn.get(b) is not None:
+                nu += interp_L_apply(H.Lf[b], inv.E[b] @ dn[b])
+            res = sla.lu_solve(inv.Flu[b], nu, check_finite=False)
+        if tree.is_leaf(b):
+            out[tree.owned(b)] = res
+        else:
+            c1, c2 = tree.kids[b]
+            k1 = inv.E[c1].shape[0]
+            dn[c1], dn[c2] = res[:k1], res[k1:]
+
+
 def apply_inverse(inv, f):
     """Up (fine->coarse) then down (coarse->fine) sweeps
     (solver_dense.py:293-329)."""
@@ -487,29 +522,8 @@ def apply_inverse(inv, f):
     f2 = f[:, None] if single else f
     out = np.zeros_like(f2)
     ups, uin = {}, {}
-    for b in tree.fine_to_coarse():
-        u = f2[tree.owned(b)] if tree.is_leaf(b) else np.vstack([ups[c] for c in tree.kids[b]])
-        uin[b] = u
-        if b == 0:
-            continue
-        phi = sla.lu_solve(inv.Flu[b], u, check_finite=False)
-        ups[b] = inv.E[b] @ interp_R_apply(H.Rf[b], phi)
-    dn = {0: None}
-    for b in tree.coarse_to_fine():
-        u = uin[b]
-        if b == 0:
-            res = sla.lu_solve(inv.Flu[0], u, check_finite=False)
-        else:
-            nu = u - interp_L_apply(H.Lf[b], ups[b])
-            if dn[b] is not None:
-                nu += interp_L_apply(H.Lf[b], inv.E[b] @ dn[b])
-            res = sla.lu_solve(inv.Flu[b], nu, check_finite=False)
-        if tree.is_leaf(b):
-            out[tree.owned(b)] = res
-        else:
-            c1, c2 = tree.kids[b]
-            k1 = inv.E[c1].shape[0]
-            dn[c1], dn[c2] = res[:k1], res[k1:]
+    apply_up(inv, f2, list(tree.fine_to_coarse()), ups, uin)
+    apply_down(inv, list(tree.coarse_to_fine()), ups, uin, {0: None}, out)
     return out[:, 0] if single else out
 
 

@@ -21,7 +21,7 @@ c_int, c_ll, c_double, c_vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_double, 
 class Problem(ctypes.Structure):
     _fields_ = [("table", c_vp), ("table_len", c_ll), ("av", c_vp), ("bv", c_vp), ("cv", c_vp),
                 ("n_side", c_int), ("is_complex", c_int), ("hh", c_double),
-                ("corr_re", c_double), ("corr_im", c_double)]
+                ("corr_re", c_double), ("corr_im", c_double), ("realify", c_int)]
 
 
 class GemmDesc(ctypes.Structure):
@@ -50,6 +50,8 @@ _SIGS = {
     "vief_launch_count": [],
     "vief_prof_enable": [c_int],
     "vief_prof_prefix": [ctypes.c_char_p],
+    "vief_prof_mark": [ctypes.c_char_p, c_vp],
+    "vief_prof_flush": [c_vp],
     "vief_prof_report": [ctypes.c_char_p, c_int],
     "vief_gen_block": [c_vp, c_vp, c_ll, c_vp, c_int, c_vp, c_ll, c_vp, c_int,
                        c_vp, c_ll, c_vp, c_int, c_int, c_vp],
@@ -73,7 +75,8 @@ _SIGS = {
                     c_vp, c_int, c_vp, c_int, c_int, c_vp],
     "vief_pad_identity": [c_vp, c_ll, c_int, c_vp, c_int, c_int, c_vp],
 }
-_RET = {"vief_last_error": ctypes.c_char_p, "vief_launch_count": c_ll, "vief_prof_enable": None, "vief_prof_prefix": None}
+_RET = {"vief_last_error": ctypes.c_char_p, "vief_launch_count": c_ll, "vief_prof_enable": None, "vief_prof_prefix": None,
+        "vief_prof_mark": None, "vief_prof_flush": None}
 
 _lib = None
 
@@ -125,6 +128,8 @@ def call(name, *args):
 
 
 def prof_enable(on=True):
+    global PROFILING
+    PROFILING = bool(on)
     load().vief_prof_enable(int(on))
 
 
@@ -215,3 +220,16 @@ def inv_batched(A, sA, lda, n, batch):
 
 def prof_prefix(tag):
     load().vief_prof_prefix(tag.encode())
+
+
+PROFILING = False
+
+
+def prof_mark(name):
+    """Open a named phase (no-op unless profiling was enabled)."""
+    if PROFILING:
+        load().vief_prof_mark(name.encode(), stream_handle())
+
+
+def prof_flush():
+    load().vief_prof_flush(stream_handle())

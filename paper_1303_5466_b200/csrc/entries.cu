@@ -72,6 +72,23 @@ __global__ void k_gen_block(vief_problem P, const int* I, long long sI, const in
   }
 }
 
+// proxy-reduced block-row entry between work point gp and source (sx, sy, sg)
+template <bool CPLX>
+__device__ __forceinline__ cd idmat_entry(const vief_problem& P, int kind, int gp, int sx, int sy,
+                                          int sg) {
+  const int n = P.n_side;
+  const int dx = gp % n - sx, dy = gp / n - sy;
+  const cd t = tab<CPLX>(P, dx * dx + dy * dy);
+  if (sg < 0) {  // proxy point: (K*b_i)*h^2 (kind 0) / (K*c_j)*h^2 (kind 1)
+    double f = kind == 0 ? fld<CPLX>(P.bv, gp) : fld<CPLX>(P.cv, gp);
+    return mulr(mulr(t, f), P.hh);
+  }
+  // near grid point: (K*h^2)*(b*c)
+  double bc = kind == 0 ? __dmul_rn(fld<CPLX>(P.bv, gp), fld<CPLX>(P.cv, sg))
+                        : __dmul_rn(fld<CPLX>(P.bv, sg), fld<CPLX>(P.cv, gp));
+  return mulr(mulr(t, P.hh), bc);
+}
+
 // ID matrices (p x m): row i = source, column j = work point
 template <bool CPLX>
 __global__ void k_gen_idmat(vief_problem P, int kind, const int* pts, long long sPts, const int* m,
@@ -82,24 +99,56 @@ __global__ void k_gen_idmat(vief_problem P, int kind, const int* pts, long long 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j0 = blockIdx.y * 8;
   if (i >= pb) return;
-  const int n = P.n_side;
   const int sx = src_xy[2 * (b * sSrc + i)], sy = src_xy[2 * (b * sSrc + i) + 1];
   const int sg = src_g[b * sSrc + i];
   double* o = out + b * sOut;
+  for (int j = j0; j < min(j0 + 8, mb); ++j)
+    store<CPLX>(o, (long long)j * ldo + i, idmat_entry<CPLX>(P, kind, pts[b * sPts + j], sx, sy, sg));
+}
+
+// ---------------------------------------------------------------------------
+// realified complex systems: unknown u = 2 g + c (g grid point, c = 0 re / 1 im);
+// the complex entry a becomes the real 2x2 block [[Re a, -Im a], [Im a, Re a]].
+__device__ __forceinline__ double realify(cd a, int ci, int cj) {
+  return ci == cj ? a.re : (ci == 0 ? -a.im : a.im);
+}
+
+__global__ void k_gen_block_r2(vief_problem P, const int* I, long long sI, const int* nI, int maxI,
+                               const int* J, long long sJ, const int* nJ, int maxJ, double* out,
+                               long long sOut, double* const* outp, int ldo) {
+  const int b = blockIdx.z;
+  const int ni = nI ? nI[b] : maxI, nj = nJ ? nJ[b] : maxJ;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = blockIdx.y * 8;
+  if (i >= ni) return;
+  const int ui = I[b * sI + i];
+  double* o = outp ? outp[b] : out + b * sOut;
+  for (int j = j0; j < min(j0 + 8, nj); ++j) {
+    const int uj = J[b * sJ + j];
+    o[(long long)j * ldo + i] = realify(block_entry<true>(P, ui >> 1, uj >> 1), ui & 1, uj & 1);
+  }
+}
+
+// realified ID matrices (2p x m): real row i = (source i>>1, component i&1),
+// column j = work unknown pts[j].  kind 0 is the transposed row block, so the
+// 2x2 block is indexed [work comp][source comp]; kind 1 [source comp][work comp].
+__global__ void k_gen_idmat_r2(vief_problem P, int kind, const int* pts, long long sPts,
+                               const int* m, int maxm, const int* src_xy, const int* src_g,
+                               long long sSrc, const int* p, int maxp, double* out, long long sOut,
+                               int ldo) {
+  const int b = blockIdx.z;
+  const int mb = m ? m[b] : maxm, pb = 2 * (p ? p[b] : maxp);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = blockIdx.y * 8;
+  if (i >= pb) return;
+  const int s = i >> 1, cs = i & 1;
+  const int sx = src_xy[2 * (b * sSrc + s)], sy = src_xy[2 * (b * sSrc + s) + 1];
+  const int sg = src_g[b * sSrc + s];
+  double* o = out + b * sOut;
   for (int j = j0; j < min(j0 + 8, mb); ++j) {
-    const int gp = pts[b * sPts + j];
-    const int dx = gp % n - sx, dy = gp / n - sy;
-    const cd t = tab<CPLX>(P, dx * dx + dy * dy);
-    cd v;
-    if (sg < 0) {  // proxy point: (K*b_i)*h^2 (kind 0) / (K*c_j)*h^2 (kind 1)
-      double f = kind == 0 ? fld<CPLX>(P.bv, gp) : fld<CPLX>(P.cv, gp);
-      v = mulr(mulr(t, f), P.hh);
-    } else {       // near grid point: (K*h^2)*(b*c)
-      double bc = kind == 0 ? __dmul_rn(fld<CPLX>(P.bv, gp), fld<CPLX>(P.cv, sg))
-                            : __dmul_rn(fld<CPLX>(P.bv, sg), fld<CPLX>(P.cv, gp));
-      v = mulr(mulr(t, P.hh), bc);
-    }
-    store<CPLX>(o, (long long)j * ldo + i, v);
+    const int u = pts[b * sPts + j];
+    const cd e = idmat_entry<true>(P, kind, u >> 1, sx, sy, sg);
+    o[(long long)j * ldo + i] = kind == 0 ? realify(e, u & 1, cs) : realify(e, cs, u & 1);
   }
 }
 
@@ -188,7 +237,9 @@ extern "C" int vief_gen_block(const vief_problem* P, const int* I, long long sI,
   if (batch <= 0 || maxI <= 0 || maxJ <= 0) return VF_OK;
   dim3 grid(cdiv(maxI, 128), cdiv(maxJ, 8), batch);
   if (grid.y > 65535 || batch > 65535) { set_error("gen_block: grid too large"); return VF_EARG; }
-  if (P->is_complex)
+  if (P->is_complex && P->realify)
+    k_gen_block_r2<<<grid, 128, 0, (cudaStream_t)stream>>>(*P, I, sI, nI, maxI, J, sJ, nJ, maxJ, out, sOut, outp, ldo);
+  else if (P->is_complex)
     k_gen_block<true><<<grid, 128, 0, (cudaStream_t)stream>>>(*P, I, sI, nI, maxI, J, sJ, nJ, maxJ, out, sOut, outp, ldo);
   else
     k_gen_block<false><<<grid, 128, 0, (cudaStream_t)stream>>>(*P, I, sI, nI, maxI, J, sJ, nJ, maxJ, out, sOut, outp, ldo);
@@ -202,9 +253,11 @@ extern "C" int vief_gen_idmat(const vief_problem* P, int kind, const int* pts, l
                               long long sSrc, const int* p, int maxp, double* out, long long sOut,
                               int ldo, int batch, void* stream) {
   if (batch <= 0 || maxm <= 0 || maxp <= 0) return VF_OK;
-  dim3 grid(cdiv(maxp, 128), cdiv(maxm, 8), batch);
+  dim3 grid(cdiv((P->is_complex && P->realify) ? 2 * maxp : maxp, 128), cdiv(maxm, 8), batch);
   if (grid.y > 65535 || batch > 65535) { set_error("gen_idmat: grid too large"); return VF_EARG; }
-  if (P->is_complex)
+  if (P->is_complex && P->realify)
+    k_gen_idmat_r2<<<grid, 128, 0, (cudaStream_t)stream>>>(*P, kind, pts, sPts, m, maxm, src_xy, src_g, sSrc, p, maxp, out, sOut, ldo);
+  else if (P->is_complex)
     k_gen_idmat<true><<<grid, 128, 0, (cudaStream_t)stream>>>(*P, kind, pts, sPts, m, maxm, src_xy, src_g, sSrc, p, maxp, out, sOut, ldo);
   else
     k_gen_idmat<false><<<grid, 128, 0, (cudaStream_t)stream>>>(*P, kind, pts, sPts, m, maxm, src_xy, src_g, sSrc, p, maxp, out, sOut, ldo);

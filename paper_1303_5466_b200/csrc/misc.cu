@@ -276,3 +276,9 @@ void ensure_pool() {
   done = true;
 }
 }  // namespace vf
+
+// phases marked from the host orchestration (Python): closes the open phase
+extern "C" void vief_prof_mark(const char* name, void* stream) {
+  vf::prof_push((cudaStream_t)stream, name);
+}
+extern "C" void vief_prof_flush(void* stream) { vf::prof_flush((cudaStream_t)stream); }

@@ -162,18 +162,39 @@ class Hss2dMatrix:
     """Outer skeleton compression of the system matrix, resident in HBM
     (solver_dense.py:98-231)."""
 
-    def __init__(self, spec, grid, tree, eps, opts, quad=PLAIN):
+    def __init__(self, spec, grid, tree, eps, opts, quad=PLAIN, level_slices=None):
+        """`level_slices` (sharded use, distributed.py): {level: (lo, hi)} box
+        ranges this object factors; other levels are absent (None)."""
         _lib.require_cuda()
         self.spec, self.grid, self.tree = spec, grid, tree
         self.eps, self.opts, self.quad = eps, opts, quad
         self.asm = get_assembler(spec, grid, quad)
         self.device = self.asm.device
-        self.symmetric = spec.symmetric
+        # complex (helmholtz2d) systems are factored in realified form: every
+        # point carries two real unknowns (Re, Im) and each complex entry the
+        # real block [[Re, -Im], [Im, Re]]; the hierarchy, skeletonization and
+        # all kernels are the real ones.  Complex symmetry is not real symmetry,
+        # so row and column IDs are both computed.
+        self.realified = bool(spec.is_complex)
+        self.problem = _lib.Problem.from_buffer_copy(self.asm.problem)
+        self.problem.realify = int(self.realified)
+        self.symmetric = spec.symmetric and not self.realified
         self.group = 1 if self.symmetric else 2
-        self.levels = [_Level(lv, tree.ids[lv], tree.rects[lv], lv == tree.depth)
-                       for lv in range(tree.depth + 1)]
+        self.levels = []
+        for lv in range(tree.depth + 1):
+            sl = (0, len(tree.ids[lv])) if level_slices is None else level_slices.get(lv)
+            if sl is None:
+                self.levels.append(None)
+                continue
+            L = _Level(lv, tree.ids[lv][sl[0]:sl[1]], tree.rects[lv][sl[0]:sl[1]],
+                       lv == tree.depth)
+            L.sl = sl
+            self.levels.append(L)
+        self.sharded = level_slices is not None
         self._lvl_of = {}
         for L in self.levels:
+            if L is None:
+                continue
             for j, i in enumerate(L.ids):
                 self._lvl_of[int(i)] = (L, j)
         nonroot = lambda: [i for i in self._lvl_of if i != 0]
@@ -238,17 +259,17 @@ class Hss2dMatrix:
     def nbytes(self):
         """D + B + T bytes of the real entries (solver_dense.py:132-139)."""
         tot = 0
-        for L in self.levels:
+        for L in _real_levels(self):
             if L.leaf:
                 tot += int((L.m.astype(np.int64) ** 2).sum()) * 8
-            if L.lv < len(self.levels) - 1:
+            if not L.leaf:
                 C = self.levels[L.lv + 1]
                 k1, k2 = C.k[0::2].astype(np.int64), C.k[1::2].astype(np.int64)
                 tot += int((2 * k1 * k2).sum()) * 8
             if L.lv > 0:
                 t = int((L.k.astype(np.int64) * (L.m - L.k)).sum()) * 8
                 tot += t * (1 if self.symmetric else 2)
-        return tot * (2 if self.spec.is_complex else 1)
+        return tot  # realified complex blocks are counted as the real doubles they occupy
 
     # -- forward operator ---------------------------------------------------
     def matvec(self, x):
@@ -281,16 +302,20 @@ def _level_sources(H, L, pad):
 
 
 def _compress_level(H, L, pad, seed):
-    dev, asm = H.device, H.asm
-    prob = ctypes.byref(asm.problem)
+    dev = H.device
+    prob = ctypes.byref(H.problem)
     st = _lib.stream_handle
     nb = L.nb
+    _lib.prof_mark("py.rows")
     # work rows / cols
     if L.leaf:
-        own = H.tree.owned_level(L.lv)
-        L.m = (own >= 0).sum(axis=1).astype(np.int32)
+        own = H.tree.owned_level(L.lv)[L.sl[0]:L.sl[1]]
+        own = np.where(own >= 0, own, 0)
+        if H.realified:  # unknowns u = 2*point + component, interleaved per point
+            own = np.stack([2 * own, 2 * own + 1], axis=-1).reshape(own.shape[0], -1)
+        L.m = np.full(nb, own.shape[1], dtype=np.int32)
         L.mmax = int(L.m.max())
-        L.rows = _dev_i32(np.where(own >= 0, own, 0), dev)
+        L.rows = _dev_i32(own, dev)
         L.cols = L.rows
         L.cat_idx = None
     else:
@@ -311,6 +336,7 @@ def _compress_level(H, L, pad, seed):
             L.cols = torch.zeros((nb, L.mmax), dtype=_I32, device=dev)
             _lib.gather_int(C.cskel, 2 * C.kmax, L.cat_idx, L.mmax, L.cols, L.mmax, m_d, L.mmax, nb)
     L.m_d = _dev_i32(L.m, dev)
+    _lib.prof_mark("py.entries_DB")
     # leaf D / sibling B blocks (solver_dense.py:243-249)
     if L.leaf:
         L.D = torch.empty((nb, L.mmax, L.mmax), dtype=_F64, device=dev)
@@ -332,15 +358,18 @@ def _compress_level(H, L, pad, seed):
                   kc, nb, st())
     if L.lv == 0:
         return
+    _lib.prof_mark("py.sources+idmat")
     # proxy + near sources and the ID matrices (solver_dense.py:250-263)
     p, pmax, src_xy, src_g = _level_sources(H, L, pad)
     L.p = p
     g = H.group
     count = nb * g
-    ldA = _even(pmax)
     mm = L.mmax
-    A = torch.zeros((count, mm, ldA), dtype=_F64, device=dev)
     p_d = _dev_i32(p, dev)
+    if H.realified:  # the realified ID matrices have (source, component) rows
+        p = 2 * p
+    ldA = _even(p.max())
+    A = torch.zeros((count, mm, ldA), dtype=_F64, device=dev)
     _lib.call("vief_gen_idmat", prob, 0, _lib.ptr(L.rows), mm, _lib.ptr(L.m_d), mm,
               _lib.ptr(src_xy), _lib.ptr(src_g), pmax, _lib.ptr(p_d), pmax, _lib.ptr(A),
               g * mm * ldA, ldA, nb, st())
@@ -354,7 +383,7 @@ def _compress_level(H, L, pad, seed):
     rank = torch.zeros(count, dtype=_I32, device=dev)
     perm = torch.zeros((count, mm), dtype=_I32, device=dev)
     T = torch.zeros((count, mm, mm), dtype=_F64, device=dev)
-    d = _lib.IdDesc(_lib.ptr(A), mm * ldA, ldA, _lib.ptr(pv), _lib.ptr(mv), pmax, mm, count, g,
+    d = _lib.IdDesc(_lib.ptr(A), mm * ldA, ldA, _lib.ptr(pv), _lib.ptr(mv), int(p.max()), mm, count, g,
                     float(H.eps), _lib.ptr(rank), _lib.ptr(perm), _lib.ptr(T), mm * mm, mm,
                     int(seed) * 1000003 + L.lv, int(getattr(H, "_force_blocked", 0)))
     _lib.call("vief_id_batched", ctypes.byref(d), st())
@@ -367,6 +396,7 @@ def _compress_level(H, L, pad, seed):
     L.nT_d = _dev_i32(nT, dev)
     L.perm_r = perm[0::g].contiguous()
     L.perm_c = perm[1::g].contiguous() if g == 2 else L.perm_r
+    _lib.prof_mark("py.T+skel")
     # T compacted to [item, col (m-k), row (k)] with ld = kmax
     L.Tr = torch.zeros((nb, L.ntmax, L.kmax), dtype=_F64, device=dev)
     _lib.copy2d(T, g * mm * mm, mm, L.Tr, L.ntmax * L.kmax, L.kmax, L.k_d, L.kmax, L.nT_d,
@@ -393,11 +423,17 @@ def compress_outer(spec, grid, tree, eps, opts, quad=PLAIN, spill=None):
     (solver_dense.py:234-272).  `spill` is accepted for signature
     compatibility; every block stays in HBM."""
     H = Hss2dMatrix(spec, grid, tree, eps, opts, quad)
-    pad = opts.resolved_proxy_layers(spec)
+    return compress_levels(H)
+
+
+def compress_levels(H):
+    """Run the per-level compression over every level H factors (fine to
+    coarse); sharded objects (distributed.py) call this directly."""
+    pad = H.opts.resolved_proxy_layers(H.spec)
     _mark("compress:start")
-    for L in reversed(H.levels):
+    for L in reversed(_real_levels(H)):
         _lib.prof_prefix(f"L{L.lv:02d}.")
-        _compress_level(H, L, pad, opts.seed)
+        _compress_level(H, L, pad, H.opts.seed)
         _mark(f"compress:{L.lv}")
     return H
 
@@ -420,6 +456,7 @@ def _invert_level(inv, L):
     H = inv.H
     dev = H.device
     nb, mm = L.nb, L.mmax
+    _lib.prof_mark("py.F_assemble")
     F = torch.zeros((nb, mm, mm), dtype=_F64, device=dev)
     if L.leaf:
         F.copy_(L.D)
@@ -446,6 +483,7 @@ def _invert_level(inv, L):
     kk = L.kmax
     k = L.k.astype(np.int64)
     base = np.arange(nb, dtype=np.int64)
+    _lib.prof_mark("py.W")
     # W = F^{-1} L = Fp[:, :k] + Fp[:, k:] Tr^T,  Fp = F^{-1}[:, perm_r]
     Fp = torch.empty((nb, mm, mm), dtype=_F64, device=dev)
     _lib.gather_cols(F, mm * mm, mm, L.perm_r, mm, Fp, mm * mm, mm, L.m_d, mm, L.m_d, mm, nb)
@@ -455,6 +493,7 @@ def _invert_level(inv, L):
               sB=L.ntmax * kk, sC=kk * mm, tB=1, alpha=1.0, beta=1.0, batch=nb,
               Mb=L.m_d, Nb=L.k_d, Kb=L.nT_d, Aptr=_ptrs(Fp, base * mm * mm + k * mm, dev))
     del Fp
+    _lib.prof_mark("py.G")
     # G = R W = Wp[:k] + Tc Wp[k:],  Wp = W[perm_c, :]
     Wp = torch.empty((nb, kk, mm), dtype=_F64, device=dev)
     _lib.gather_rows(W, kk * mm, mm, L.perm_c, mm, Wp, kk * mm, mm, L.m_d, mm, L.k_d, kk, nb)
@@ -469,6 +508,7 @@ def _invert_level(inv, L):
     _check_singular(H, L, pmin, pmax, "E")
     L.E = G
     L.W = W
+    _lib.prof_mark("py.C")
     # C = E R: Cp = [E, E Tc] then columns scattered to perm_c
     Cp = torch.zeros((nb, mm, kk), dtype=_F64, device=dev)
     _lib.copy2d(G, kk * kk, kk, Cp, mm * kk, kk, L.k_d, kk, L.k_d, kk, nb)
@@ -487,7 +527,7 @@ class DenseBlockInverse:
     def __init__(self, H):
         self.H = H
         self.tree = H.tree
-        levels = H.levels
+        levels = _real_levels(H)
         ids = lambda pred: [int(i) for L in levels if pred(L) for i in L.ids]
         self.E = _BoxView(self, lambda i: self._get(i, "E"), lambda: ids(lambda L: L.lv > 0))
         self.Finv = _BoxView(self, lambda i: self._get(i, "Finv"), lambda: ids(lambda L: True))
@@ -504,7 +544,7 @@ class DenseBlockInverse:
         """Bytes of the factors this object holds (F^{-1}, E, W, C, T)."""
         tot = 0
         H = self.H
-        for L in H.levels:
+        for L in _real_levels(H):
             m = L.m.astype(np.int64)
             tot += int((m * m).sum()) * 8
             if L.lv > 0:
@@ -518,7 +558,7 @@ class DenseBlockInverse:
         F + E + T (solver_dense.py:284-291)."""
         tot = 0
         H = self.H
-        for L in H.levels:
+        for L in _real_levels(H):
             m = L.m.astype(np.int64)
             tot += int((m * m).sum()) * 8
             if L.lv > 0:
@@ -535,7 +575,7 @@ def invert_dense_block(H, spill=None, free_source=False):
     (solver_dense.py:332-368).  `free_source` drops D/B once consumed."""
     inv = DenseBlockInverse(H)
     _mark("invert:start")
-    for L in reversed(H.levels):
+    for L in reversed(_real_levels(H)):
         _lib.prof_prefix(f"L{L.lv:02d}.")
         _invert_level(inv, L)
         _mark(f"invert:{L.lv}")
@@ -550,20 +590,39 @@ def invert_dense_block(H, spill=None, free_source=False):
 # ---------------------------------------------------------------------------
 # solve sweeps
 
-def _as_device_rhs(x, n, device):
-    """(N,) or (N, r) numpy/torch -> (r, N) float64 device tensor (column-major N x r)."""
+def _as_device_rhs(x, n, device, realified=False):
+    """(N,) or (N, r) numpy/torch -> ((r, N') float64 device tensor, single).
+    Realified (complex) systems interleave (Re, Im) per point: N' = 2N."""
     if isinstance(x, torch.Tensor):
-        t = x.to(device=device, dtype=_F64)
+        if x.is_complex() and not realified:
+            raise TypeError("complex right-hand side for a real system")
+        t = x.to(device=device, dtype=torch.complex128 if realified else _F64)
     else:
         arr = np.asarray(x)
-        if np.iscomplexobj(arr):
-            raise NotImplementedError("complex right-hand sides need the complex128 path")
-        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device)
+        if np.iscomplexobj(arr) and not realified:
+            raise TypeError("complex right-hand side for a real system")
+        dt = np.complex128 if realified else np.float64
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=dt)).to(device)
     single = t.dim() == 1
     t2 = t[:, None] if single else t
     if t2.shape[0] != n:
         raise ValueError(f"rhs has {t2.shape[0]} rows, expected {n}")
-    return t2.t().contiguous(), single
+    tt = t2.t().contiguous()
+    if realified:
+        tt = torch.view_as_real(tt).reshape(tt.shape[0], 2 * n)
+    return tt, single
+
+
+def _from_device(out, like, single, realified):
+    """(r, N') device result -> the caller's layout/type (solver_dense.py:296-329)."""
+    if realified:
+        out = torch.view_as_complex(out.reshape(out.shape[0], -1, 2).contiguous())
+    res = out.t()
+    if isinstance(like, torch.Tensor):
+        res = res.to(like.device)
+        return res[:, 0] if single else res
+    arr = res.cpu().numpy()
+    return arr[:, 0].copy() if single else np.ascontiguousarray(arr)
 
 
 def _level_dn_idx(H, L):
@@ -590,21 +649,25 @@ def _mv(A, sA, lda, X, sx, ldx, Y, sy, ldy, M, K, Mb, Kb, nb, r, alpha, beta):
                   alpha=alpha, beta=beta, batch=nb, Mb=Mb, Kb=Kb)
 
 
-def _apply_device(inv, fd):
-    """fd: (r, N) device tensor -> (r, N) solution (device)."""
-    H = inv.H
+def _real_levels(H):
+    """Levels this object factors (absent levels are None; a 'virtual' level
+    only carries a sharded neighbour's interface data)."""
+    return [L for L in H.levels if L is not None and not getattr(L, "virtual", False)]
+
+
+def _sweep_up(H, fd, phi, ups):
+    """Up sweep (solver_dense.py:303-310): phi = F^{-1} u, ups = C phi = E R phi.
+    ups of a virtual child level must be present in `ups` beforehand."""
     dev = H.device
     r, n = fd.shape
-    levels = H.levels
-    phi, ups = {}, {}
-    for L in reversed(levels):
+    for L in reversed(_real_levels(H)):
         nb, mm = L.nb, L.mmax
         ldv = nb * mm
         U = torch.zeros((r, ldv), dtype=_F64, device=dev)
         if L.leaf:
             _lib.gather_rows(fd, 0, n, L.rows, mm, U, mm, ldv, L.m_d, mm, None, r, nb)
         else:
-            C = levels[L.lv + 1]
+            C = H.levels[L.lv + 1]
             _lib.gather_rows(ups[C.lv], 2 * C.kmax, C.nb * C.kmax, L.cat_idx, mm, U, mm, ldv,
                              L.m_d, mm, None, r, nb)
         Phi = torch.zeros((r, ldv), dtype=_F64, device=dev)
@@ -618,19 +681,32 @@ def _apply_device(inv, fd):
         _mv(L.C, mm * kk, kk, Phi, mm, ldv, Ups, kk, nb * kk, kk, mm, L.k_d, L.m_d, nb, r,
             1.0, 0.0)
         ups[L.lv] = Ups
-    out = torch.zeros((r, n), dtype=_F64, device=dev)
-    for L in levels:
+
+
+def _phi_dn(H, L, phi, r):
+    """phi_dn of level L's boxes: slices of the parent level's result."""
+    P = H.levels[L.lv - 1]
+    kk = L.kmax
+    PD = torch.zeros((r, L.nb * kk), dtype=_F64, device=H.device)
+    _lib.gather_rows(phi[P.lv], 0, P.nb * P.mmax, _level_dn_idx(H, L), kk, PD, kk, L.nb * kk,
+                     L.k_d, kk, None, r, L.nb)
+    return PD
+
+
+def _sweep_down(H, phi, ups, out, pd_top=None):
+    """Down sweep (solver_dense.py:312-328): res = phi - W (ups - E phi_dn),
+    leaves scattered into `out`.  `pd_top` supplies phi_dn of the coarsest
+    level when its parent is factored elsewhere (sharded subtree)."""
+    r, n = out.shape
+    for L in _real_levels(H):
         nb, mm = L.nb, L.mmax
         ldv = nb * mm
         Phi = phi[L.lv]
         if L.lv > 0:
-            P = levels[L.lv - 1]
             kk = L.kmax
-            PD = torch.zeros((r, nb * kk), dtype=_F64, device=dev)
-            _lib.gather_rows(phi[P.lv], 0, P.nb * P.mmax, _level_dn_idx(H, L), kk, PD, kk,
-                             nb * kk, L.k_d, kk, None, r, nb)
+            par = H.levels[L.lv - 1]
+            PD = pd_top if par is None else _phi_dn(H, L, phi, r)
             Ups = ups[L.lv]
-            # d = ups - E phi_dn ; res = phi - W d
             _mv(L.E, kk * kk, kk, PD, kk, nb * kk, Ups, kk, nb * kk, kk, kk, L.k_d, L.k_d, nb, r,
                 -1.0, 1.0)
             _mv(L.W, kk * mm, mm, Ups, kk, nb * kk, Phi, mm, ldv, mm, kk, L.m_d, L.k_d, nb, r,
@@ -638,18 +714,22 @@ def _apply_device(inv, fd):
             del PD
         if L.leaf:
             _lib.scatter_rows(Phi, mm, ldv, L.rows, mm, out, 0, n, L.m_d, mm, None, r, nb)
+
+
+def _apply_device(inv, fd):
+    """fd: (r, N) device tensor -> (r, N) solution (device)."""
+    H = inv.H
+    phi, ups = {}, {}
+    _sweep_up(H, fd, phi, ups)
+    out = torch.zeros_like(fd)
+    _sweep_down(H, phi, ups, out)
     return out
 
 
 def _apply(inv, f):
     H = inv.H
-    fd, single = _as_device_rhs(f, H.grid.n, H.device)
-    out = _apply_device(inv, fd)
-    res = out.t()
-    if isinstance(f, torch.Tensor):
-        return res[:, 0] if single else res
-    arr = res.cpu().numpy()
-    return arr[:, 0].copy() if single else np.ascontiguousarray(arr)
+    fd, single = _as_device_rhs(f, H.grid.n, H.device, H.realified)
+    return _from_device(_apply_device(inv, fd), f, single, H.realified)
 
 
 def apply_inverse_dense_block(inv, f):
@@ -660,6 +740,8 @@ def apply_inverse_dense_block(inv, f):
 # forward operator (solver_dense.py:143-178)
 
 def _matvec_device(H, xd):
+    if H.sharded:
+        raise NotImplementedError("matvec of a sharded (distributed) compression")
     dev = H.device
     r, n = xd.shape
     levels = H.levels
@@ -774,12 +856,8 @@ def _scatter_add_children(t, L, C, wc, r, dev):
 
 
 def _matvec(H, x):
-    xd, single = _as_device_rhs(x, H.grid.n, H.device)
-    out = _matvec_device(H, xd).t()
-    if isinstance(x, torch.Tensor):
-        return out[:, 0] if single else out
-    arr = out.cpu().numpy()
-    return arr[:, 0].copy() if single else np.ascontiguousarray(arr)
+    xd, single = _as_device_rhs(x, H.grid.n, H.device, H.realified)
+    return _from_device(_matvec_device(H, xd), x, single, H.realified)
 
 
 def hss_matvec(H, x):

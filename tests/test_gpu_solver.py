@@ -266,3 +266,36 @@ def test_torch_device_rhs_roundtrip():
     assert X.is_cuda and X.shape == F.shape
     r = (F - H.matvec(X)).norm() / F.norm()
     assert float(r) <= 1e-9
+
+
+# ---- complex (helmholtz2d), factored in realified form ---------------------
+
+def test_helmholtz_small_inverse():
+    """Port of the reference's test_solver_dense.py:131-144."""
+    P, sd = _api()
+    k = 2 * np.pi * 2
+    spec = P.KernelSpec("helmholtz2d", k=k)
+    grid = P.Grid(18)
+    tree = P.build_tree(grid, 81)
+    H = sd.compress_outer(spec, grid, tree, 1e-10, P.SolverOptions())
+    A = dense_matrix(spec, grid)
+    assert np.linalg.norm(H.densify() - A) / np.linalg.norm(A) <= 1e-8
+    inv = sd.invert_dense_block(H)
+    rng = np.random.default_rng(6)
+    v = rng.standard_normal(grid.n) + 1j * rng.standard_normal(grid.n)
+    x = inv.apply(v)
+    assert x.dtype == np.complex128
+    assert np.linalg.norm(A @ x - v) / np.linalg.norm(v) <= 1e-8
+
+
+def test_helmholtz_matches_reference_solution():
+    P, sd = _api()
+    g = np.load(os.path.join(G, "solve_helm18.npz"))
+    spec = P.KernelSpec("helmholtz2d", k=2 * np.pi * 2)
+    grid = P.Grid(18)
+    tree = P.build_tree(grid, 81)
+    H = sd.compress_outer(spec, grid, tree, 1e-10, P.SolverOptions(eps=1e-10, leaf_size=81))
+    inv = sd.invert_dense_block(H)
+    x = inv.apply(g["f"])
+    assert np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"]) <= 1e-9
+    assert np.linalg.norm(g["f"] - H.matvec(x)) / np.linalg.norm(g["f"]) <= 1e-9

@@ -43,5 +43,11 @@ if os.environ.get("VF_PROF"):
     H = sd.compress_outer(spec, grid, tree, 1e-10, opts, CELL)
     inv = sd.invert_dense_block(H)
     torch.cuda.synchronize(); t1 = time.time()
+    _lib.prof_prefix("")
+    _lib.prof_mark("solve1")
+    x = inv.apply(torch.randn(grid.n, 1, dtype=torch.float64, device="cuda"))
+    _lib.prof_mark("solve256")
+    x = inv.apply(torch.randn(grid.n, 256, dtype=torch.float64, device="cuda"))
+    _lib.prof_flush()
     print(f"profiled factor {t1-t0:.3f}s")
     print(_lib.prof_report())
