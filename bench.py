@@ -192,14 +192,111 @@ def _algorithmic_work(H):
     return id_fl, lu_fl, solve_bytes, solve_fl
 
 
+def run_sharded(a):
+    """N > 1 GPUs: one 1024^2 problem, subtree-sharded (distributed.py): each
+    rank factors its subtree, the top levels run on rank 0 from interface data
+    gathered over NCCL.  Strong scaling (the total work is fixed)."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    from paper_1303_5466_b200 import CELL, Grid, KernelSpec, SolverOptions, build_tree, make_field, _lib
+    from paper_1303_5466_b200.distributed import ShardedInverse, TorchComm
+    comm = TorchComm()
+    n, nrhs = a.n, a.nrhs
+    N = n * n
+    spec = KernelSpec("laplace2d", b_field=make_field("centre_bump", scale=math.pi / 2),
+                      c_field=make_field("one"))
+    grid = Grid(n)
+    opts = SolverOptions(eps=1e-10, leaf_size=64, k_cut=None)
+    gen = torch.Generator(device="cuda").manual_seed(1234)
+    Ft = torch.randn((nrhs, N), dtype=torch.float64, device="cuda", generator=gen)
+    fac, sol = [], []
+
+    def barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(record=False):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        inv = ShardedInverse(spec, grid, build_tree(grid, 64), 1e-10, opts, CELL, world, comm=comm)
+        ev[1].record()
+        X = inv.apply_device(Ft)
+        ev[2].record()
+        if record:
+            torch.cuda.synchronize()
+            fac.append(ev[0].elapsed_time(ev[1]))
+            sol.append(ev[1].elapsed_time(ev[2]))
+        return inv, X
+
+    for _ in range(a.warmup):
+        inv, X = step()
+        del inv, X
+    barrier()
+    L0 = _lib.launch_count()
+    with Clocks(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record()
+        for i in range(a.steps):
+            inv, X = step(record=True)
+            if i < a.steps - 1:
+                del inv, X
+        e1.record()
+        barrier()
+    launches = _lib.launch_count() - L0
+    t = torch.tensor([e0.elapsed_time(e1) / a.steps, statistics.mean(fac), statistics.mean(sol)],
+                     device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, tf, ts = (float(v) for v in t.tolist())
+    local_bytes = inv.nbytes_local()
+    del inv, X
+    torch.cuda.empty_cache()
+    out = {"metric": METRIC, "value": N / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": dict(_config(n, nrhs, world), parallelism=f"subtree shards x{world} + "
+                          "top levels on rank 0 (NCCL gathers)"),
+           "factor_s": tf / 1e3, "solve_s": ts / 1e3, "factor_bytes_rank": local_bytes,
+           "gpu_launches": int(launches), "clocks": clk.summary()}
+    if not a.no_e2e:
+        Fh = Ft.t().contiguous().cpu().pin_memory()
+
+        def e2e_step():
+            inv2 = ShardedInverse(spec, grid, build_tree(grid, 64), 1e-10, opts, CELL, world,
+                                  comm=comm)
+            Xh = inv2.apply(Fh)
+            torch.cuda.synchronize()
+            del inv2, Xh
+
+        for _ in range(a.warmup):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            e2e_step()
+        barrier()
+        te = torch.tensor([(time.perf_counter() - t0) / a.steps], device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = float(te.item())
+        out["e2e"] = {"value": N / te, "unit": UNIT, "h2d_bytes_per_step": int(N * nrhs * 8),
+                      "d2h_bytes_per_step": int(N * nrhs * 8), "ms_per_step": te * 1e3,
+                      "api": "distributed.ShardedInverse(...).apply(host RHS)"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(a):
     import torch
     rank, world, local = _dist()
+    if world > 1:
+        return run_sharded(a)
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
     from paper_1303_5466_b200 import (CELL, Grid, KernelSpec, SolverOptions, build_tree,
                                       make_field, _lib)
     from paper_1303_5466_b200 import solver_dense as sd

@@ -162,7 +162,8 @@ class ShardedInverse:
             sd.compress_levels(Hl)
             invl = sd.invert_dense_block(Hl)
             self.local[g] = (Hl, invl)
-            payloads[g] = _interface_payload(Hl, invl, s)
+            if world > 1:
+                payloads[g] = _interface_payload(Hl, invl, s)
         self.dev = next(iter(self.local.values()))[0].device
         self.realified = next(iter(self.local.values()))[0].realified
         self.top = None

@@ -310,10 +310,12 @@ def _compress_level(H, L, pad, seed):
     # work rows / cols
     if L.leaf:
         own = H.tree.owned_level(L.lv)[L.sl[0]:L.sl[1]]
+        cnt = (own >= 0).sum(axis=1)          # ragged leaves: valid points first
         own = np.where(own >= 0, own, 0)
         if H.realified:  # unknowns u = 2*point + component, interleaved per point
             own = np.stack([2 * own, 2 * own + 1], axis=-1).reshape(own.shape[0], -1)
-        L.m = np.full(nb, own.shape[1], dtype=np.int32)
+            cnt = 2 * cnt
+        L.m = cnt.astype(np.int32)
         L.mmax = int(L.m.max())
         L.rows = _dev_i32(own, dev)
         L.cols = L.rows
