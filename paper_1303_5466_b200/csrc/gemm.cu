@@ -32,80 +32,65 @@ __device__ __forceinline__ GemmItem gemm_item(const vief_gemm_desc& d, int b) {
   return it;
 }
 
-// load one BK x BMT tile of op(A) into As[k][m] (row stride BMT + PAD)
-template <int BMT>
-__device__ __forceinline__ void load_a(double* As, const double* A, int lda, int trans, int m0,
-                                       int k0, int M, int K, int tid) {
-  constexpr int LD = BMT + PAD, KQ = 128 / BMT, N_IT = BMT * BK / 128;
-  if (!trans) {  // A(m,k) = A[k*lda + m], contiguous in m
-    const int m = tid % BMT, kq = tid / BMT;
-    const int gm = m0 + m;
-#pragma unroll
-    for (int i = 0; i < N_IT; ++i) {
-      const int k = kq + KQ * i, gk = k0 + k;
-      const bool v = gm < M && gk < K;
-      cp_async8(As + k * LD + m, v ? A + (long long)gk * lda + gm : A, v);
-    }
-  } else {       // op(A)(m,k) = A[m*lda + k], contiguous in k
-    const int k = tid % BK, mq = tid / BK;
-    const int gk = k0 + k;
-#pragma unroll
-    for (int i = 0; i < N_IT; ++i) {
-      const int m = mq + 8 * i, gm = m0 + m;
-      const bool v = gm < M && gk < K;
-      cp_async8(As + k * LD + m, v ? A + (long long)gm * lda + gk : A, v);
-    }
-  }
-}
+// Shared-memory tile layouts follow the global contiguity of each operand so
+// that both the cp.async stores and the DMMA fragment loads are bank-conflict
+// free: an operand contiguous in its outer dimension (A not transposed: m;
+// B transposed: n) is staged k-major ([k][outer], stride OUTER+4); an operand
+// contiguous in k is staged outer-major ([outer][k], stride BK+4 = 20).  Both
+// strides are 4 mod 16 doubles, so the 16 lanes of a half warp (g = 0..3,
+// t = 0..3) hit distinct 8-byte banks.
+template <int OUT, bool KCONTIG>
+struct Tile {
+  static constexpr int LD = KCONTIG ? BK + PAD : OUT + PAD;
+  static constexpr int SIZE = KCONTIG ? OUT * (BK + PAD) : BK * (OUT + PAD);
+  __device__ __forceinline__ static int at(int o, int k) { return KCONTIG ? o * LD + k : k * LD + o; }
+};
 
-// load one BK x BNT tile of op(B) into Bs[k][n]
-template <int BNT>
-__device__ __forceinline__ void load_b(double* Bs, const double* B, int ldb, int trans, int n0,
-                                       int k0, int N, int K, int tid) {
-  constexpr int LD = BNT + PAD, KQ = 128 / BNT, N_IT = BNT * BK / 128;
-  if (!trans) {  // B(k,n) = B[n*ldb + k], contiguous in k
-    const int k = tid % BK, nq = tid / BK;
+// load one BK x OUT tile of an operand whose element (o, k) lives at
+// src[k*ld + o] (outer-contiguous) or src[o*ld + k] (k-contiguous)
+template <int OUT, bool KCONTIG>
+__device__ __forceinline__ void load_tile(double* S, const double* src, int ld, int o0, int k0,
+                                          int O, int K, int tid) {
+  constexpr int N_IT = OUT * BK / 128;
+  if (!KCONTIG) {
+    constexpr int KQ = 128 / OUT > 0 ? 128 / OUT : 1;
+    if (OUT <= 128) {
+      const int o = tid % OUT, kq = tid / OUT;
+      const int go = o0 + o;
+#pragma unroll
+      for (int i = 0; i < N_IT; ++i) {
+        const int k = kq + KQ * i, gk = k0 + k;
+        const bool v = go < O && gk < K;
+        cp_async8(S + Tile<OUT, false>::at(o, k), v ? src + (long long)gk * ld + go : src, v);
+      }
+    }
+  } else {
+    const int k = tid % BK, oq = tid / BK;
     const int gk = k0 + k;
 #pragma unroll
     for (int i = 0; i < N_IT; ++i) {
-      const int n = nq + 8 * i, gn = n0 + n;
-      const bool v = gn < N && gk < K;
-      cp_async8(Bs + k * LD + n, v ? B + (long long)gn * ldb + gk : B, v);
-    }
-  } else {       // op(B)(k,n) = B[k*ldb + n], contiguous in n
-    if (KQ >= 1) {
-      const int n = tid % BNT, kq = tid / BNT;
-      const int gn = n0 + n;
-#pragma unroll
-      for (int i = 0; i < N_IT; ++i) {
-        const int k = kq + (KQ > 0 ? KQ : 1) * i, gk = k0 + k;
-        const bool v = gn < N && gk < K;
-        cp_async8(Bs + k * LD + n, v ? B + (long long)gk * ldb + gn : B, v);
-      }
-    } else {     // BNT > 128: each thread covers several n per k row
-#pragma unroll
-      for (int i = 0; i < N_IT; ++i) {
-        const int e = tid + 128 * i, n = e % BNT, k = e / BNT;
-        const int gn = n0 + n, gk = k0 + k;
-        const bool v = gn < N && gk < K;
-        cp_async8(Bs + k * LD + n, v ? B + (long long)gk * ldb + gn : B, v);
-      }
+      const int o = oq + 8 * i, go = o0 + o;
+      const bool v = go < O && gk < K;
+      cp_async8(S + Tile<OUT, true>::at(o, k), v ? src + (long long)go * ld + gk : src, v);
     }
   }
 }
 
 // CTA tile BMT x BNT with 4 warps, each a 32 x 32 warp tile of 4 x 4 m8n8k4
 // DMMA fragments.  (64,64): 2x2 warps; (32,128): 1x4 warps for skinny M.
-template <int BMT, int BNT>
+// TA/TB: op(A) = A^T / op(B) = B^T (compile-time: selects the smem layouts).
+template <int BMT, int BNT, bool TA, bool TB>
 __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
-  constexpr int LDA_S = BMT + PAD, LDB_S = BNT + PAD, WN = BNT / 32;
+  using TAt = Tile<BMT, TA>;    // A^T stored K x M col-major -> contiguous in k
+  using TBt = Tile<BNT, !TB>;   // B stored K x N col-major   -> contiguous in k
+  constexpr int WN = BNT / 32;
   const int b = blockIdx.z;
   GemmItem it = gemm_item(d, b);
   const int m0 = blockIdx.y * BMT, n0 = blockIdx.x * BNT;
   if (m0 >= it.M || n0 >= it.N) return;
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;
-  double* Bs = gsm + STAGES * BK * LDA_S;
+  double* Bs = gsm + STAGES * TAt::SIZE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
   const int g = lane >> 2, t = lane & 3;
@@ -122,8 +107,8 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       if (s < nk) {
-        load_a<BMT>(As + s * BK * LDA_S, it.A, d.lda, d.transA, m0, s * BK, it.M, it.K, tid);
-        load_b<BNT>(Bs + s * BK * LDB_S, it.B, d.ldb, d.transB, n0, s * BK, it.N, it.K, tid);
+        load_tile<BMT, TA>(As + s * TAt::SIZE, it.A, d.lda, m0, s * BK, it.M, it.K, tid);
+        load_tile<BNT, !TB>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, s * BK, it.N, it.K, tid);
       }
       cp_async_commit();
     }
@@ -133,19 +118,19 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
       const int nxt = kt + STAGES - 1;
       if (nxt < nk) {
         const int s = nxt % STAGES;
-        load_a<BMT>(As + s * BK * LDA_S, it.A, d.lda, d.transA, m0, nxt * BK, it.M, it.K, tid);
-        load_b<BNT>(Bs + s * BK * LDB_S, it.B, d.ldb, d.transB, n0, nxt * BK, it.N, it.K, tid);
+        load_tile<BMT, TA>(As + s * TAt::SIZE, it.A, d.lda, m0, nxt * BK, it.M, it.K, tid);
+        load_tile<BNT, !TB>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, nxt * BK, it.N, it.K, tid);
       }
       cp_async_commit();
-      const double* as = As + (kt % STAGES) * BK * LDA_S;
-      const double* bs = Bs + (kt % STAGES) * BK * LDB_S;
+      const double* as = As + (kt % STAGES) * TAt::SIZE;
+      const double* bs = Bs + (kt % STAGES) * TBt::SIZE;
 #pragma unroll
       for (int kk = 0; kk < BK; kk += 4) {
         double af[4], bf[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = as[(kk + t) * LDA_S + wm + 8 * i + g];
+        for (int i = 0; i < 4; ++i) af[i] = as[TAt::at(wm + 8 * i + g, kk + t)];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = bs[(kk + t) * LDB_S + wn + 8 * j + g];
+        for (int j = 0; j < 4; ++j) bf[j] = bs[TBt::at(wn + 8 * j + g, kk + t)];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -172,6 +157,29 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
       }
     }
   }
+}
+
+template <int BMT, int BNT, bool TA, bool TB>
+static int launch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
+  constexpr int smem = STAGES * (Tile<BMT, TA>::SIZE + Tile<BNT, !TB>::SIZE) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    VF_CUDA(cudaFuncSetAttribute(k_dgemm<BMT, BNT, TA, TB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  dim3 grid(cdiv(d->N, BNT), cdiv(d->M, BMT), d->batch);
+  if (grid.y > 65535) { set_error("dgemm: M too large"); return VF_EARG; }
+  k_dgemm<BMT, BNT, TA, TB><<<grid, 128, smem, st>>>(*d);
+  return VF_OK;
+}
+
+template <int BMT, int BNT>
+static int dispatch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
+  if (!d->transA && !d->transB) return launch_gemm<BMT, BNT, false, false>(d, st);
+  if (!d->transA && d->transB) return launch_gemm<BMT, BNT, false, true>(d, st);
+  if (d->transA && !d->transB) return launch_gemm<BMT, BNT, true, false>(d, st);
+  return launch_gemm<BMT, BNT, true, true>(d, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -257,22 +265,10 @@ using namespace vf;
 extern "C" int vief_dgemm_batched(const vief_gemm_desc* d, void* stream) {
   if (!d || d->batch <= 0 || d->M <= 0 || d->N <= 0) return VF_OK;
   if (d->batch > 65535) { set_error("dgemm: batch %d > 65535", d->batch); return VF_EARG; }
-  static bool attr = false;
-  constexpr int smemA = STAGES * BK * ((64 + PAD) + (64 + PAD)) * sizeof(double);
-  constexpr int smemB = STAGES * BK * ((32 + PAD) + (128 + PAD)) * sizeof(double);
-  if (!attr) {
-    VF_CUDA(cudaFuncSetAttribute(k_dgemm<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemA));
-    VF_CUDA(cudaFuncSetAttribute(k_dgemm<32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemB));
-    attr = true;
-  }
-  if (d->M <= 32) {  // skinny: 32 x 128 tiles (no idle DMMA rows)
-    dim3 grid(cdiv(d->N, 128), cdiv(d->M, 32), d->batch);
-    k_dgemm<32, 128><<<grid, 128, smemB, (cudaStream_t)stream>>>(*d);
-  } else {
-    dim3 grid(cdiv(d->N, 64), cdiv(d->M, 64), d->batch);
-    if (grid.y > 65535) { set_error("dgemm: M too large"); return VF_EARG; }
-    k_dgemm<64, 64><<<grid, 128, smemA, (cudaStream_t)stream>>>(*d);
-  }
+  cudaStream_t st = (cudaStream_t)stream;
+  // skinny M: 32 x 128 tiles (no idle DMMA rows); otherwise 64 x 64
+  const int rc = d->M <= 32 ? dispatch_gemm<32, 128>(d, st) : dispatch_gemm<64, 64>(d, st);
+  if (rc) return rc;
   ++g_launches;
   VF_LAUNCH_CHECK("k_dgemm");
   return VF_OK;

@@ -2,7 +2,7 @@
 // Gauss-Jordan), replacing lu_factor_checked + lu_solve(., I)
 // (dense_core.py:222-230, solver_dense.py:361-367).
 //
-// Two-level blocking.  Outer block columns of NBO = 128; inside each, inner
+// Two-level blocking.  Outer block columns of NBO = 256; inside each, inner
 // panels of 32:
 //   inner step on [c0, c0+32) (restricted to the outer block's columns):
 //     1. lu_panel  (cluster of CTAs per item, panels.cu): partial-pivoting LU
@@ -14,11 +14,12 @@
 //     5. A[:, block cols] -= Pw * Rw                           (DMMA GEMM)
 //     6. A[pivot rows, block cols] = Rw
 //   outer step: the block columns now hold X = [.. -P A11^{-1} ..; A11^{-1}]
-//     (128 x 128 pivot block inverse).  Apply the 128 row swaps to the other
+//     (NBO x NBO pivot block inverse).  Apply the NBO row swaps to the other
 //     columns, save their pivot rows R and zero them, then
-//        A[:, other] += X * R                (DMMA GEMM, K = 128)
+//        A[:, other] += X * R                (DMMA GEMM, K = NBO)
 //     which is the Gauss-Jordan update of all other columns at once.
-// Finally columns are interchanged in reverse pivot order.  The pivots are the
+// Finally columns are interchanged in reverse pivot order (one gather).  Row
+// interchanges are applied as (dst, src) permutations of the touched rows.  The pivots are the
 // partial-pivoting pivots of getrf (the trailing Schur complements coincide).
 #include <vector>
 #include "common.cuh"
@@ -29,21 +30,7 @@ namespace vf {
 extern long long g_launches;
 
 constexpr int GJ_NB = 32;    // inner panel
-constexpr int GJ_NBO = 128;  // outer block
-
-// apply row interchanges ipiv[s0..s1) (in order) to columns [col0, col1) of A
-__global__ void k_gj_swap(double* A, long long sA, int lda, int col0, int col1, int s0, int s1,
-                          const int* ipiv, long long sPiv) {
-  const int b = blockIdx.y;
-  const int col = col0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= col1) return;
-  double* a = A + b * sA + (long long)col * lda;
-  const int* pv = ipiv + b * sPiv;
-  for (int s = s0; s < s1; ++s) {
-    int r = pv[s];
-    if (r != s) { double t = a[s]; a[s] = a[r]; a[r] = t; }
-  }
-}
+constexpr int GJ_NBO = 256;  // outer block (K of the big update GEMM)
 
 __global__ void k_gj_prep(double* A, long long sA, int lda, int n, int c0, int nbs, double* Pw,
                           long long sP) {
@@ -72,21 +59,78 @@ __global__ void k_gj_outer_prep(double* A, long long sA, int lda, int n, int C0,
   if (!inblock) *a = 0.0;
 }
 
-__global__ void k_gj_colswap(double* A, long long sA, int lda, int n, const int* ipiv,
-                             long long sPiv) {
-  const int b = blockIdx.y;
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= n) return;
-  double* a = A + b * sA + row;
+// Row interchanges ipiv[s0..s1) as one permutation of the touched rows:
+// scratch (n ints per item) tracks which original row ends at each position;
+// the result is a list of (dst, src) pairs, 2 per interchange.
+__global__ void k_rowperm_build(const int* ipiv, long long sPiv, int s0, int s1, int n,
+                                int* scratch, int2* pairs) {
+  const int b = blockIdx.x, tid = threadIdx.x;
+  int* p = scratch + (long long)b * n;
   const int* pv = ipiv + b * sPiv;
-  for (int s = n - 1; s >= 0; --s) {
-    int c = pv[s];
-    if (c != s) {
-      double t = a[(long long)s * lda];
-      a[(long long)s * lda] = a[(long long)c * lda];
-      a[(long long)c * lda] = t;
+  for (int i = s0 + tid; i < n; i += blockDim.x) p[i] = i;
+  __syncthreads();
+  if (tid == 0)
+    for (int s = s0; s < s1; ++s) {
+      const int r = pv[s];
+      const int t = p[s]; p[s] = p[r]; p[r] = t;
     }
+  __syncthreads();
+  const int ns = s1 - s0;
+  int2* pr = pairs + (long long)b * 2 * GJ_NBO;
+  for (int t = tid; t < ns; t += blockDim.x) {
+    const int s = s0 + t, r = pv[s];
+    pr[t] = make_int2(s, p[s]);
+    pr[ns + t] = r >= s1 ? make_int2(r, p[r]) : make_int2(s, p[s]);
   }
+}
+
+// apply the (dst, src) row permutation to columns [col0, col1): warp per
+// column, all sources read before any destination is written
+__global__ void k_rowperm_apply(double* A, long long sA, int lda, int col0, int col1,
+                                const int2* pairs, int npairs) {
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = col0 + blockIdx.x * 8 + warp;
+  if (col >= col1) return;
+  double* a = A + b * sA + (long long)col * lda;
+  const int2* pr = pairs + (long long)b * 2 * GJ_NBO;
+  double v[2 * GJ_NBO / 32];
+#pragma unroll
+  for (int q = 0; q < 2 * GJ_NBO / 32; ++q) {
+    const int t = lane + 32 * q;
+    if (t < npairs) v[q] = a[pr[t].y];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 2 * GJ_NBO / 32; ++q) {
+    const int t = lane + 32 * q;
+    if (t < npairs) a[pr[t].x] = v[q];
+  }
+}
+
+// final column interchanges (reverse pivot order) as one gather permutation
+__global__ void k_colperm_build(const int* ipiv, long long sPiv, int n, int* content) {
+  const int b = blockIdx.x;
+  int* c = content + (long long)b * n;
+  const int* pv = ipiv + b * sPiv;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) c[j] = j;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = n - 1; s >= 0; --s) {
+      const int r = pv[s];
+      const int t = c[s]; c[s] = c[r]; c[r] = t;
+    }
+}
+
+// dst(:, j) = src(:, content[j])
+__global__ void k_colperm_gather(const double* src, long long sS, int lds, double* dst,
+                                 long long sD, int ldd, int n, const int* content) {
+  const int b = blockIdx.z;
+  const int j = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = content[(long long)b * n + j];
+  dst[b * sD + (long long)j * ldd + i] = src[b * sS + (long long)c * lds + i];
 }
 
 __global__ void k_fill(double* p, long long n, double v) {
@@ -116,6 +160,10 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
   VF_CUDA(cudaMallocAsync(&Xw, sizeof(double) * sX * batch, st));
   VF_CUDA(cudaMallocAsync(&Ro, sizeof(double) * sX * batch, st));
   VF_CUDA(cudaMallocAsync(&ipiv, sizeof(int) * n * batch, st));
+  int* scratch = nullptr;
+  int2* pairs = nullptr;
+  VF_CUDA(cudaMallocAsync(&scratch, sizeof(int) * n * batch, st));
+  VF_CUDA(cudaMallocAsync(&pairs, sizeof(int2) * 2 * NBO * batch, st));
   k_fill<<<cdiv(batch, 256), 256, 0, st>>>(pivmin, batch, INFINITY);
   k_fill<<<cdiv(batch, 256), 256, 0, st>>>(pivmax, batch, 0.0);
   g_launches += 2;
@@ -129,8 +177,10 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
       rc = lu_panel(A, sA, lda, n, c0, nbs, batch, ipiv, n, Ai, nb * nb, pivmin, pivmax, st);
       if (rc) break;
       prof_push(st, "gj.inner");
-      k_gj_swap<<<dim3(cdiv(NB, 128), batch), 128, 0, st>>>(A, sA, lda, C0, C0 + NB, c0, c0 + nbs,
-                                                            ipiv, n);
+      k_rowperm_build<<<batch, 256, 0, st>>>(ipiv, n, c0, c0 + nbs, n, scratch, pairs);
+      k_rowperm_apply<<<dim3(cdiv(NB, 8), batch), 256, 0, st>>>(A, sA, lda, C0, C0 + NB, pairs,
+                                                               2 * nbs);
+      g_launches += 1;
       k_gj_prep<<<dim3(cdiv(n, 32), cdiv(nbs, 8), batch), dim3(32, 8), 0, st>>>(A, sA, lda, n, c0,
                                                                                  nbs, Pw, sPw);
       g_launches += 2;
@@ -154,12 +204,13 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
     if (NB == n) continue;  // single block: nothing outside it
     // ---- outer update of all other columns
     prof_push(st, "gj.outer_prep");
+    k_rowperm_build<<<batch, 256, 0, st>>>(ipiv, n, C0, C0 + NB, n, scratch, pairs);
     if (C0 > 0)
-      k_gj_swap<<<dim3(cdiv(C0, 128), batch), 128, 0, st>>>(A, sA, lda, 0, C0, C0, C0 + NB, ipiv,
-                                                            n);
+      k_rowperm_apply<<<dim3(cdiv(C0, 8), batch), 256, 0, st>>>(A, sA, lda, 0, C0, pairs, 2 * NB);
     if (n - C0 - NB > 0)
-      k_gj_swap<<<dim3(cdiv(n - C0 - NB, 128), batch), 128, 0, st>>>(A, sA, lda, C0 + NB, n, C0,
-                                                                     C0 + NB, ipiv, n);
+      k_rowperm_apply<<<dim3(cdiv(n - C0 - NB, 8), batch), 256, 0, st>>>(A, sA, lda, C0 + NB, n,
+                                                                          pairs, 2 * NB);
+    g_launches += 1;
     k_gj_outer_prep<<<dim3(cdiv(NB, 32), cdiv(n, 8), batch), dim3(32, 8), 0, st>>>(
         A, sA, lda, n, C0, NB, Ro, sX, NBO);
     g_launches += 3;
@@ -181,10 +232,18 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
     }
   }
   prof_push(st, "gj.colswap");
-  if (rc == VF_OK) {
-    k_gj_colswap<<<dim3(cdiv(n, 128), batch), 128, 0, st>>>(A, sA, lda, n, ipiv, n);
-    ++g_launches;
-    VF_LAUNCH_CHECK("k_gj_colswap");
+  if (rc == VF_OK) {  // column interchanges as one gather into a temporary, copied back
+    double* tmp = nullptr;
+    VF_CUDA(cudaMallocAsync(&tmp, sizeof(double) * (size_t)n * n * batch, st));
+    k_colperm_build<<<batch, 256, 0, st>>>(ipiv, n, n, scratch);
+    k_colperm_gather<<<dim3(cdiv(n, 128), n, batch), 128, 0, st>>>(A, sA, lda, tmp,
+                                                                     (long long)n * n, n, n,
+                                                                     scratch);
+    g_launches += 2;
+    VF_LAUNCH_CHECK("gj colperm");
+    rc = vief_copy2d(tmp, (long long)n * n, nullptr, n, A, sA, nullptr, lda, nullptr, n, nullptr,
+                     n, batch, st);
+    cudaFreeAsync(tmp, st);
   }
   prof_flush(st);
   cudaFreeAsync(Pw, st);
@@ -193,5 +252,7 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
   cudaFreeAsync(Xw, st);
   cudaFreeAsync(Ro, st);
   cudaFreeAsync(ipiv, st);
+  cudaFreeAsync(scratch, st);
+  cudaFreeAsync(pairs, st);
   return rc;
 }

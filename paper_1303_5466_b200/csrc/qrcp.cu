@@ -688,7 +688,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.tn0 = buf.get<double>((size_t)maxm * count);
     S.flag = buf.get<int>((size_t)maxm * count);
     S.Rt = buf.get<double>((size_t)HB * HB * count);
-    S.D = maxm >= 2048 ? 4 : (maxm >= 512 ? 2 : 1);
+    S.D = maxm >= 4096 ? 8 : (maxm >= 2048 ? 4 : (maxm >= 512 ? 2 : 1));
     S.Qw = buf.get<double>((size_t)maxp * HB * S.D * count);
     S.G = buf.get<double>((size_t)HB * HB * S.D * count);
     S.work = nullptr;
