@@ -9,6 +9,7 @@
 // GEMV: one pass over each matrix (HBM-streaming), column-major A read with
 // coalesced 8-byte loads along rows, fixed-order reductions (bitwise
 // deterministic, as DenseBlockInverse.apply requires, solver_dense.py:293-329).
+#include <algorithm>
 #include "common.cuh"
 #include "../../include/vief_b200.h"
 
@@ -79,15 +80,23 @@ __device__ __forceinline__ void load_tile(double* S, const double* src, int ld, 
 // CTA tile BMT x BNT with 4 warps, each a 32 x 32 warp tile of 4 x 4 m8n8k4
 // DMMA fragments.  (64,64): 2x2 warps; (32,128): 1x4 warps for skinny M.
 // TA/TB: op(A) = A^T / op(B) = B^T (compile-time: selects the smem layouts).
+//
+// Split-K (ksplit > 1, for few output tiles over a long K): grid z = item *
+// ksplit + chunk; chunk s covers k in [s*kchunk, (s+1)*kchunk) and writes
+// alpha * partial to ws[z] (M x N, ld M of the descriptor); k_splitk_reduce
+// then sums the chunks in fixed order (deterministic) and applies beta.
 template <int BMT, int BNT, bool TA, bool TB>
-__global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
+__global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d, int ksplit, int kchunk,
+                                               double* ws) {
   using TAt = Tile<BMT, TA>;    // A^T stored K x M col-major -> contiguous in k
   using TBt = Tile<BNT, !TB>;   // B stored K x N col-major   -> contiguous in k
   constexpr int WN = BNT / 32;
-  const int b = blockIdx.z;
+  const int b = blockIdx.z / ksplit, chunk = blockIdx.z % ksplit;
   GemmItem it = gemm_item(d, b);
   const int m0 = blockIdx.y * BMT, n0 = blockIdx.x * BNT;
   if (m0 >= it.M || n0 >= it.N) return;
+  const int kbeg = chunk * kchunk;
+  const int kend = ksplit > 1 ? min(it.K, kbeg + kchunk) : it.K;
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;
   double* Bs = gsm + STAGES * TAt::SIZE;
@@ -102,13 +111,13 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int nk = (it.K + BK - 1) / BK;
+  const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
   if (nk > 0 && d.alpha != 0.0) {
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       if (s < nk) {
-        load_tile<BMT, TA>(As + s * TAt::SIZE, it.A, d.lda, m0, s * BK, it.M, it.K, tid);
-        load_tile<BNT, !TB>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, s * BK, it.N, it.K, tid);
+        load_tile<BMT, TA>(As + s * TAt::SIZE, it.A, d.lda, m0, kbeg + s * BK, it.M, kend, tid);
+        load_tile<BNT, !TB>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, kbeg + s * BK, it.N, kend, tid);
       }
       cp_async_commit();
     }
@@ -118,8 +127,8 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
       const int nxt = kt + STAGES - 1;
       if (nxt < nk) {
         const int s = nxt % STAGES;
-        load_tile<BMT, TA>(As + s * TAt::SIZE, it.A, d.lda, m0, nxt * BK, it.M, it.K, tid);
-        load_tile<BNT, !TB>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, nxt * BK, it.N, it.K, tid);
+        load_tile<BMT, TA>(As + s * TAt::SIZE, it.A, d.lda, m0, kbeg + nxt * BK, it.M, kend, tid);
+        load_tile<BNT, !TB>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, kbeg + nxt * BK, it.N, kend, tid);
       }
       cp_async_commit();
       const double* as = As + (kt % STAGES) * TAt::SIZE;
@@ -140,6 +149,35 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
     cp_async_wait<0>();
   }
   // epilogue
+  if (ksplit > 1) {
+    double* W = ws + (long long)blockIdx.z * d.M * d.N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gm = m0 + wm + 8 * i + g;
+      if (gm >= it.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int gn = n0 + wn + 8 * j + 2 * t + e;
+          if (gn < it.N) W[(long long)gn * d.M + gm] = d.alpha * acc[i][j][e];
+        }
+    }
+    return;
+  }
+  // all C loads are issued before any store (no load waits behind a store)
+  double cv[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + wm + 8 * i + g;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gn = n0 + wn + 8 * j + 2 * t + e;
+        cv[i][j][e] = (use_c && gm < it.M && gn < it.N) ? it.C[(long long)gn * d.ldc + gm] : 0.0;
+      }
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int gm = m0 + wm + 8 * i + g;
@@ -150,12 +188,30 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d) {
       for (int e = 0; e < 2; ++e) {
         const int gn = n0 + wn + 8 * j + 2 * t + e;
         if (gn >= it.N) continue;
-        double* c = it.C + (long long)gn * d.ldc + gm;
         double v = d.alpha * acc[i][j][e];
-        if (use_c) v = fma(d.beta, *c, v);
-        *c = v;
+        if (use_c) v = fma(d.beta, cv[i][j][e], v);
+        it.C[(long long)gn * d.ldc + gm] = v;
       }
     }
+  }
+}
+
+// C(item) = sum_s ws[item*ksplit + s] + beta C, chunks in fixed order
+__global__ void k_splitk_reduce(vief_gemm_desc d, int ksplit, const double* ws) {
+  const int b = blockIdx.y;
+  GemmItem it = gemm_item(d, b);
+  const long long mn = (long long)it.M * it.N;
+  const long long stride = (long long)d.M * d.N;
+  const double* W = ws + (long long)b * ksplit * stride;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < mn;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(idx % it.M), n = (int)(idx / it.M);
+    const long long o = (long long)n * d.M + m;
+    double v = W[o];
+    for (int s = 1; s < ksplit; ++s) v += W[s * stride + o];
+    double* c = it.C + (long long)n * d.ldc + m;
+    if (d.beta != 0.0) v = fma(d.beta, *c, v);
+    *c = v;
   }
 }
 
@@ -168,9 +224,29 @@ static int launch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  dim3 grid(cdiv(d->N, BNT), cdiv(d->M, BMT), d->batch);
+  const long long tiles = (long long)cdiv(d->N, BNT) * cdiv(d->M, BMT) * d->batch;
+  int ksplit = 1, kchunk = d->K;
+  if (tiles < 148 && d->K >= 1024) {  // too few tiles to fill the GPU: split K
+    ksplit = (int)std::min<long long>(d->K / 256, std::max<long long>(1, 296 / tiles));
+    ksplit = std::min(ksplit, 65535 / d->batch);
+    if (ksplit > 1) kchunk = cdiv(cdiv(d->K, ksplit), BK) * BK;
+    if (ksplit > 1) ksplit = cdiv(d->K, kchunk);
+  }
+  dim3 grid(cdiv(d->N, BNT), cdiv(d->M, BMT), d->batch * ksplit);
   if (grid.y > 65535) { set_error("dgemm: M too large"); return VF_EARG; }
-  k_dgemm<BMT, BNT, TA, TB><<<grid, 128, smem, st>>>(*d);
+  double* ws = nullptr;
+  if (ksplit > 1) {
+    VF_CUDA(cudaMallocAsync(&ws, sizeof(double) * (size_t)d->M * d->N * d->batch * ksplit, st));
+  }
+  k_dgemm<BMT, BNT, TA, TB><<<grid, 128, smem, st>>>(*d, ksplit, kchunk, ws);
+  if (ksplit > 1) {
+    const long long mn = (long long)d->M * d->N;
+    dim3 rg((unsigned)std::min<long long>(cdiv((int)std::min<long long>(mn, 1 << 30), 256), 1024),
+            d->batch);
+    k_splitk_reduce<<<rg, 256, 0, st>>>(*d, ksplit, ws);
+    ++g_launches;
+    cudaFreeAsync(ws, st);
+  }
   return VF_OK;
 }
 

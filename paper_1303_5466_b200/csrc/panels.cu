@@ -15,6 +15,9 @@
 //                    Q = (I - V T V^T) [I;0] in WY form (one more barrier)
 //   k_select_cl      QRCP on the sketch Y(:, J:m) choosing bs pivots -> swap list
 #include <cooperative_groups.h>
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 #include "common.cuh"
 #include "panels.cuh"
 
@@ -185,6 +188,7 @@ __global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long s
   // Gram exchange lives in dynamic shared memory after the panel slice
   __shared__ double tau[PNB], Rl[PNB][PNB + 1], w[PNB], Tm[PNB][PNB + 1], Mm[PNB][PNB + 1];
   __shared__ double red[32];
+  __shared__ double Sp[16][PNB];
   const int r0 = cr * rows_per, r1 = min(p, r0 + rows_per), nr = max(r1 - r0, 0);
   const int ldp = rows_per;
   double* P = sm;
@@ -240,9 +244,16 @@ __global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long s
         sc = 1.0 / (alpha - beta);
       }
     }
+    // remote partials: one DSMEM load per thread (all in flight together),
+    // then a fixed-order sum over ranks from shared memory
+    for (int idx = tid; idx < cs * PNB; idx += PT) {
+      const int q = idx / PNB, l = idx % PNB;
+      if (l > j && l < bs) Sp[q][l] = remote(cl, &x, q)->S[l];
+    }
+    __syncthreads();
     for (int l = j + 1 + tid; l < bs; l += PT) {
       double s = 0.0;
-      for (int q = 0; q < cs; ++q) s += remote(cl, &x, q)->S[l];
+      for (int q = 0; q < cs; ++q) s += Sp[q][l];
       const double rjl = xo->rowj[l];
       const double wl = tj * fma(sc, s, rjl);
       w[l] = wl;
@@ -378,31 +389,37 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
   __shared__ int sel[PNB];
   __shared__ int s_gi, s_own;
   const int c0 = cr * cols_per, c1 = min(n, c0 + cols_per), nc = max(c1 - c0, 0);
-  double* Ys = sm;  // HSK x cols_per
-  double* nrm = Ys + (long long)HSK * cols_per;
+  constexpr int LDY = HSK + 1;  // odd column stride: thread-per-column reads are conflict free
+  double* Ys = sm;              // LDY x cols_per
+  double* nrm = Ys + (long long)LDY * cols_per;
   const double* Y = Yg + b * sY + (long long)(J + c0) * ldy;
   for (int idx = tid; idx < nc * HSK; idx += PT) {
     int r = idx % HSK, c = idx / HSK;
-    Ys[c * HSK + r] = Y[(long long)c * ldy + r];
+    Ys[c * LDY + r] = Y[(long long)c * ldy + r];
   }
   __syncthreads();
-  for (int c = warp; c < nc; c += NW) {
-    double s = 0.0;
-    for (int r = lane; r < HSK; r += 32) s = fma(Ys[c * HSK + r], Ys[c * HSK + r], s);
-    s = warp_sum(s);
-    if (lane == 0) nrm[c] = s;
+  // column norms^2 and this thread's best candidate (thread per column)
+  double bv = -1.0;
+  int bi = 0x7fffffff;
+  for (int c = tid; c < nc; c += PT) {
+    const double* yc = Ys + c * LDY;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int r = 0; r < HSK; r += 4) {
+      s0 = fma(yc[r], yc[r], s0); s1 = fma(yc[r + 1], yc[r + 1], s1);
+      s2 = fma(yc[r + 2], yc[r + 2], s2); s3 = fma(yc[r + 3], yc[r + 3], s3);
+    }
+    const double s = (s0 + s1) + (s2 + s3);
+    nrm[c] = s;
+    if (s > bv) { bv = s; bi = c0 + c; }
   }
-  __syncthreads();
   for (int i = 0; i < bs; ++i) {
     XSel& x = xch[i & 1];
-    double v = -1.0;
-    int iv = 0x7fffffff;
-    for (int c = tid; c < nc; c += PT)
-      if (nrm[c] > v) { v = nrm[c]; iv = c0 + c; }
+    double v = bv;
+    int iv = bi;
     block_argmax(v, iv, redv, redi);
     if (tid == 0) { x.cand_v = v; x.cand_i = iv; }
-    if (v >= 0.0)
-      for (int r = tid; r < HSK; r += PT) x.y[r] = Ys[(iv - c0) * HSK + r];
+    if (v >= 0.0 && tid < HSK) x.y[tid] = Ys[(iv - c0) * LDY + tid];
     cl.sync();
     if (tid < 32) {
       double cv = -2.0;
@@ -414,45 +431,58 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
     }
     __syncthreads();
     const int gi = s_gi;
-    {
-      XSel* xo = remote(cl, &x, s_own);
-      for (int r = tid; r < HSK; r += PT) yv[r] = xo->y[r];
-    }
+    if (tid < HSK) yv[tid] = remote(cl, &x, s_own)->y[tid];
     if (gi >= c0 && gi < c1 && tid == 0) nrm[gi - c0] = -1.0;
     __syncthreads();
-    // q = (I - Qb Qb^T) y twice (classical Gram-Schmidt with reorthogonalisation)
+    // q = (I - Qb Qb^T) y, twice (classical Gram-Schmidt with reorthogonalisation)
     for (int pass = 0; pass < 2; ++pass) {
-      if (tid < i) {
-        double s = 0.0;
-        for (int r = 0; r < HSK; ++r) s = fma(Qb[tid][r], yv[r], s);
-        dv[tid] = s;
+      for (int c = warp; c < i; c += NW) {
+        double d = Qb[c][lane] * yv[lane];
+        if (lane + 32 < HSK) d = fma(Qb[c][lane + 32], yv[lane + 32], d);
+        d = warp_sum(d);
+        if (lane == 0) dv[c] = d;
       }
       __syncthreads();
       if (tid < HSK) {
-        double s = yv[tid];
-        for (int c = 0; c < i; ++c) s = fma(-dv[c], Qb[c][tid], s);
-        yv[tid] = s;
+        double a0 = yv[tid], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int c = 0;
+        for (; c + 3 < i; c += 4) {
+          a0 = fma(-dv[c], Qb[c][tid], a0); a1 = fma(-dv[c + 1], Qb[c + 1][tid], a1);
+          a2 = fma(-dv[c + 2], Qb[c + 2][tid], a2); a3 = fma(-dv[c + 3], Qb[c + 3][tid], a3);
+        }
+        for (; c < i; ++c) a0 = fma(-dv[c], Qb[c][tid], a0);
+        yv[tid] = (a0 + a1) + (a2 + a3);
       }
       __syncthreads();
     }
     if (warp == 0) {
-      double y0 = lane < HSK ? yv[lane] : 0.0;
+      double y0 = yv[lane];
       double y1 = lane + 32 < HSK ? yv[lane + 32] : 0.0;
       double nn = warp_sum(y0 * y0 + y1 * y1);
       double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-      if (lane < HSK) Qb[i][lane] = y0 * inv;
+      Qb[i][lane] = y0 * inv;
       if (lane + 32 < HSK) Qb[i][lane + 32] = y1 * inv;
     }
     __syncthreads();
-    for (int c = warp; c < nc; c += NW) {
+    // downdate every live column's residual norm and pick the next candidate
+    bv = -1.0;
+    bi = 0x7fffffff;
+    const double* q = Qb[i];
+    for (int c = tid; c < nc; c += PT) {
       const double cur = nrm[c];
       if (cur < 0.0) continue;
-      double d = 0.0;
-      for (int r = lane; r < HSK; r += 32) d = fma(Qb[i][r], Ys[c * HSK + r], d);
-      d = warp_sum(d);
-      if (lane == 0) nrm[c] = fmax(cur - d * d, 0.0);
+      const double* yc = Ys + c * LDY;
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+      for (int r = 0; r < HSK; r += 4) {
+        d0 = fma(q[r], yc[r], d0); d1 = fma(q[r + 1], yc[r + 1], d1);
+        d2 = fma(q[r + 2], yc[r + 2], d2); d3 = fma(q[r + 3], yc[r + 3], d3);
+      }
+      const double d = (d0 + d1) + (d2 + d3);
+      const double nv = fmax(cur - d * d, 0.0);
+      nrm[c] = nv;
+      if (nv > bv) { bv = nv; bi = c0 + c; }
     }
-    __syncthreads();
   }
   cl.sync();
   if (cr != 0 || tid != 0) return;
@@ -477,6 +507,437 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
 }
 
 // ---------------------------------------------------------------------------
+// Register-resident panels.  Each thread keeps RPT whole panel rows (32
+// columns) in registers for the entire column loop (rows r0 + tid + q*PT).
+// The column loop is NOT unrolled (a fully unrolled 32-step body thrashes the
+// instruction cache when one CTA runs per SM); instead the registers rotate
+// one position per step so the current column is always position 0:
+// position t holds column (j + t) mod 32.  A step is RPT*32 register FMAs,
+// one warp transpose-reduction (QR) or warp argmax (LU), two CTA barriers and
+// one cluster barrier.  The smem-resident kernels above remain for panels
+// taller than 16*PT*RPT rows.
+
+// Warp transpose-reduction: lane l returns sum over the warp of v[l].
+// 16+8+4+2+1 = 31 shuffles (fixed order: deterministic).
+__device__ __forceinline__ double transpose_reduce32(double (&v)[PNB], int lane) {
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool up = lane & h;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return v[0];
+}
+
+// Half-width variant: lane l returns sum over the warp of v[l & 15].
+__device__ __forceinline__ double transpose_reduce16(double (&v)[16], int lane) {
+#pragma unroll
+  for (int h = 8; h >= 1; h >>= 1) {
+    const bool up = lane & h;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
+template <int RPT, int K>
+__device__ __forceinline__ void rotate_left(double (&a)[RPT][PNB]) {
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    double t0[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) t0[t] = a[q][t];
+#pragma unroll
+    for (int t = 0; t < PNB - K; ++t) a[q][t] = a[q][t + K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) a[q][PNB - K + t] = t0[t];
+  }
+}
+
+template <int V>
+struct IC { static constexpr int value = V; };
+
+template <int RPT>
+__global__ void __launch_bounds__(PT, 1) k_lu_panel_rr(const double* A, long long sA, int lda,
+                                                       int n, int c0, int nbs, int* ipiv,
+                                                       long long sPiv, double* Ainv,
+                                                       long long sAi, double* pivmin,
+                                                       double* pivmax) {
+  constexpr int RP = PT * RPT;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = cl.num_blocks(), cr = cl.block_rank();
+  const int b = blockIdx.x / cs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ XLu xch[2];
+  __shared__ double prow[PNB], pel[PNB], rj[PNB];
+  __shared__ double redv[NW];
+  __shared__ int redi[NW];
+  __shared__ int s_iv;
+  __shared__ double s_rinv;
+  __shared__ double wrow[NW][PNB];
+  __shared__ double M[PNB][PNB + 1], Li[PNB][PNB + 1], Ui[PNB][PNB + 1];
+  const int R = n - c0;
+  const int r0 = cr * RP;
+  const double* Ab = A + b * sA + (long long)c0 * lda + c0;
+  double a[RPT][PNB];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = r0 + tid + q * PT;
+#pragma unroll
+    for (int l = 0; l < PNB; ++l)
+      a[q][l] = (i < R && l < nbs) ? Ab[(long long)l * lda + i] : 0.0;
+  }
+  double pmin = INFINITY, pmax = 0.0;
+  // one column step; the group started at column j0 (= rotation so far), so
+  // the current column sits at position u = j - j0 and position t holds
+  // column (j0 + t) mod 32; trailing columns are positions u < t < 32 - j0
+  auto step = [&](const int j, const int j0, auto uc) {
+    constexpr int u = decltype(uc)::value;
+    XLu& x = xch[j & 1];
+    double v = -1.0;
+    int iv = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = r0 + tid + q * PT;
+      if (i >= j && i < R) {
+        double t = fabs(a[q][u]);
+        if (t != t) t = INFINITY;  // NaN (from an earlier singular pivot) stays selectable
+        if (t > v) { v = t; iv = i; }
+      }
+    }
+    warp_argmax(v, iv);
+    // the warp's winning lane stages its row; lane 0 the warp's candidate
+#pragma unroll
+    for (int q = 0; q < RPT; ++q)
+      if (v >= 0.0 && r0 + tid + q * PT == iv)
+#pragma unroll
+        for (int t = 0; t < PNB; ++t) wrow[warp][t] = a[q][t];
+    if (lane == 0) { redv[warp] = v; redi[warp] = iv; }
+    if (cr == 0 && tid == j)
+#pragma unroll
+      for (int t = 0; t < PNB; ++t) x.rowj[t] = a[0][t];
+    __syncthreads();
+    if (warp == 0) {  // CTA candidate: fixed warp order, ties -> smaller row
+      double bv = redv[0];
+      int bi = redi[0], bw = 0;
+#pragma unroll
+      for (int ww = 1; ww < NW; ++ww)
+        if (redv[ww] > bv || (redv[ww] == bv && redi[ww] < bi)) { bv = redv[ww]; bi = redi[ww]; bw = ww; }
+      x.cand_row[lane] = bv >= 0.0 ? wrow[bw][lane] : 0.0;
+      if (lane == 0) { x.cand_v = bv; x.cand_i = bi; }
+    }
+    cl.sync();
+    if (warp == 0) {  // lanes read one rank's candidate each; ties -> smaller row
+      double cv = -2.0;
+      int ci = 0x7fffffff;
+      if (lane < cs) { XLu* xr = remote(cl, &x, lane); cv = xr->cand_v; ci = xr->cand_i; }
+      warp_argmax(cv, ci);
+      if (ci < j || ci >= R) { ci = j; cv = 0.0; }  // defensive: always a valid owner rank
+      const double pr = remote(cl, &x, ci / RP)->cand_row[lane];
+      prow[lane] = pr;
+      pel[lane] = (lane > u && lane < PNB - j0) ? pr : 0.0;  // trailing columns only
+      rj[lane] = remote(cl, &x, 0)->rowj[lane];
+      const double pd = __shfl_sync(0xffffffffu, pr, u);
+      if (lane == 0) {
+        s_iv = ci;
+        s_rinv = pd != 0.0 ? 1.0 / pd : 1.0;
+        pmin = fmin(pmin, cv);
+        pmax = fmax(pmax, cv);
+      }
+    }
+    __syncthreads();
+    const int piv = s_iv;
+    if (piv != j) {
+      if (cr == 0 && tid == j)
+#pragma unroll
+        for (int t = 0; t < PNB; ++t) a[0][t] = prow[t];
+#pragma unroll
+      for (int q = 0; q < RPT; ++q)
+        if (r0 + tid + q * PT == piv)
+#pragma unroll
+          for (int t = 0; t < PNB; ++t) a[q][t] = rj[t];
+    }
+    const double rinv = s_rinv;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = r0 + tid + q * PT;
+      if (i > j && i < R) {
+        const double lij = a[q][u] * rinv;
+        a[q][u] = lij;
+#pragma unroll
+        for (int t = u + 1; t < PNB; ++t) a[q][t] = fma(-lij, pel[t], a[q][t]);
+      }
+    }
+    if (cr == 0 && tid == 0) ipiv[b * sPiv + c0 + j] = c0 + piv;
+  };
+  int j = 0;
+#pragma unroll 1
+  for (; j + 4 <= nbs; j += 4) {
+    step(j, j, IC<0>{});
+    step(j + 1, j, IC<1>{});
+    step(j + 2, j, IC<2>{});
+    step(j + 3, j, IC<3>{});
+    rotate_left<RPT, 4>(a);
+  }
+#pragma unroll 1
+  for (; j < nbs; ++j) {
+    step(j, j, IC<0>{});
+    rotate_left<RPT, 1>(a);
+  }
+  // position t now holds column (nbs + t) mod 32
+  if (cr == 0 && tid < nbs)
+#pragma unroll
+    for (int t = 0; t < PNB; ++t) M[tid][(nbs + t) & (PNB - 1)] = a[0][t];
+  cl.sync();  // no CTA may exit while others could still read its exchange area
+  if (cr != 0) return;
+  __syncthreads();
+  if (tid < nbs) {
+    const int j = tid;
+    for (int i = 0; i < nbs; ++i) Li[i][j] = (i == j) ? 1.0 : 0.0;
+    for (int i = j + 1; i < nbs; ++i) {
+      double s = 0.0;
+      for (int k = j; k < i; ++k) s = fma(M[i][k], Li[k][j], s);
+      Li[i][j] = -s;
+    }
+    for (int i = 0; i < nbs; ++i) Ui[i][j] = 0.0;
+    Ui[j][j] = 1.0 / M[j][j];
+    for (int i = j - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int k = i + 1; k <= j; ++k) s = fma(M[i][k], Ui[k][j], s);
+      Ui[i][j] = -s / M[i][i];
+    }
+  }
+  __syncthreads();
+  double* Ai = Ainv + b * sAi;
+  for (int idx = tid; idx < nbs * nbs; idx += PT) {
+    int i = idx % nbs, j = idx / nbs;
+    double s = 0.0;
+    for (int k = i; k < nbs; ++k) s = fma(Ui[i][k], Li[k][j], s);
+    Ai[j * PNB + i] = s;
+  }
+  if (tid == 0) {
+    pivmin[b] = fmin(pivmin[b], pmin);
+    pivmax[b] = fmax(pivmax[b], pmax);
+  }
+}
+
+// Householder QR of the ID block panel with the rows in registers.  One
+// 32-slot reduction per column: with the current column x at position 0,
+// slot t = x . (position t) gives |x|^2 (t = 0), x . c_l for the trailing
+// columns (-> w_l) and v_i . x for the finished ones (-> Gram G(i,j) =
+// v_i(j) + sc v_i . x, so T needs no extra pass).  Every CTA keeps G, tau, R
+// and V1 (rows 0..bs-1 of V, from the published pivot rows), so the tail
+// (T, M = T V1^T, Q = E - V M) runs without further cluster traffic.
+struct XQr2 {
+  double S[PNB];
+  double rowj[PNB];
+};
+
+template <int RPT>
+__global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long long sA, int lda,
+                                                       const int* pv, const int* active,
+                                                       const int* bsv, int J, double* Qw,
+                                                       long long sQ, int ldq, double* Rt) {
+  constexpr int RP = PT * RPT;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = cl.num_blocks(), cr = cl.block_rank();
+  const int b = blockIdx.x / cs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (!active[b] || bsv[b] <= 0) return;  // uniform for the whole cluster
+  const int bs = bsv[b];
+  const int p = pv[b];
+  __shared__ XQr2 xch[2];
+  __shared__ double red[NW][PNB];
+  __shared__ double Sp[2 * NW][PNB];
+  __shared__ double w[PNB], tau[PNB];
+  __shared__ double s_sc;
+  __shared__ double Rl[PNB][PNB + 1], Gm[PNB][PNB + 1], Tm[PNB][PNB + 1], V1[PNB][PNB + 1];
+  const int r0 = cr * RP;
+  for (int idx = tid; idx < PNB * PNB; idx += PT) {
+    const int i = idx % PNB, c = idx / PNB;
+    Rl[i][c] = 0.0; Gm[i][c] = 0.0; V1[i][c] = 0.0; Tm[i][c] = 0.0;
+  }
+  if (tid < PNB) { tau[tid] = 0.0; w[tid] = 0.0; }
+  const double* Ab = A + b * sA + (long long)J * lda;
+  double a[RPT][PNB];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int g = r0 + tid + q * PT;
+#pragma unroll
+    for (int l = 0; l < PNB; ++l) a[q][l] = (g < p && l < bs) ? Ab[(long long)l * lda + g] : 0.0;
+  }
+  __syncthreads();
+  const int jmax = min(bs, p);
+  // one column step (see k_lu_panel_rr for the position bookkeeping)
+  auto step = [&](const int j, const int j0, auto uc) {
+    constexpr int u = decltype(uc)::value;
+    XQr2& x = xch[j & 1];
+    // slots in two halves of 16 (register budget): lane l ends with slot l
+    double part = 0.0;
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      double v[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) v[t] = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int g = r0 + tid + q * PT;
+        if (g > j && g < p) {
+          const double xr = a[q][u];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) v[t] = fma(xr, a[q][16 * hf + t], v[t]);
+        }
+      }
+      const double r = transpose_reduce16(v, lane);
+      if ((lane >> 4) == hf) part = r;
+    }
+    red[warp][lane] = part;
+    if (cr == 0 && tid == j)
+#pragma unroll
+      for (int t = 0; t < PNB; ++t) x.rowj[t] = a[0][t];
+    __syncthreads();
+    if (warp == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) s += red[ww][lane];
+      x.S[lane] = s;
+    }
+    cl.sync();
+    // warp w fetches ranks 2w, 2w+1 (all remote loads in flight together)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (2 * warp + h < cs) Sp[2 * warp + h][lane] = remote(cl, &x, 2 * warp + h)->S[lane];
+    __syncthreads();
+    if (warp == 0) {  // lane t: slot t summed over ranks in fixed order
+      const int t = lane;
+      const int c = (j0 + t) & (PNB - 1);  // the column at position t
+      const double rl = remote(cl, &x, 0)->rowj[t];
+      double s = Sp[0][t];
+      for (int q = 1; q < cs; ++q) s += Sp[q][t];
+      const double tot = __shfl_sync(0xffffffffu, s, u);
+      const double alpha = __shfl_sync(0xffffffffu, rl, u);
+      double tj, beta, sc;
+      const double xn = sqrt(tot);
+      if (xn == 0.0) { tj = 0.0; beta = alpha; sc = 0.0; }
+      else {
+        beta = -copysign(hypot(alpha, xn), alpha);
+        tj = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+      }
+      if (t == u) {
+        tau[j] = tj;
+        Rl[j][j] = beta;
+        Gm[j][j] = 1.0 + sc * sc * tot;
+        V1[j][j] = 1.0;
+        s_sc = sc;
+        w[t] = 0.0;
+      } else if (c > j) {
+        const double wl = tj * fma(sc, s, rl);
+        w[t] = wl;
+        Rl[j][c] = rl - wl;
+      } else {  // finished column c < j
+        Gm[c][j] = fma(sc, s, rl);
+        V1[j][c] = rl;
+        w[t] = 0.0;
+      }
+    }
+    __syncthreads();
+    const double sc = s_sc;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int g = r0 + tid + q * PT;
+      if (g > j && g < p) {
+        const double xv = a[q][u] * sc;
+        a[q][u] = xv;
+#pragma unroll
+        for (int t = u + 1; t < PNB; ++t) a[q][t] = fma(-w[t], xv, a[q][t]);
+      } else if (g == j) {
+#pragma unroll
+        for (int t = u + 1; t < PNB; ++t) a[q][t] -= w[t];
+      }
+    }
+  };
+  int j = 0;
+#pragma unroll 1
+  for (; j + 4 <= jmax; j += 4) {
+    step(j, j, IC<0>{});
+    step(j + 1, j, IC<1>{});
+    step(j + 2, j, IC<2>{});
+    step(j + 3, j, IC<3>{});
+    rotate_left<RPT, 4>(a);
+  }
+#pragma unroll 1
+  for (; j < jmax; ++j) {
+    step(j, j, IC<0>{});
+    rotate_left<RPT, 1>(a);
+  }
+  // position t now holds column (jmax + t) mod 32
+  // T (upper, dlarft forward columnwise): T(0:c, c) = -tau_c T(0:c, 0:c) G(0:c, c)
+  if (tid < PNB) {
+    const int i = tid;
+    for (int c = 0; c < bs; ++c) {
+      double t = 0.0;
+      if (i < c) {
+        double s = 0.0;
+        for (int k = i; k < c; ++k) s = fma(Tm[i][k], Gm[k][c], s);
+        t = -tau[c] * s;
+      } else if (i == c) {
+        t = tau[c];
+      }
+      Tm[i][c] = (i <= c) ? t : 0.0;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // M = T V1^T into Gm: M(a, c) = sum_k T(a,k) V1(c,k)
+  for (int idx = tid; idx < bs * bs; idx += PT) {
+    const int a0 = idx % bs, c = idx / bs;
+    double s = 0.0;
+    for (int k = a0; k < bs; ++k) s = fma(Tm[a0][k], V1[c][k], s);
+    Gm[a0][c] = s;
+  }
+  __syncthreads();
+  // V rows above bs: unit diagonal, zeros to the right; Q = E - V M
+  double* Qo = Qw + b * sQ;
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int g = r0 + tid + q * PT;
+    if (g < bs)
+#pragma unroll
+      for (int t = 0; t < PNB; ++t) {
+        const int k = (jmax + t) & (PNB - 1);
+        a[q][t] = (k == g) ? 1.0 : (k > g ? 0.0 : a[q][t]);
+      }
+    if (g < p)
+      for (int c = 0; c < bs; ++c) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < PNB; t += 2) {
+          s0 = fma(a[q][t], Gm[(jmax + t) & (PNB - 1)][c], s0);
+          s1 = fma(a[q][t + 1], Gm[(jmax + t + 1) & (PNB - 1)][c], s1);
+        }
+        Qo[(long long)c * ldq + g] = ((g == c) ? 1.0 : 0.0) - (s0 + s1);
+      }
+  }
+  if (cr == 0) {
+    double* Rr = Rt + (long long)b * PNB * PNB;
+    for (int idx = tid; idx < PNB * PNB; idx += PT) {
+      int i = idx % PNB, c = idx / PNB;
+      Rr[c * PNB + i] = Rl[i][c];
+    }
+  }
+  cl.sync();  // remote reads of this CTA's exchange area are done before it exits
+}
+
+// ---------------------------------------------------------------------------
 // launch helpers
 
 static int launch_cluster(const void* fn, int count, int cs, size_t smem, cudaStream_t st,
@@ -493,8 +954,13 @@ static int launch_cluster(const void* fn, int count, int cs, size_t smem, cudaSt
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  VF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  {
+  // function attributes are set once per (kernel, dynamic smem high-water mark)
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> set_smem;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = set_smem.find(fn);
+  if (it == set_smem.end() || it->second < smem) {
+    VF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
       cudaFuncAttributes fa{};
@@ -503,6 +969,7 @@ static int launch_cluster(const void* fn, int count, int cs, size_t smem, cudaSt
                 fa.sharedSizeBytes, cs, count, cudaGetErrorString(e));
       return VF_ECUDA;
     }
+    set_smem[fn] = smem;
   }
   VF_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
   ++g_launches;
@@ -512,6 +979,16 @@ static int launch_cluster(const void* fn, int count, int cs, size_t smem, cudaSt
 // cluster size: enough CTAs that one slice fits `max_slice` rows/cols, and,
 // when there are few matrices, split further (down to 256 per CTA) so the
 // cluster work spreads over the SMs
+// VF_PANEL=cl / rr forces the smem-resident / register-resident panels (A/B timing)
+static int panel_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("VF_PANEL");
+    mode = !e ? 0 : (e[0] == 'c' ? 1 : (e[0] == 'r' ? 2 : 0));
+  }
+  return mode;
+}
+
 static int pick_cs(int total, int max_slice, int count) {
   int cs = (total + max_slice - 1) / max_slice;
   if (count * cs < 120) cs = std::max(cs, (total + 255) / 256);
@@ -522,6 +999,22 @@ int lu_panel(const double* A, long long sA, int lda, int n, int c0, int nbs, int
              long long sPiv, double* Ainv, long long sAi, double* pivmin, double* pivmax,
              cudaStream_t st) {
   const int R = n - c0;
+  {
+    // register-resident panel: 256 threads x RPT rows per CTA, up to 16 CTAs
+    // measured: the register-resident panel wins for tall panels; for short
+    // ones in large batches the smem kernel's higher occupancy wins
+    int rpt = R <= PT ? 1 : (R <= 16 * 2 * PT ? 2 : (R <= 16 * 3 * PT ? 3 : 0));
+    if (panel_mode() == 1 || (panel_mode() == 0 && R <= 320)) rpt = 0;
+    if (rpt) {
+      const int cs = (R + rpt * PT - 1) / (rpt * PT);
+      void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&n, (void*)&c0, (void*)&nbs,
+                      (void*)&ipiv, (void*)&sPiv, (void*)&Ainv, (void*)&sAi,
+                      (void*)&pivmin, (void*)&pivmax};
+      const void* fn = rpt == 1 ? (const void*)k_lu_panel_rr<1>
+                     : rpt == 2 ? (const void*)k_lu_panel_rr<2> : (const void*)k_lu_panel_rr<3>;
+      return launch_cluster(fn, batch, cs, 0, st, args);
+    }
+  }
   int cs = pick_cs(R, 768, batch);
   int rows_per = (R + cs - 1) / cs;
   if (rows_per < PNB) rows_per = PNB;
@@ -536,6 +1029,14 @@ int lu_panel(const double* A, long long sA, int lda, int n, int c0, int nbs, int
 int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* active,
              const int* bsv, int J, int maxp, int count, double* Qw, long long sQ, int ldq,
              double* Rt, cudaStream_t st) {
+  if (maxp <= 16 * 2 * PT && panel_mode() != 1) {
+    const int rpt = maxp <= PT ? 1 : 2;
+    const int cs = (maxp + rpt * PT - 1) / (rpt * PT);
+    void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
+                    (void*)&J, (void*)&Qw, (void*)&sQ, (void*)&ldq, (void*)&Rt};
+    const void* fn = rpt == 1 ? (const void*)k_qr_panel_rr<1> : (const void*)k_qr_panel_rr<2>;
+    return launch_cluster(fn, count, cs, 0, st, args);
+  }
   int cs = pick_cs(maxp, 640, count);
   int rows_per = (maxp + cs - 1) / cs;
   if (rows_per < PNB) rows_per = PNB;
@@ -552,7 +1053,7 @@ int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const i
   if (n <= 0) return VF_OK;
   int cs = pick_cs(n, 512, count);
   int cols_per = (n + cs - 1) / cs;
-  size_t smem = ((size_t)HSK * cols_per + (size_t)cols_per) * sizeof(double);
+  size_t smem = ((size_t)(HSK + 1) * cols_per + (size_t)cols_per) * sizeof(double);
   void* args[] = {(void*)&Y, (void*)&ldy, (void*)&sY, (void*)&mv, (void*)&active, (void*)&bsv,
                   (void*)&J, (void*)&cols_per, (void*)&swaps};
   return launch_cluster((const void*)k_select_cl, count, cs, smem, st, args);

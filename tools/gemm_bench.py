@@ -31,6 +31,18 @@ def bench(M, N, K, batch=1, tA=0, tB=0, beta=1.0):
     fl = 2.0 * M * N * K * batch
     print(f"M={M:6d} N={N:6d} K={K:6d} b={batch:5d} tA={tA} tB={tB}: ours {fl/ms/1e9:7.2f} TF ({ms:8.3f} ms)  cublas {fl/ms2/1e9:7.2f} TF", flush=True)
 
+import sys as _s
+if len(_s.argv) > 1 and _s.argv[1] == "hss":
+    bench(12272, 12016, 256)                    # GJ outer update at the 1024^2 root
+    bench(8208, 8000, 256, batch=4)             # ID delayed update, level 1
+    bench(32, 8000, 8208, batch=4, tA=1, beta=0.0)  # ID W = Q^T A, level 1
+    bench(3104, 2000, 128, batch=64)            # ID update, level 5
+    bench(32, 2000, 3104, batch=64, tA=1, beta=0.0)
+    bench(3000, 2744, 256, batch=32)            # GJ outer, level 5
+    bench(544, 368, 64, batch=2048)             # ID update, level 10
+    bench(40, 32, 8208, batch=4, beta=0.0)      # sketch Z = Omega Q
+    bench(8192, 8192, 8192)
+    _s.exit(0)
 bench(8192, 8192, 8192)
 bench(8192, 8192, 128)
 bench(12272, 12272, 32)
