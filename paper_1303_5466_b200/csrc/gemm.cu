@@ -10,6 +10,8 @@
 // coalesced 8-byte loads along rows, fixed-order reductions (bitwise
 // deterministic, as DenseBlockInverse.apply requires, solver_dense.py:293-329).
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include "common.cuh"
 #include "../../include/vief_b200.h"
 
@@ -49,13 +51,15 @@ struct Tile {
 
 // load one BK x OUT tile of an operand whose element (o, k) lives at
 // src[k*ld + o] (outer-contiguous) or src[o*ld + k] (k-contiguous)
-template <int OUT, bool KCONTIG>
+template <int OUT, bool KCONTIG, int NT>
 __device__ __forceinline__ void load_tile(double* S, const double* src, int ld, int o0, int k0,
                                           int O, int K, int tid) {
-  constexpr int N_IT = OUT * BK / 128;
+  constexpr int N_IT = OUT * BK / NT;
+  static_assert(N_IT >= 1 && OUT * BK % NT == 0, "tile/threads");
   if (!KCONTIG) {
-    constexpr int KQ = 128 / OUT > 0 ? 128 / OUT : 1;
-    if (OUT <= 128) {
+    constexpr int KQ = NT / OUT > 0 ? NT / OUT : 1;
+    static_assert(NT % OUT == 0 || OUT % NT == 0, "tile/threads");
+    if (OUT <= NT) {
       const int o = tid % OUT, kq = tid / OUT;
       const int go = o0 + o;
 #pragma unroll
@@ -70,7 +74,7 @@ __device__ __forceinline__ void load_tile(double* S, const double* src, int ld, 
     const int gk = k0 + k;
 #pragma unroll
     for (int i = 0; i < N_IT; ++i) {
-      const int o = oq + 8 * i, go = o0 + o;
+      const int o = oq + (NT / BK) * i, go = o0 + o;
       const bool v = go < O && gk < K;
       cp_async8(S + Tile<OUT, true>::at(o, k), v ? src + (long long)go * ld + gk : src, v);
     }
@@ -85,12 +89,14 @@ __device__ __forceinline__ void load_tile(double* S, const double* src, int ld, 
 // ksplit + chunk; chunk s covers k in [s*kchunk, (s+1)*kchunk) and writes
 // alpha * partial to ws[z] (M x N, ld M of the descriptor); k_splitk_reduce
 // then sums the chunks in fixed order (deterministic) and applies beta.
-template <int BMT, int BNT, bool TA, bool TB>
-__global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d, int ksplit, int kchunk,
-                                               double* ws) {
+template <int BMT, int BNT, int WTM, int WTN, bool TA, bool TB>
+__global__ void __launch_bounds__((BMT / WTM) * (BNT / WTN) * 32)
+    k_dgemm(vief_gemm_desc d, int ksplit, int kchunk, double* ws) {
+  constexpr int NT = (BMT / WTM) * (BNT / WTN) * 32;  // one warp per WTM x WTN warp tile
+  constexpr int FI = WTM / 8, FJ = WTN / 8;           // m8n8 fragments per warp
   using TAt = Tile<BMT, TA>;    // A^T stored K x M col-major -> contiguous in k
   using TBt = Tile<BNT, !TB>;   // B stored K x N col-major   -> contiguous in k
-  constexpr int WN = BNT / 32;
+  constexpr int WNW = BNT / WTN;  // warps along N
   const int b = blockIdx.z / ksplit, chunk = blockIdx.z % ksplit;
   GemmItem it = gemm_item(d, b);
   const int m0 = blockIdx.y * BMT, n0 = blockIdx.x * BNT;
@@ -101,23 +107,23 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d, int ksplit, int
   double* As = gsm;
   double* Bs = gsm + STAGES * TAt::SIZE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
+  const int wm = (warp / WNW) * WTM, wn = (warp % WNW) * WTN;
   const int g = lane >> 2, t = lane & 3;
 
   const bool use_c = d.beta != 0.0;
-  double acc[4][4][2];
+  double acc[FI][FJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
   if (nk > 0 && d.alpha != 0.0) {
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       if (s < nk) {
-        load_tile<BMT, TA>(As + s * TAt::SIZE, it.A, d.lda, m0, kbeg + s * BK, it.M, kend, tid);
-        load_tile<BNT, !TB>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, kbeg + s * BK, it.N, kend, tid);
+        load_tile<BMT, TA, NT>(As + s * TAt::SIZE, it.A, d.lda, m0, kbeg + s * BK, it.M, kend, tid);
+        load_tile<BNT, !TB, NT>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, kbeg + s * BK, it.N, kend, tid);
       }
       cp_async_commit();
     }
@@ -127,23 +133,23 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d, int ksplit, int
       const int nxt = kt + STAGES - 1;
       if (nxt < nk) {
         const int s = nxt % STAGES;
-        load_tile<BMT, TA>(As + s * TAt::SIZE, it.A, d.lda, m0, kbeg + nxt * BK, it.M, kend, tid);
-        load_tile<BNT, !TB>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, kbeg + nxt * BK, it.N, kend, tid);
+        load_tile<BMT, TA, NT>(As + s * TAt::SIZE, it.A, d.lda, m0, kbeg + nxt * BK, it.M, kend, tid);
+        load_tile<BNT, !TB, NT>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, kbeg + nxt * BK, it.N, kend, tid);
       }
       cp_async_commit();
       const double* as = As + (kt % STAGES) * TAt::SIZE;
       const double* bs = Bs + (kt % STAGES) * TBt::SIZE;
 #pragma unroll
       for (int kk = 0; kk < BK; kk += 4) {
-        double af[4], bf[4];
+        double af[FI], bf[FJ];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = as[TAt::at(wm + 8 * i + g, kk + t)];
+        for (int i = 0; i < FI; ++i) af[i] = as[TAt::at(wm + 8 * i + g, kk + t)];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = bs[TBt::at(wn + 8 * j + g, kk + t)];
+        for (int j = 0; j < FJ; ++j) bf[j] = bs[TBt::at(wn + 8 * j + g, kk + t)];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < FI; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j], af[i], bf[j]);
+          for (int j = 0; j < FJ; ++j) dmma_m8n8k4(acc[i][j], af[i], bf[j]);
       }
     }
     cp_async_wait<0>();
@@ -152,11 +158,11 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d, int ksplit, int
   if (ksplit > 1) {
     double* W = ws + (long long)blockIdx.z * d.M * d.N;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < FI; ++i) {
       const int gm = m0 + wm + 8 * i + g;
       if (gm >= it.M) continue;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < FJ; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int gn = n0 + wn + 8 * j + 2 * t + e;
@@ -166,12 +172,12 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d, int ksplit, int
     return;
   }
   // all C loads are issued before any store (no load waits behind a store)
-  double cv[4][4][2];
+  double cv[FI][FJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < FI; ++i) {
     const int gm = m0 + wm + 8 * i + g;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < FJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int gn = n0 + wn + 8 * j + 2 * t + e;
@@ -179,11 +185,11 @@ __global__ void __launch_bounds__(128) k_dgemm(vief_gemm_desc d, int ksplit, int
       }
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < FI; ++i) {
     const int gm = m0 + wm + 8 * i + g;
     if (gm >= it.M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < FJ; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int gn = n0 + wn + 8 * j + 2 * t + e;
@@ -215,12 +221,12 @@ __global__ void k_splitk_reduce(vief_gemm_desc d, int ksplit, const double* ws) 
   }
 }
 
-template <int BMT, int BNT, bool TA, bool TB>
+template <int BMT, int BNT, int WTM, int WTN, bool TA, bool TB>
 static int launch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
   constexpr int smem = STAGES * (Tile<BMT, TA>::SIZE + Tile<BNT, !TB>::SIZE) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    VF_CUDA(cudaFuncSetAttribute(k_dgemm<BMT, BNT, TA, TB>,
+    VF_CUDA(cudaFuncSetAttribute(k_dgemm<BMT, BNT, WTM, WTN, TA, TB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
@@ -238,7 +244,8 @@ static int launch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
   if (ksplit > 1) {
     VF_CUDA(cudaMallocAsync(&ws, sizeof(double) * (size_t)d->M * d->N * d->batch * ksplit, st));
   }
-  k_dgemm<BMT, BNT, TA, TB><<<grid, 128, smem, st>>>(*d, ksplit, kchunk, ws);
+  k_dgemm<BMT, BNT, WTM, WTN, TA, TB><<<grid, (BMT / WTM) * (BNT / WTN) * 32, smem, st>>>(
+      *d, ksplit, kchunk, ws);
   if (ksplit > 1) {
     const long long mn = (long long)d->M * d->N;
     dim3 rg((unsigned)std::min<long long>(cdiv((int)std::min<long long>(mn, 1 << 30), 256), 1024),
@@ -250,12 +257,12 @@ static int launch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
   return VF_OK;
 }
 
-template <int BMT, int BNT>
+template <int BMT, int BNT, int WTM = 32, int WTN = 32>
 static int dispatch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
-  if (!d->transA && !d->transB) return launch_gemm<BMT, BNT, false, false>(d, st);
-  if (!d->transA && d->transB) return launch_gemm<BMT, BNT, false, true>(d, st);
-  if (d->transA && !d->transB) return launch_gemm<BMT, BNT, true, false>(d, st);
-  return launch_gemm<BMT, BNT, true, true>(d, st);
+  if (!d->transA && !d->transB) return launch_gemm<BMT, BNT, WTM, WTN, false, false>(d, st);
+  if (!d->transA && d->transB) return launch_gemm<BMT, BNT, WTM, WTN, false, true>(d, st);
+  if (d->transA && !d->transB) return launch_gemm<BMT, BNT, WTM, WTN, true, false>(d, st);
+  return launch_gemm<BMT, BNT, WTM, WTN, true, true>(d, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -343,7 +350,18 @@ extern "C" int vief_dgemm_batched(const vief_gemm_desc* d, void* stream) {
   if (d->batch > 65535) { set_error("dgemm: batch %d > 65535", d->batch); return VF_EARG; }
   cudaStream_t st = (cudaStream_t)stream;
   // skinny M: 32 x 128 tiles (no idle DMMA rows); otherwise 64 x 64
-  const int rc = d->M <= 32 ? dispatch_gemm<32, 128>(d, st) : dispatch_gemm<64, 64>(d, st);
+  static int tile = -1;  // VF_GEMM_TILE (A/B timing of CTA / warp tilings)
+  if (tile < 0) {
+    const char* e = getenv("VF_GEMM_TILE");
+    tile = !e ? 0 : !strcmp(e, "64x64w16") ? 1 : !strcmp(e, "64x64w32") ? 2
+         : !strcmp(e, "128x64w16") ? 3 : !strcmp(e, "64x128w16") ? 4 : 0;
+  }
+  int rc;
+  if (d->M <= 32) rc = dispatch_gemm<32, 128>(d, st);
+  else if (tile == 1) rc = dispatch_gemm<64, 64, 32, 16>(d, st);
+  else if (tile == 3) rc = dispatch_gemm<128, 64, 32, 32>(d, st);
+  else if (tile == 4) rc = dispatch_gemm<64, 128, 32, 16>(d, st);
+  else rc = dispatch_gemm<64, 64, 32, 32>(d, st);
   if (rc) return rc;
   ++g_launches;
   VF_LAUNCH_CHECK("k_dgemm");

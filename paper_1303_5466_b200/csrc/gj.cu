@@ -22,6 +22,7 @@
 // interchanges are applied as (dst, src) permutations of the touched rows.  The pivots are the
 // partial-pivoting pivots of getrf (the trailing Schur complements coincide).
 #include <vector>
+#include <algorithm>
 #include "common.cuh"
 #include "panels.cuh"
 #include "../../include/vief_b200.h"
@@ -167,41 +168,67 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
   k_fill<<<cdiv(batch, 256), 256, 0, st>>>(pivmin, batch, INFINITY);
   k_fill<<<cdiv(batch, 256), 256, 0, st>>>(pivmax, batch, 0.0);
   g_launches += 2;
-  int rc = VF_OK;
-  for (int C0 = 0; C0 < n && rc == VF_OK; C0 += NBO) {
-    const int NB = n - C0 < NBO ? n - C0 : NBO;
-    // ---- inner steps restricted to block columns [C0, C0+NB)
-    for (int c0 = C0; c0 < C0 + NB && rc == VF_OK; c0 += nb) {
+  // Look-ahead: the inner (panel) steps of block C0+NBO run on a side stream
+  // as soon as the outer update has reached that block's columns, while the
+  // main stream finishes the outer update of all other columns.  The two
+  // touch disjoint columns of A and disjoint work buffers (the side stream
+  // owns Pw/Rw/Ai/ipiv-block/scratch/pairs until `inner_done` is waited on).
+  static cudaStream_t side = nullptr;
+  if (!side) {  // highest priority: its CTAs are scheduled ahead of the trailing GEMM's
+    int lo = 0, hi = 0;
+    VF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    VF_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
+  }
+  cudaEvent_t ev_next = nullptr, inner_done = nullptr;
+  VF_CUDA(cudaEventCreateWithFlags(&ev_next, cudaEventDisableTiming));
+  VF_CUDA(cudaEventCreateWithFlags(&inner_done, cudaEventDisableTiming));
+  auto inner = [&](int C0, int NB, cudaStream_t s, bool prof) -> int {
+    for (int c0 = C0; c0 < C0 + NB; c0 += nb) {
       const int nbs = C0 + NB - c0 < nb ? C0 + NB - c0 : nb;
-      prof_push(st, "gj.panel");
-      rc = lu_panel(A, sA, lda, n, c0, nbs, batch, ipiv, n, Ai, nb * nb, pivmin, pivmax, st);
-      if (rc) break;
-      prof_push(st, "gj.inner");
-      k_rowperm_build<<<batch, 256, 0, st>>>(ipiv, n, c0, c0 + nbs, n, scratch, pairs);
-      k_rowperm_apply<<<dim3(cdiv(NB, 8), batch), 256, 0, st>>>(A, sA, lda, C0, C0 + NB, pairs,
-                                                               2 * nbs);
-      g_launches += 1;
-      k_gj_prep<<<dim3(cdiv(n, 32), cdiv(nbs, 8), batch), dim3(32, 8), 0, st>>>(A, sA, lda, n, c0,
-                                                                                 nbs, Pw, sPw);
-      g_launches += 2;
+      if (prof) prof_push(s, "gj.panel");
+      int r = lu_panel(A, sA, lda, n, c0, nbs, batch, ipiv, n, Ai, nb * nb, pivmin, pivmax, s);
+      if (r) return r;
+      if (prof) prof_push(s, "gj.inner");
+      k_rowperm_build<<<batch, 256, 0, s>>>(ipiv, n, c0, c0 + nbs, n, scratch, pairs);
+      k_rowperm_apply<<<dim3(cdiv(NB, 8), batch), 256, 0, s>>>(A, sA, lda, C0, C0 + NB, pairs,
+                                                              2 * nbs);
+      k_gj_prep<<<dim3(cdiv(n, 32), cdiv(nbs, 8), batch), dim3(32, 8), 0, s>>>(A, sA, lda, n, c0,
+                                                                                nbs, Pw, sPw);
+      g_launches += 3;
       VF_LAUNCH_CHECK("gj swap/prep");
       vief_gemm_desc g{};  // Rw (nbs x NB, ld nb) = Ainv * A[c0:c0+nbs, C0:C0+NB]
       g.A = Ai; g.strideA = nb * nb; g.lda = nb;
       g.B = A + (long long)C0 * lda + c0; g.strideB = sA; g.ldb = lda;
       g.C = Rw; g.strideC = sRw; g.ldc = nb;
       g.M = nbs; g.N = NB; g.K = nbs; g.alpha = 1.0; g.beta = 0.0; g.batch = batch;
-      if ((rc = vief_dgemm_batched(&g, st))) break;
+      if ((r = vief_dgemm_batched(&g, s))) return r;
       vief_gemm_desc u{};  // A[:, C0:C0+NB] -= Pw * Rw
       u.A = Pw; u.strideA = sPw; u.lda = n;
       u.B = Rw; u.strideB = sRw; u.ldb = nb;
       u.C = A + (long long)C0 * lda; u.strideC = sA; u.ldc = lda;
       u.M = n; u.N = NB; u.K = nbs; u.alpha = -1.0; u.beta = 1.0; u.batch = batch;
-      if ((rc = vief_dgemm_batched(&u, st))) break;
-      rc = vief_copy2d(Rw, sRw, nullptr, nb, A + (long long)C0 * lda + c0, sA, nullptr, lda,
-                       nullptr, nbs, nullptr, NB, batch, st);
+      if ((r = vief_dgemm_batched(&u, s))) return r;
+      if ((r = vief_copy2d(Rw, sRw, nullptr, nb, A + (long long)C0 * lda + c0, sA, nullptr, lda,
+                           nullptr, nbs, nullptr, NB, batch, s)))
+        return r;
     }
-    if (rc) break;
-    if (NB == n) continue;  // single block: nothing outside it
+    return VF_OK;
+  };
+  auto outer_gemm = [&](int C0, int NB, int j0, int nj, cudaStream_t s) -> int {
+    if (nj <= 0) return VF_OK;
+    vief_gemm_desc u{};  // A[:, j0:j0+nj] += Xw * Ro[:, j0:j0+nj]
+    u.A = Xw; u.strideA = sX; u.lda = n;
+    u.B = Ro + (long long)j0 * NBO; u.strideB = sX; u.ldb = NBO;
+    u.C = A + (long long)j0 * lda; u.strideC = sA; u.ldc = lda;
+    u.M = n; u.N = nj; u.K = NB; u.alpha = 1.0; u.beta = 1.0; u.batch = batch;
+    return vief_dgemm_batched(&u, s);
+  };
+  int rc = inner(0, std::min(n, NBO), st, true);
+  bool pending = false;  // inner steps of the current block still running on `side`
+  for (int C0 = 0; C0 < n && rc == VF_OK; C0 += NBO) {
+    const int NB = n - C0 < NBO ? n - C0 : NBO;
+    if (pending) { VF_CUDA(cudaStreamWaitEvent(st, inner_done, 0)); pending = false; }
+    if (NB == n) break;  // single block: nothing outside it
     // ---- outer update of all other columns
     prof_push(st, "gj.outer_prep");
     k_rowperm_build<<<batch, 256, 0, st>>>(ipiv, n, C0, C0 + NB, n, scratch, pairs);
@@ -219,18 +246,21 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
                           n, nullptr, NB, batch, st)))
       break;
     prof_push(st, "gj.gemm_update");
-    for (int side = 0; side < 2; ++side) {
-      const int j0 = side == 0 ? 0 : C0 + NB;
-      const int nj = side == 0 ? C0 : n - C0 - NB;
-      if (nj <= 0) continue;
-      vief_gemm_desc u{};  // A[:, j0:j0+nj] += Xw * Ro[:, j0:j0+nj]
-      u.A = Xw; u.strideA = sX; u.lda = n;
-      u.B = Ro + (long long)j0 * NBO; u.strideB = sX; u.ldb = NBO;
-      u.C = A + (long long)j0 * lda; u.strideC = sA; u.ldc = lda;
-      u.M = n; u.N = nj; u.K = NB; u.alpha = 1.0; u.beta = 1.0; u.batch = batch;
-      if ((rc = vief_dgemm_batched(&u, st))) break;
+    const int N1 = C0 + NB, NB1 = std::min(NBO, n - N1);  // the next block
+    if (NB1 > 0) {
+      if ((rc = outer_gemm(C0, NB, N1, NB1, st))) break;
+      VF_CUDA(cudaEventRecord(ev_next, st));
+      VF_CUDA(cudaStreamWaitEvent(side, ev_next, 0));
+      if ((rc = inner(N1, NB1, side, false))) break;
+      VF_CUDA(cudaEventRecord(inner_done, side));
+      pending = true;
     }
+    if ((rc = outer_gemm(C0, NB, 0, C0, st))) break;
+    if ((rc = outer_gemm(C0, NB, N1 + NB1, n - N1 - NB1, st))) break;
   }
+  if (pending) VF_CUDA(cudaStreamWaitEvent(st, inner_done, 0));
+  cudaEventDestroy(ev_next);
+  cudaEventDestroy(inner_done);
   prof_push(st, "gj.colswap");
   if (rc == VF_OK) {  // column interchanges as one gather into a temporary, copied back
     double* tmp = nullptr;

@@ -384,10 +384,9 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
   __shared__ XSel xch[2];
   __shared__ double Qb[PNB][HSK];
   __shared__ double yv[HSK], dv[PNB];
-  __shared__ double redv[32];
-  __shared__ int redi[32];
+  __shared__ double redv[NW];
+  __shared__ int redi[NW];
   __shared__ int sel[PNB];
-  __shared__ int s_gi, s_own;
   const int c0 = cr * cols_per, c1 = min(n, c0 + cols_per), nc = max(c1 - c0, 0);
   constexpr int LDY = HSK + 1;  // odd column stride: thread-per-column reads are conflict free
   double* Ys = sm;              // LDY x cols_per
@@ -413,53 +412,74 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
     nrm[c] = s;
     if (s > bv) { bv = s; bi = c0 + c; }
   }
+  // per step: CTA argmax (1 barrier), cluster exchange (1 cluster barrier),
+  // warp 0 picks the winner and orthogonalises its sketch column against the
+  // chosen ones (no block barriers), then every thread downdates its columns'
+  // residual norms and keeps its next candidate (1 barrier)
   for (int i = 0; i < bs; ++i) {
     XSel& x = xch[i & 1];
     double v = bv;
     int iv = bi;
-    block_argmax(v, iv, redv, redi);
-    if (tid == 0) { x.cand_v = v; x.cand_i = iv; }
-    if (v >= 0.0 && tid < HSK) x.y[tid] = Ys[(iv - c0) * LDY + tid];
+    warp_argmax(v, iv);
+    if (lane == 0) { redv[warp] = v; redi[warp] = iv; }
+    __syncthreads();
+    if (warp == 0) {
+      double cv = lane < NW ? redv[lane] : -2.0;
+      int ci = lane < NW ? redi[lane] : 0x7fffffff;
+      warp_argmax(cv, ci);
+      if (lane == 0) { x.cand_v = cv; x.cand_i = ci; }
+      if (cv >= 0.0) {
+        x.y[lane] = Ys[(ci - c0) * LDY + lane];
+        if (lane + 32 < HSK) x.y[lane + 32] = Ys[(ci - c0) * LDY + lane + 32];
+      }
+    }
     cl.sync();
-    if (tid < 32) {
+    if (warp == 0) {
       double cv = -2.0;
       int ci = 0x7fffffff;
-      if (tid < cs) { XSel* xr = remote(cl, &x, tid); cv = xr->cand_v; ci = xr->cand_i; }
+      if (lane < cs) { XSel* xr = remote(cl, &x, lane); cv = xr->cand_v; ci = xr->cand_i; }
       warp_argmax(cv, ci);
       if (ci < 0 || ci >= n) ci = min(i, n - 1);  // defensive (NaN data): stay in range
-      if (tid == 0) { s_gi = ci; s_own = ci / cols_per; sel[i] = ci; }
-    }
-    __syncthreads();
-    const int gi = s_gi;
-    if (tid < HSK) yv[tid] = remote(cl, &x, s_own)->y[tid];
-    if (gi >= c0 && gi < c1 && tid == 0) nrm[gi - c0] = -1.0;
-    __syncthreads();
-    // q = (I - Qb Qb^T) y, twice (classical Gram-Schmidt with reorthogonalisation)
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int c = warp; c < i; c += NW) {
-        double d = Qb[c][lane] * yv[lane];
-        if (lane + 32 < HSK) d = fma(Qb[c][lane + 32], yv[lane + 32], d);
-        d = warp_sum(d);
-        if (lane == 0) dv[c] = d;
+      const XSel* xo = remote(cl, &x, ci / cols_per);
+      double y0 = xo->y[lane];
+      double y1 = lane + 32 < HSK ? xo->y[lane + 32] : 0.0;
+      if (lane == 0) {
+        sel[i] = ci;
+        if (ci >= c0 && ci < c1) nrm[ci - c0] = -1.0;
       }
-      __syncthreads();
-      if (tid < HSK) {
-        double a0 = yv[tid], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int c = 0;
-        for (; c + 3 < i; c += 4) {
-          a0 = fma(-dv[c], Qb[c][tid], a0); a1 = fma(-dv[c + 1], Qb[c + 1][tid], a1);
-          a2 = fma(-dv[c + 2], Qb[c + 2][tid], a2); a3 = fma(-dv[c + 3], Qb[c + 3][tid], a3);
+      // classical Gram-Schmidt against Qb[0..i), twice
+      for (int pass = 0; pass < 2; ++pass) {
+        yv[lane] = y0;
+        if (lane + 32 < HSK) yv[lane + 32] = y1;
+        __syncwarp();
+        if (lane < i) {  // lane c: dv[c] = Qb[c] . y
+          double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+          for (int r = 0; r < HSK; r += 4) {
+            d0 = fma(Qb[lane][r], yv[r], d0); d1 = fma(Qb[lane][r + 1], yv[r + 1], d1);
+            d2 = fma(Qb[lane][r + 2], yv[r + 2], d2); d3 = fma(Qb[lane][r + 3], yv[r + 3], d3);
+          }
+          dv[lane] = (d0 + d1) + (d2 + d3);
         }
-        for (; c < i; ++c) a0 = fma(-dv[c], Qb[c][tid], a0);
-        yv[tid] = (a0 + a1) + (a2 + a3);
+        __syncwarp();
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        int c = 0;
+        for (; c + 1 < i; c += 2) {
+          a0 = fma(dv[c], Qb[c][lane], a0); a1 = fma(dv[c + 1], Qb[c + 1][lane], a1);
+          if (lane + 32 < HSK) {
+            b0 = fma(dv[c], Qb[c][lane + 32], b0); b1 = fma(dv[c + 1], Qb[c + 1][lane + 32], b1);
+          }
+        }
+        if (c < i) {
+          a0 = fma(dv[c], Qb[c][lane], a0);
+          if (lane + 32 < HSK) b0 = fma(dv[c], Qb[c][lane + 32], b0);
+        }
+        y0 -= a0 + a1;
+        y1 -= b0 + b1;
+        __syncwarp();
       }
-      __syncthreads();
-    }
-    if (warp == 0) {
-      double y0 = yv[lane];
-      double y1 = lane + 32 < HSK ? yv[lane + 32] : 0.0;
-      double nn = warp_sum(y0 * y0 + y1 * y1);
-      double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+      const double nn = warp_sum(y0 * y0 + y1 * y1);
+      const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
       Qb[i][lane] = y0 * inv;
       if (lane + 32 < HSK) Qb[i][lane + 32] = y1 * inv;
     }
@@ -485,24 +505,48 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
     }
   }
   cl.sync();
-  if (cr != 0 || tid != 0) return;
-  int mid[2 * PNB + 2], mpos[2 * PNB + 2];
+  if (cr != 0 || warp != 0) return;
+  // swap list (dst = J+i, src = current position of the chosen column),
+  // tracking moved columns as (id, pos) pairs; lookups are warp ballots
+  constexpr int NM = 2 * PNB + 2;
+  __shared__ int mid[NM], mpos[NM];
   int nm = 0;
   for (int i = 0; i < bs; ++i) {
-    const int id = J + sel[i];
-    int src = id;
-    for (int t = 0; t < nm; ++t) if (mid[t] == id) src = mpos[t];
-    const int dst = J + i;
-    int at_dst = dst;
-    for (int t = 0; t < nm; ++t) if (mpos[t] == dst) at_dst = mid[t];
-    swaps[b * PNB + i] = src;
-    bool f1 = false, f2 = false;
-    for (int t = 0; t < nm; ++t) {
-      if (mid[t] == at_dst) { mpos[t] = src; f1 = true; }
-      else if (mid[t] == id) { mpos[t] = dst; f2 = true; }
+    const int id = J + sel[i], dst = J + i;
+    int src = id, at_dst = dst;
+    unsigned f_id = 0, f_dst = 0;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      const int t = lane + 32 * h;
+      const bool live = t < nm;
+      const unsigned bid = __ballot_sync(0xffffffffu, live && mid[t] == id);
+      const unsigned bds = __ballot_sync(0xffffffffu, live && mpos[t] == dst);
+      if (bid && !f_id) { src = mpos[32 * h + __ffs(bid) - 1]; f_id = 1; }
+      if (bds && !f_dst) { at_dst = mid[32 * h + __ffs(bds) - 1]; f_dst = 1; }
     }
-    if (!f1 && at_dst != src) { mid[nm] = at_dst; mpos[nm] = src; ++nm; }
-    if (!f2 && id != dst) { mid[nm] = id; mpos[nm] = dst; ++nm; }
+    if (lane == 0) swaps[b * PNB + i] = src;
+    bool f1 = false, f2 = false;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      const int t = lane + 32 * h;
+      bool m1 = false, m2 = false;
+      if (t < nm) {
+        if (mid[t] == at_dst) { mpos[t] = src; m1 = true; }
+        else if (mid[t] == id) { mpos[t] = dst; m2 = true; }
+      }
+      f1 |= __any_sync(0xffffffffu, m1);
+      f2 |= __any_sync(0xffffffffu, m2);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (!f1 && at_dst != src) { mid[nm] = at_dst; mpos[nm] = src; }
+      if (!f2 && id != dst) {
+        const int k = nm + ((!f1 && at_dst != src) ? 1 : 0);
+        mid[k] = id; mpos[k] = dst;
+      }
+    }
+    nm += ((!f1 && at_dst != src) ? 1 : 0) + ((!f2 && id != dst) ? 1 : 0);
+    __syncwarp();
   }
 }
 
@@ -1029,12 +1073,13 @@ int lu_panel(const double* A, long long sA, int lda, int n, int c0, int nbs, int
 int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* active,
              const int* bsv, int J, int maxp, int count, double* Qw, long long sQ, int ldq,
              double* Rt, cudaStream_t st) {
-  if (maxp <= 16 * 2 * PT && panel_mode() != 1) {
-    const int rpt = maxp <= PT ? 1 : 2;
+  if (maxp <= 16 * 3 * PT && panel_mode() != 1) {
+    const int rpt = maxp <= PT ? 1 : (maxp <= 16 * 2 * PT ? 2 : 3);
     const int cs = (maxp + rpt * PT - 1) / (rpt * PT);
     void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
                     (void*)&J, (void*)&Qw, (void*)&sQ, (void*)&ldq, (void*)&Rt};
-    const void* fn = rpt == 1 ? (const void*)k_qr_panel_rr<1> : (const void*)k_qr_panel_rr<2>;
+    const void* fn = rpt == 1 ? (const void*)k_qr_panel_rr<1>
+                   : rpt == 2 ? (const void*)k_qr_panel_rr<2> : (const void*)k_qr_panel_rr<3>;
     return launch_cluster(fn, count, cs, 0, st, args);
   }
   int cs = pick_cs(maxp, 640, count);

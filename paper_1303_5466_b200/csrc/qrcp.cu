@@ -666,7 +666,8 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   VF_CUDA(cudaMemsetAsync(Rm, 0, sizeof(double) * sR * count, st));
   int Kmax = 0;
   const size_t smem_small = ((size_t)(maxp | 1) * maxm + 2 * (size_t)maxm) * sizeof(double);
-  const bool small = !d->force_blocked && smem_small <= 220 * 1024;
+  // measured: the one-CTA-per-matrix SMEM QRCP wins only while two CTAs fit an SM
+  const bool small = !d->force_blocked && smem_small <= 110 * 1024;
   int* kdev = d->rank;
   if (small) {
     prof_push(st, "id.small_qrcp");

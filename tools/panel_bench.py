@@ -22,7 +22,16 @@ for spec in a.inv.split(","):
     for rep in range(2):
         A = A0.clone()
         _lib.prof_prefix(f"inv{n}x{b}.")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         _lib.inv_batched(A, n * n, n, n, b)
+        e1.record()
+        torch.cuda.synchronize()
+        if rep:
+            fl = 2.0 * n ** 3 * b
+            print(f"inv {n}x{b}: {e0.elapsed_time(e1):.2f} ms  {fl / e0.elapsed_time(e1) / 1e9:.2f} TF/s")
+    err = (torch.linalg.inv(A0[:2]) - A[:2]).abs().max().item() / A[:2].abs().max().item()
+    print(f"  inverse check (first 2): max rel err {err:.2e}")
     torch.cuda.synchronize()
     del A, A0
 import ctypes
@@ -47,7 +56,8 @@ for spec in a.id.split(","):
         perm = torch.zeros((c, m), dtype=torch.int32, device="cuda")
         T = torch.zeros((c, m, m), dtype=torch.float64, device="cuda")
         d = _lib.IdDesc(_lib.ptr(A), m * ldA, ldA, _lib.ptr(pv), _lib.ptr(mv), p, m, c, 2, 1e-10,
-                        _lib.ptr(rank), _lib.ptr(perm), _lib.ptr(T), m * m, m, 0, 1)
+                        _lib.ptr(rank), _lib.ptr(perm), _lib.ptr(T), m * m, m, 0,
+                        int(os.environ.get("VF_FB", "1")))
         _lib.prof_prefix(f"id{p}x{m}x{c}.")
         _lib.call("vief_id_batched", ctypes.byref(d), _lib.stream_handle())
         torch.cuda.synchronize()
