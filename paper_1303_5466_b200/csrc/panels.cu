@@ -174,15 +174,15 @@ struct XGram {
 __global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long sA, int lda,
                                                     const int* pv, const int* active,
                                                     const int* bsv, int J, int rows_per,
-                                                    double* Qw, long long sQ, int ldq,
-                                                    double* Rt) {
+                                                    double* Vw, long long sV, int ldv,
+                                                    double* Tt, double* Rt) {
   cg::cluster_group cl = cg::this_cluster();
   const int cs = cl.num_blocks(), cr = cl.block_rank();
   const int b = blockIdx.x / cs;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (!active[b] || bsv[b] <= 0) return;  // uniform for the whole cluster
   const int bs = bsv[b];
-  const int p = pv[b];
+  const int p = pv[b] - J;  // panel rows J..p-1
   extern __shared__ double sm[];
   __shared__ XQr xch[2];
   // Gram exchange lives in dynamic shared memory after the panel slice
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long s
   const int ldp = rows_per;
   double* P = sm;
   XGram& xg = *reinterpret_cast<XGram*>(sm + (long long)rows_per * PNB);
-  const double* Ab = A + b * sA + (long long)J * lda;
+  const double* Ab = A + b * sA + (long long)J * lda + J;
   for (int idx = tid; idx < nr * bs; idx += PT) {
     int i = idx % nr, c = idx / nr;
     P[c * ldp + i] = Ab[(long long)c * lda + r0 + i];
@@ -330,33 +330,20 @@ __global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long s
     }
   }
   __syncthreads();
-  // M = T V1^T  (bs x bs): M(a, c) = sum_k T(a,k) V1(c,k)
-  __shared__ double V1s[PNB][PNB + 1];
-  for (int idx = tid; idx < bs * bs; idx += PT) {
-    const int r = idx % bs, c = idx / bs;
-    V1s[r][c] = x0->V1[c * PNB + r];
-  }
-  __syncthreads();
-  for (int idx = tid; idx < bs * bs; idx += PT) {
-    const int a = idx % bs, c = idx / bs;
-    double s = 0.0;
-    for (int k = a; k < bs; ++k) s = fma(Tm[a][k], V1s[c][k], s);
-    Mm[a][c] = s;
-  }
   cl.sync();  // remote reads done before any CTA may exit / reuse
-  // Q_local = E - V M
-  double* Qo = Qw + b * sQ;
+  // V (already unit lower trapezoidal in P) at absolute rows J.., T and R from CTA 0
+  double* Vo = Vw + b * sV + J;
   for (int idx = tid; idx < nr * bs; idx += PT) {
     const int i = idx % nr, c = idx / nr;
-    double s = 0.0;
-    for (int k = 0; k < bs; ++k) s = fma(P[k * ldp + i], Mm[k][c], s);
-    Qo[(long long)c * ldq + r0 + i] = ((r0 + i == c) ? 1.0 : 0.0) - s;
+    Vo[(long long)c * ldv + r0 + i] = P[c * ldp + i];
   }
   if (cr == 0) {
     double* Rr = Rt + (long long)b * PNB * PNB;
+    double* To = Tt + (long long)b * PNB * PNB;
     for (int idx = tid; idx < PNB * PNB; idx += PT) {
       int i = idx % PNB, c = idx / PNB;
       Rr[c * PNB + i] = Rl[i][c];
+      To[c * PNB + i] = Tm[i][c];
     }
   }
 }
@@ -788,8 +775,9 @@ struct XQr2 {
 template <int RPT>
 __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long long sA, int lda,
                                                        const int* pv, const int* active,
-                                                       const int* bsv, int J, double* Qw,
-                                                       long long sQ, int ldq, double* Rt) {
+                                                       const int* bsv, int J, double* Vw,
+                                                       long long sV, int ldv, double* Tt,
+                                                       double* Rt) {
   constexpr int RP = PT * RPT;
   cg::cluster_group cl = cg::this_cluster();
   const int cs = cl.num_blocks(), cr = cl.block_rank();
@@ -797,7 +785,7 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (!active[b] || bsv[b] <= 0) return;  // uniform for the whole cluster
   const int bs = bsv[b];
-  const int p = pv[b];
+  const int p = pv[b] - J;  // panel rows J..p-1 (Householder form: rows < J are finished)
   __shared__ XQr2 xch[2];
   __shared__ double red[NW][PNB];
   __shared__ double Sp[2 * NW][PNB];
@@ -810,7 +798,7 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
     Rl[i][c] = 0.0; Gm[i][c] = 0.0; V1[i][c] = 0.0; Tm[i][c] = 0.0;
   }
   if (tid < PNB) { tau[tid] = 0.0; w[tid] = 0.0; }
-  const double* Ab = A + b * sA + (long long)J * lda;
+  const double* Ab = A + b * sA + (long long)J * lda + J;
   double a[RPT][PNB];
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
@@ -941,35 +929,24 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
     }
   }
   __syncthreads();
-  // M = T V1^T into Gm: M(a, c) = sum_k T(a,k) V1(c,k)
-  for (int idx = tid; idx < bs * bs; idx += PT) {
-    const int a0 = idx % bs, c = idx / bs;
-    double s = 0.0;
-    for (int k = a0; k < bs; ++k) s = fma(Tm[a0][k], V1[c][k], s);
-    Gm[a0][c] = s;
-  }
-  __syncthreads();
-  // V rows above bs: unit diagonal, zeros to the right; Q = E - V M
-  double* Qo = Qw + b * sQ;
+  // V (unit lower trapezoidal: 1 on the diagonal, 0 above) at absolute rows J..
+  double* Vo = Vw + b * sV + J;
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
     const int g = r0 + tid + q * PT;
-    if (g < bs)
+    if (g < p)
 #pragma unroll
       for (int t = 0; t < PNB; ++t) {
-        const int k = (jmax + t) & (PNB - 1);
-        a[q][t] = (k == g) ? 1.0 : (k > g ? 0.0 : a[q][t]);
+        const int k = (jmax + t) & (PNB - 1);  // the column at position t
+        if (k < bs) Vo[(long long)k * ldv + g] = (k == g) ? 1.0 : (k > g ? 0.0 : a[q][t]);
       }
-    if (g < p)
-      for (int c = 0; c < bs; ++c) {
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int t = 0; t < PNB; t += 2) {
-          s0 = fma(a[q][t], Gm[(jmax + t) & (PNB - 1)][c], s0);
-          s1 = fma(a[q][t + 1], Gm[(jmax + t + 1) & (PNB - 1)][c], s1);
-        }
-        Qo[(long long)c * ldq + g] = ((g == c) ? 1.0 : 0.0) - (s0 + s1);
-      }
+  }
+  if (cr == 0) {
+    double* To = Tt + (long long)b * PNB * PNB;
+    for (int idx = tid; idx < PNB * PNB; idx += PT) {
+      const int i = idx % PNB, c = idx / PNB;
+      To[c * PNB + i] = Tm[i][c];
+    }
   }
   if (cr == 0) {
     double* Rr = Rt + (long long)b * PNB * PNB;
@@ -1071,24 +1048,26 @@ int lu_panel(const double* A, long long sA, int lda, int n, int c0, int nbs, int
 }
 
 int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* active,
-             const int* bsv, int J, int maxp, int count, double* Qw, long long sQ, int ldq,
-             double* Rt, cudaStream_t st) {
-  if (maxp <= 16 * 3 * PT && panel_mode() != 1) {
-    const int rpt = maxp <= PT ? 1 : (maxp <= 16 * 2 * PT ? 2 : 3);
-    const int cs = (maxp + rpt * PT - 1) / (rpt * PT);
+             const int* bsv, int J, int maxp, int count, double* Vw, long long sV, int ldv,
+             double* Tt, double* Rt, cudaStream_t st) {
+  const int rows = maxp - J;  // panel rows J..p-1
+  if (rows <= 16 * 3 * PT && panel_mode() != 1) {
+    const int rpt = rows <= PT ? 1 : (rows <= 16 * 2 * PT ? 2 : 3);
+    const int cs = (rows + rpt * PT - 1) / (rpt * PT);
     void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
-                    (void*)&J, (void*)&Qw, (void*)&sQ, (void*)&ldq, (void*)&Rt};
+                    (void*)&J, (void*)&Vw, (void*)&sV, (void*)&ldv, (void*)&Tt, (void*)&Rt};
     const void* fn = rpt == 1 ? (const void*)k_qr_panel_rr<1>
                    : rpt == 2 ? (const void*)k_qr_panel_rr<2> : (const void*)k_qr_panel_rr<3>;
     return launch_cluster(fn, count, cs, 0, st, args);
   }
-  int cs = pick_cs(maxp, 640, count);
-  int rows_per = (maxp + cs - 1) / cs;
+  int cs = pick_cs(rows, 640, count);
+  int rows_per = (rows + cs - 1) / cs;
   if (rows_per < PNB) rows_per = PNB;
   rows_per = (rows_per + 1) & ~1;
   size_t smem = (size_t)rows_per * PNB * sizeof(double) + sizeof(XGram);
   void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
-                  (void*)&J, (void*)&rows_per, (void*)&Qw, (void*)&sQ, (void*)&ldq, (void*)&Rt};
+                  (void*)&J, (void*)&rows_per, (void*)&Vw, (void*)&sV, (void*)&ldv, (void*)&Tt,
+                  (void*)&Rt};
   return launch_cluster((const void*)k_qr_panel_cl, count, cs, smem, st, args);
 }
 

@@ -10,9 +10,11 @@ constexpr int HSK = PNB + 8;  // sketch rows
 int lu_panel(const double* A, long long sA, int lda, int n, int c0, int nbs, int batch, int* ipiv,
              long long sPiv, double* Ainv, long long sAi, double* pivmin, double* pivmax,
              cudaStream_t st);
+// Householder QR of A(J:p, J:J+bs) -> V (unit lower trapezoidal, written at
+// absolute rows J..p-1 of Vw), T (upper, block reflector I - V T V^T), R11
 int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* active,
-             const int* bsv, int J, int maxp, int count, double* Qw, long long sQ, int ldq,
-             double* Rt, cudaStream_t st);
+             const int* bsv, int J, int maxp, int count, double* Vw, long long sV, int ldv,
+             double* Tt, double* Rt, cudaStream_t st);
 int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const int* active,
                   const int* bsv, int J, int maxm, int count, int* swaps, cudaStream_t st);
 }  // namespace vf

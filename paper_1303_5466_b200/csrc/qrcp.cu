@@ -272,9 +272,10 @@ __global__ void k_norm_exact(const double* A, long long sA, int lda, const int* 
   if (bs <= 0 || c >= m) return;
   const long long o = (long long)b * ldt + c;
   if (!flag[o]) return;
+  // Householder form: the residual of column c lives in rows J+bs..p-1
   const double* a = A + b * sA + (long long)c * lda;
   double s = 0.0;
-  for (int i = lane; i < p; i += 32) s = fma(a[i], a[i], s);
+  for (int i = J + bs + lane; i < p; i += 32) s = fma(a[i], a[i], s);
   s = sqrt(warp_sum(s));
   if (lane == 0) { tn[o] = s; tn0[o] = s; flag[o] = 0; }
 }
@@ -293,18 +294,23 @@ struct HState {
   double* tn;     // count x maxm trailing residual norms (travel with their columns)
   double* tn0;    // last exactly computed norm of each column (downdating reference)
   int* flag;      // count x maxm: column needs an exact norm
+  int* pf;        // p - Jf (rows touched by the pending reflectors) if active else 0
   double* Rt;     // count x HB x HB block R (upper)
-  double* Qw;     // count x maxp x (HB*D): explicit panel Q's of the pending blocks
-  double* G;      // count x HB x (HB*D): Q_i^T Qcat
+  double* Tt;     // count x HB x HB block reflector T (upper)
+  double* Vw;     // count x maxp x (HB*D): Householder vectors of the pending blocks
+  double* Up;     // count x (HB*D) x maxm: U = T_cat^T V_cat^T A_stale (pending blocks)
+  double* X;      // count x HB x maxm: V_i^T A_stale
+  double* G;      // count x HB x (HB*D): V_i^T V_cat
   int D;          // inner blocks per delayed trailing update
-  double* work;   // count x maxp x HB panel work copy (large panels)
   double* Y;      // count x HS x maxm sketch
-  double* Z;      // count x HS x HB
+  double* Om;     // count x HS x maxp: Omega H_1 ... H_i (sketch in original coordinates)
+  double* OV;     // count x HS x HB
+  double* OVT;    // count x HS x HB
   int* any;       // 1 int: any active
   int ldtn;       // row stride of tn (= maxm)
 };
 
-__global__ void k_block_setup(int J, const int* pv, const int* mv, int count, HState S) {
+__global__ void k_block_setup(int J, int Jf, const int* pv, const int* mv, int count, HState S) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= count) return;
   const int act = S.active[b];
@@ -313,14 +319,35 @@ __global__ void k_block_setup(int J, const int* pv, const int* mv, int count, HS
   if (bs < 0) bs = 0;
   S.bs[b] = bs;
   S.nrem[b] = act ? max(m - J - bs, 0) : 0;
-  S.pact[b] = act ? pv[b] : 0;
+  S.pact[b] = act ? max(pv[b] - J, 0) : 0;
+  S.pf[b] = act ? max(pv[b] - Jf, 0) : 0;
   S.sact[b] = act ? HS : 0;
+}
+
+// rows [r0, r1) of the HB columns of a pending-reflector block are zero
+// (V_i lives at rows >= J_i; the stacked GEMMs start at row Jf)
+__global__ void k_zero_rows(double* V, long long sV, int ldv, int r0, int r1, const int* active) {
+  const int b = blockIdx.y;
+  if (!active[b]) return;
+  const int n = r1 - r0;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * HB; idx += gridDim.x * blockDim.x) {
+    const int r = idx % n, c = idx / n;
+    V[b * sV + (long long)c * ldv + r0 + r] = 0.0;
+  }
+}
+
+// per-item copy of the shared Gaussian sketch matrix
+__global__ void k_bcast_omega(const double* Om, long long n, double* Omr, int count) {
+  const int b = blockIdx.y;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    Omr[b * n + i] = Om[i];
 }
 
 // apply the swap sequence to A (p rows), Y (HS rows), perm, and the norms.
 __global__ void k_apply_swaps(double* A, long long sA, int lda, double* Y, long long sY, int ldy,
                               int* perm, int ldperm, const int* pv, int J, HState S,
-                              double* Rm, long long sR, int ldR) {
+                              double* Rm, long long sR, int ldR, int kp, int ldU) {
   const int b = blockIdx.y;
   if (!S.active[b]) return;
   const int bs = S.bs[b];
@@ -344,6 +371,16 @@ __global__ void k_apply_swaps(double* A, long long sA, int lda, double* Y, long 
       if (src != dst) {
         double t = rr[(long long)src * ldR]; rr[(long long)src * ldR] = rr[(long long)dst * ldR];
         rr[(long long)dst * ldR] = t;
+      }
+    }
+  }
+  if (r < kp) {  // pending U rows travel with their columns
+    double* u = S.Up + (long long)b * ldU * S.ldtn + r;
+    for (int i = 0; i < bs; ++i) {
+      const int src = sw[i], dst = J + i;
+      if (src != dst) {
+        double t = u[(long long)src * ldU]; u[(long long)src * ldU] = u[(long long)dst * ldU];
+        u[(long long)dst * ldU] = t;
       }
     }
   }
@@ -684,23 +721,34 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     HState S{};
     S.active = buf.get<int>(count); S.done = buf.get<int>(count); S.k = kdev;
     S.bs = buf.get<int>(count); S.nrem = buf.get<int>(count); S.pact = buf.get<int>(count);
-    S.sact = buf.get<int>(count); S.swaps = buf.get<int>((size_t)HB * count);
+    S.sact = buf.get<int>(count); S.pf = buf.get<int>(count);
+    S.swaps = buf.get<int>((size_t)HB * count);
     S.cut = buf.get<double>(count); S.tn = buf.get<double>((size_t)maxm * count);
     S.tn0 = buf.get<double>((size_t)maxm * count);
     S.flag = buf.get<int>((size_t)maxm * count);
     S.Rt = buf.get<double>((size_t)HB * HB * count);
+    S.Tt = buf.get<double>((size_t)HB * HB * count);
     S.D = maxm >= 4096 ? 8 : (maxm >= 2048 ? 4 : (maxm >= 512 ? 2 : 1));
-    S.Qw = buf.get<double>((size_t)maxp * HB * S.D * count);
-    S.G = buf.get<double>((size_t)HB * HB * S.D * count);
-    S.work = nullptr;
+    const int D = S.D, ldU = HB * D;
+    S.Vw = buf.get<double>((size_t)maxp * HB * D * count);
+    S.Up = buf.get<double>((size_t)ldU * maxm * count);
+    S.X = buf.get<double>((size_t)HB * maxm * count);
+    S.G = buf.get<double>((size_t)HB * HB * D * count);
     S.Y = buf.get<double>((size_t)HS * maxm * count);
-    S.Z = buf.get<double>((size_t)HS * HB * count);
+    S.Om = buf.get<double>((size_t)HS * maxp * count);
+    S.OV = buf.get<double>((size_t)HS * HB * count);
+    S.OVT = buf.get<double>((size_t)HS * HB * count);
     S.any = buf.get<int>(1);
     S.ldtn = maxm;
     double* Om = buf.get<double>((size_t)HS * maxp);
-    if (!S.Y || !S.Qw || !Om || !S.any) { set_error("id: out of device memory (blocked)"); return VF_ENOMEM; }
+    if (!S.Y || !S.Vw || !S.Up || !S.X || !S.Om || !Om || !S.any) {
+      set_error("id: out of device memory (blocked)");
+      return VF_ENOMEM;
+    }
     prof_push(st, "id.init+sketch");
-    const long long sY = (long long)HS * maxm, sQ = (long long)maxp * HB * S.D;
+    const long long sY = (long long)HS * maxm, sV = (long long)maxp * HB * D;
+    const long long sU = (long long)ldU * maxm, sX = (long long)HB * maxm;
+    const long long sOm = (long long)HS * maxp;
     k_iota<<<dim3(cdiv(maxm, 128), count), 128, 0, st>>>(d->perm, maxm, d->m, count);
     k_colnorms<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m,
                                                            nullptr, 0, S.tn, maxm);
@@ -710,7 +758,9 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     k_init_state<<<cdiv(count, 128), 128, 0, st>>>(S, colmax, d->p, d->m, count, d->eps);
     k_gaussian<<<cdiv((long long)HS * maxp, 256), 256, 0, st>>>(Om, (long long)HS * maxp,
                                                                d->seed ^ 0x5eedULL);
-    g_launches += 5;
+    k_bcast_omega<<<dim3(std::min<unsigned>(cdiv((long long)HS * maxp, 256), 64u), count), 256, 0, st>>>(
+        Om, sOm, S.Om, count);
+    g_launches += 6;
     VF_LAUNCH_CHECK("id init");
     int rc;
     {  // Y = Omega A
@@ -723,69 +773,122 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       if ((rc = vief_dgemm_batched(&g, st))) return rc;
     }
     const int kcap = std::min(maxp, maxm);
-    // Trailing updates are delayed over D inner blocks (K = 32 D in the update
-    // GEMM).  Between flushes: the panel is made current with the pending
-    // (Q, W) pairs, W of a new block is corrected for the pending blocks, and
-    // norms recomputed exactly use the implicit residual a - Qcat W.
-    const int D = S.D;
+    // Blocked Householder QRCP (rows shrink: block J works on rows J..p-1)
+    // with pivots from the downdated sketch.  The reflectors of up to D
+    // blocks are aggregated (compact WY, A_cur = A_stale - V_cat U_cat with
+    // U_cat = T_cat^T V_cat^T A_stale) before one trailing update (K = 32 D):
+    //   X_i = V_i^T A_stale,  U_i = T_i^T (X_i - (V_i^T V_cat) U_cat),
+    //   R(J block, trail) = A_stale(J rows) - [V_cat V_i](J rows) [U_cat; U_i].
+    // The sketch is kept in original coordinates: Omega_i = Omega H_1..H_i,
+    // Y_trail -= Omega_i(:, J block) R(J block, trail).
     int pend = 0, Jf = 0;
     for (int J = 0; J < kcap; J += HB) {
+      const int kp = pend * HB;  // pending reflector columns
       prof_push(st, "id.setup+select");
-      k_block_setup<<<cdiv(count, 128), 128, 0, st>>>(J, d->p, d->m, count, S);
+      k_block_setup<<<cdiv(count, 128), 128, 0, st>>>(J, Jf, d->p, d->m, count, S);
       ++g_launches;
       if ((rc = sketch_select(S.Y, HS, sY, d->m, S.active, S.bs, J, maxm, count, S.swaps, st)))
         return rc;
       prof_push(st, "id.swaps");
-      k_apply_swaps<<<dim3(cdiv(std::max(std::max(maxp, HS), J), 128), count), 128, 0, st>>>(
-          d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S, Rm, sR, ldR);
+      k_apply_swaps<<<dim3(cdiv(std::max(std::max(maxp, HS), std::max(J, kp)), 128), count), 128,
+                      0, st>>>(d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S, Rm,
+                               sR, ldR, kp, ldU);
       g_launches += 2;
       VF_LAUNCH_CHECK("id select/swap");
-      double* Qi = S.Qw + (long long)pend * HB * maxp;
-      const int kp = pend * HB;  // pending Q columns
-      if (pend > 0) {  // make the panel current: A(:, J:J+bs) -= Qcat W_pend(:, J:J+bs)
+      double* Vi = S.Vw + (long long)kp * maxp;
+      if (pend > 0) {  // make the panel current: A(Jf:p, J:J+bs) -= V_cat U_cat(:, J:J+bs)
         prof_push(st, "id.panel_catchup");
         vief_gemm_desc c{};
-        c.A = S.Qw; c.strideA = sQ; c.lda = maxp;
-        c.B = Rm + (long long)J * ldR + Jf; c.strideB = sR; c.ldb = ldR;
-        c.C = d->A + (long long)J * d->lda; c.strideC = d->sA; c.ldc = d->lda;
-        c.M = maxp; c.N = HB; c.K = kp; c.Mb = S.pact; c.Nb = S.bs;
+        c.A = S.Vw + Jf; c.strideA = sV; c.lda = maxp;
+        c.B = S.Up + (long long)J * ldU; c.strideB = sU; c.ldb = ldU;
+        c.C = d->A + (long long)J * d->lda + Jf; c.strideC = d->sA; c.ldc = d->lda;
+        c.M = maxp - Jf; c.N = HB; c.K = kp; c.Mb = S.pf; c.Nb = S.bs;
         c.alpha = -1.0; c.beta = 1.0; c.batch = count;
         if ((rc = vief_dgemm_batched(&c, st))) return rc;
+        k_zero_rows<<<dim3(cdiv((J - Jf) * HB, 256), count), 256, 0, st>>>(Vi, sV, maxp, Jf, J,
+                                                                        S.active);
+        ++g_launches;
       }
       prof_push(st, "id.panel_qr");
-      if ((rc = qr_panel(d->A, d->sA, d->lda, d->p, S.active, S.bs, J, maxp, count, Qi, sQ, maxp,
-                         S.Rt, st)))
+      if ((rc = qr_panel(d->A, d->sA, d->lda, d->p, S.active, S.bs, J, maxp, count, Vi, sV, maxp,
+                         S.Tt, S.Rt, st)))
         return rc;
       k_store_rblock<<<count, 256, 0, st>>>(S, Rm, sR, ldR, J);
       ++g_launches;
-      {  // W = Q^T A_trail -> R(J:J+bs, J+bs:m); columns start at J+bs per item: use J+HB
-        // items with bs < HB have nrem = 0, so the fixed offset J+HB is exact for all active work
+      const int T0 = J + HB;  // first trailing column (items with bs < HB have nrem = 0)
+      {
         prof_push(st, "id.gemm_W");
-        vief_gemm_desc w{};
-        w.A = Qi; w.strideA = sQ; w.lda = maxp; w.transA = 1;
-        w.B = d->A + (long long)(J + HB) * d->lda; w.strideB = d->sA; w.ldb = d->lda;
-        w.C = Rm + (long long)(J + HB) * ldR + J; w.strideC = sR; w.ldc = ldR;
-        w.M = HB; w.N = maxm; w.K = maxp; w.Mb = S.bs; w.Nb = S.nrem; w.Kb = S.pact;
-        w.alpha = 1.0; w.beta = 0.0; w.batch = count;
-        if ((rc = vief_dgemm_batched(&w, st))) return rc;
-        // W is taken against the stale trailing columns: W_true = W - (Q_i^T Qcat) W_pend,
-        // and Q_i is orthogonal to the pending Q's to O(u ||P_stale|| / ||P_res||) = O(u)
-        // for D <= 4 blocks of the slowly decaying proxy rows, so the correction is
-        // below u ||A|| and is not formed (the bookkeeping A P = Q R + residual stays
-        // exact up to that term).
-        // sketch downdate: Y_trail -= (Omega Q) W  (= Omega A_trail after the update)
+        vief_gemm_desc x{};  // X_i = V_i^T A_stale(J:p, trail)
+        x.A = Vi + J; x.strideA = sV; x.lda = maxp; x.transA = 1;
+        x.B = d->A + (long long)T0 * d->lda + J; x.strideB = d->sA; x.ldb = d->lda;
+        x.C = S.X + (long long)T0 * HB; x.strideC = sX; x.ldc = HB;
+        x.M = HB; x.N = maxm; x.K = maxp - J; x.Mb = S.bs; x.Nb = S.nrem; x.Kb = S.pact;
+        x.alpha = 1.0; x.beta = 0.0; x.batch = count;
+        if ((rc = vief_dgemm_batched(&x, st))) return rc;
+        prof_push(st, "id.wy");
+        if (pend > 0) {
+          vief_gemm_desc g{};  // G = V_i^T V_cat(J:p, :)
+          g.A = Vi + J; g.strideA = sV; g.lda = maxp; g.transA = 1;
+          g.B = S.Vw + J; g.strideB = sV; g.ldb = maxp;
+          g.C = S.G; g.strideC = (long long)HB * HB * D; g.ldc = HB;
+          g.M = HB; g.N = kp; g.K = maxp - J; g.Mb = S.bs; g.Kb = S.pact;
+          g.alpha = 1.0; g.beta = 0.0; g.batch = count;
+          if ((rc = vief_dgemm_batched(&g, st))) return rc;
+          vief_gemm_desc xg{};  // X_i -= G U_cat(:, trail)
+          xg.A = S.G; xg.strideA = (long long)HB * HB * D; xg.lda = HB;
+          xg.B = S.Up + (long long)T0 * ldU; xg.strideB = sU; xg.ldb = ldU;
+          xg.C = S.X + (long long)T0 * HB; xg.strideC = sX; xg.ldc = HB;
+          xg.M = HB; xg.N = maxm; xg.K = kp; xg.Mb = S.bs; xg.Nb = S.nrem;
+          xg.alpha = -1.0; xg.beta = 1.0; xg.batch = count;
+          if ((rc = vief_dgemm_batched(&xg, st))) return rc;
+        }
+        vief_gemm_desc u{};  // U_i = T_i^T X_i  -> rows kp..kp+HB of U_cat
+        u.A = S.Tt; u.strideA = (long long)HB * HB; u.lda = HB; u.transA = 1;
+        u.B = S.X + (long long)T0 * HB; u.strideB = sX; u.ldb = HB;
+        u.C = S.Up + (long long)T0 * ldU + kp; u.strideC = sU; u.ldc = ldU;
+        u.M = HB; u.N = maxm; u.K = HB; u.Nb = S.nrem; u.Kb = S.bs;
+        u.alpha = 1.0; u.beta = 0.0; u.batch = count;
+        if ((rc = vief_dgemm_batched(&u, st))) return rc;
+        // R(J:J+bs, trail) = A_stale(J:J+bs, trail) - V_cat'(J:J+bs, :) U_cat'
+        if ((rc = vief_copy2d(d->A + (long long)T0 * d->lda + J, d->sA, nullptr, d->lda,
+                              Rm + (long long)T0 * ldR + J, sR, nullptr, ldR, S.bs, HB, S.nrem,
+                              maxm, count, st)))
+          return rc;
+        vief_gemm_desc r{};
+        r.A = S.Vw + J; r.strideA = sV; r.lda = maxp;
+        r.B = S.Up + (long long)T0 * ldU; r.strideB = sU; r.ldb = ldU;
+        r.C = Rm + (long long)T0 * ldR + J; r.strideC = sR; r.ldc = ldR;
+        r.M = HB; r.N = maxm; r.K = kp + HB; r.Mb = S.bs; r.Nb = S.nrem;
+        r.alpha = -1.0; r.beta = 1.0; r.batch = count;
+        if ((rc = vief_dgemm_batched(&r, st))) return rc;
+        // sketch: Omega_i = Omega_{i-1} H_i on columns J..p-1, then
+        // Y_trail -= Omega_i(:, J:J+bs) R(J block, trail)
         prof_push(st, "id.sketch_downdate");
-        vief_gemm_desc z{};
-        z.A = Om; z.strideA = 0; z.lda = HS;
-        z.B = Qi; z.strideB = sQ; z.ldb = maxp;
-        z.C = S.Z; z.strideC = (long long)HS * HB; z.ldc = HS;
-        z.M = HS; z.N = HB; z.K = maxp; z.Mb = S.sact; z.Nb = S.bs; z.Kb = S.pact;
-        z.alpha = 1.0; z.beta = 0.0; z.batch = count;
-        if ((rc = vief_dgemm_batched(&z, st))) return rc;
+        vief_gemm_desc o1{};  // OV = Omega(:, J:p) V_i
+        o1.A = S.Om + (long long)J * HS; o1.strideA = sOm; o1.lda = HS;
+        o1.B = Vi + J; o1.strideB = sV; o1.ldb = maxp;
+        o1.C = S.OV; o1.strideC = (long long)HS * HB; o1.ldc = HS;
+        o1.M = HS; o1.N = HB; o1.K = maxp - J; o1.Mb = S.sact; o1.Nb = S.bs; o1.Kb = S.pact;
+        o1.alpha = 1.0; o1.beta = 0.0; o1.batch = count;
+        if ((rc = vief_dgemm_batched(&o1, st))) return rc;
+        vief_gemm_desc o2{};  // OVT = OV T_i
+        o2.A = S.OV; o2.strideA = (long long)HS * HB; o2.lda = HS;
+        o2.B = S.Tt; o2.strideB = (long long)HB * HB; o2.ldb = HB;
+        o2.C = S.OVT; o2.strideC = (long long)HS * HB; o2.ldc = HS;
+        o2.M = HS; o2.N = HB; o2.K = HB; o2.Mb = S.sact; o2.Nb = S.bs; o2.Kb = S.bs;
+        o2.alpha = 1.0; o2.beta = 0.0; o2.batch = count;
+        if ((rc = vief_dgemm_batched(&o2, st))) return rc;
+        vief_gemm_desc o3{};  // Omega(:, J:p) -= OVT V_i^T
+        o3.A = S.OVT; o3.strideA = (long long)HS * HB; o3.lda = HS;
+        o3.B = Vi + J; o3.strideB = sV; o3.ldb = maxp; o3.transB = 1;
+        o3.C = S.Om + (long long)J * HS; o3.strideC = sOm; o3.ldc = HS;
+        o3.M = HS; o3.N = maxp - J; o3.K = HB; o3.Mb = S.sact; o3.Nb = S.pact; o3.Kb = S.bs;
+        o3.alpha = -1.0; o3.beta = 1.0; o3.batch = count;
+        if ((rc = vief_dgemm_batched(&o3, st))) return rc;
         vief_gemm_desc y{};
-        y.A = S.Z; y.strideA = (long long)HS * HB; y.lda = HS;
-        y.B = Rm + (long long)(J + HB) * ldR + J; y.strideB = sR; y.ldb = ldR;
-        y.C = S.Y + (long long)(J + HB) * HS; y.strideC = sY; y.ldc = HS;
+        y.A = S.Om + (long long)J * HS; y.strideA = sOm; y.lda = HS;
+        y.B = Rm + (long long)T0 * ldR + J; y.strideB = sR; y.ldb = ldR;
+        y.C = S.Y + (long long)T0 * HS; y.strideC = sY; y.ldc = HS;
         y.M = HS; y.N = maxm; y.K = HB; y.Mb = S.sact; y.Nb = S.nrem; y.Kb = S.bs;
         y.alpha = -1.0; y.beta = 1.0; y.batch = count;
         if ((rc = vief_dgemm_batched(&y, st))) return rc;
@@ -801,13 +904,13 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       VF_CUDA(cudaMemcpyAsync(&need, S.any, sizeof(int), cudaMemcpyDeviceToHost, st));
       VF_CUDA(cudaStreamSynchronize(st));
       ++pend;
-      if (pend == D || need) {  // flush: A_trail -= Qcat W_pend  (K = 32 pend)
+      if (pend == D || need) {  // flush: A(Jf:p, trail) -= V_cat U_cat(:, trail)  (K = 32 pend)
         prof_push(st, "id.gemm_update");
         vief_gemm_desc u{};
-        u.A = S.Qw; u.strideA = sQ; u.lda = maxp;
-        u.B = Rm + (long long)(J + HB) * ldR + Jf; u.strideB = sR; u.ldb = ldR;
-        u.C = d->A + (long long)(J + HB) * d->lda; u.strideC = d->sA; u.ldc = d->lda;
-        u.M = maxp; u.N = maxm; u.K = pend * HB; u.Mb = S.pact; u.Nb = S.nrem;
+        u.A = S.Vw + Jf; u.strideA = sV; u.lda = maxp;
+        u.B = S.Up + (long long)T0 * ldU; u.strideB = sU; u.ldb = ldU;
+        u.C = d->A + (long long)T0 * d->lda + Jf; u.strideC = d->sA; u.ldc = d->lda;
+        u.M = maxp - Jf; u.N = maxm; u.K = pend * HB; u.Mb = S.pf; u.Nb = S.nrem;
         u.alpha = -1.0; u.beta = 1.0; u.batch = count;
         if ((rc = vief_dgemm_batched(&u, st))) return rc;
         pend = 0;
