@@ -364,7 +364,10 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
   const int cs = cl.num_blocks(), cr = cl.block_rank();
   const int b = blockIdx.x / cs;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (!active[b] || bsv[b] <= 0) return;
+  if (!active[b] || bsv[b] <= 0) {
+    if (cr == 0 && tid == 0) swaps[(long long)b * SWL] = 0;
+    return;
+  }
   const int bs = bsv[b];
   const int n = mv[b] - J;
   extern __shared__ double sm[];
@@ -493,8 +496,10 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
   }
   cl.sync();
   if (cr != 0 || warp != 0) return;
-  // swap list (dst = J+i, src = current position of the chosen column),
-  // tracking moved columns as (id, pos) pairs; lookups are warp ballots
+  // net permutation of the column window: the sequence of transpositions
+  // (J+i <-> current position of the chosen column) is tracked as (id, pos)
+  // pairs of moved columns; lookups are warp ballots.  Output per item:
+  // [nm, id[0..nm), pos[0..nm)] -- column originally at id ends at pos.
   constexpr int NM = 2 * PNB + 2;
   __shared__ int mid[NM], mpos[NM];
   int nm = 0;
@@ -511,7 +516,6 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
       if (bid && !f_id) { src = mpos[32 * h + __ffs(bid) - 1]; f_id = 1; }
       if (bds && !f_dst) { at_dst = mid[32 * h + __ffs(bds) - 1]; f_dst = 1; }
     }
-    if (lane == 0) swaps[b * PNB + i] = src;
     bool f1 = false, f2 = false;
 #pragma unroll
     for (int h = 0; h < 3; ++h) {
@@ -535,6 +539,9 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
     nm += ((!f1 && at_dst != src) ? 1 : 0) + ((!f2 && id != dst) ? 1 : 0);
     __syncwarp();
   }
+  int* out = swaps + (long long)b * SWL;
+  if (lane == 0) out[0] = nm;
+  for (int t = lane; t < nm; t += 32) { out[1 + t] = mid[t]; out[1 + NM + t] = mpos[t]; }
 }
 
 // ---------------------------------------------------------------------------

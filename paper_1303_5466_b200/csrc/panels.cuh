@@ -6,6 +6,7 @@
 namespace vf {
 constexpr int PNB = 32;       // panel width (GJ block, ID block)
 constexpr int HSK = PNB + 8;  // sketch rows
+constexpr int SWL = 1 + 2 * (2 * PNB + 2);  // per-item net column permutation record
 
 int lu_panel(const double* A, long long sA, int lda, int n, int c0, int nbs, int batch, int* ipiv,
              long long sPiv, double* Ainv, long long sAi, double* pivmin, double* pivmax,

@@ -289,7 +289,7 @@ struct HState {
   int* nrem;      // trailing columns after the block
   int* pact;      // p if active else 0
   int* sact;      // HS if active else 0
-  int* swaps;     // count x HB (source positions)
+  int* swaps;     // count x SWL net column permutation records (select kernel)
   double* cut;    // eps * max column norm
   double* tn;     // count x maxm trailing residual norms (travel with their columns)
   double* tn0;    // last exactly computed norm of each column (downdating reference)
@@ -344,68 +344,51 @@ __global__ void k_bcast_omega(const double* Om, long long n, double* Omr, int co
     Omr[b * n + i] = Om[i];
 }
 
-// apply the swap sequence to A (p rows), Y (HS rows), perm, and the norms.
-__global__ void k_apply_swaps(double* A, long long sA, int lda, double* Y, long long sY, int ldy,
-                              int* perm, int ldperm, const int* pv, int J, HState S,
-                              double* Rm, long long sR, int ldR, int kp, int ldU) {
+// apply the block's net column permutation (from the select kernel: column
+// originally at id[t] ends at pos[t]) to A (p rows), R rows < J, the pending
+// U rows, Y, perm and the norms.  Gather form: every source value of a row is
+// read (into shared memory) before any destination is written.
+constexpr int AP_T = 64;
+__global__ void __launch_bounds__(AP_T) k_apply_perm(double* A, long long sA, int lda, double* Y,
+                                                     long long sY, int ldy, int* perm, int ldperm,
+                                                     const int* pv, int J, HState S, double* Rm,
+                                                     long long sR, int ldR, int kp, int ldU) {
   const int b = blockIdx.y;
   if (!S.active[b]) return;
-  const int bs = S.bs[b];
-  const int p = pv[b];
-  const int* sw = S.swaps + b * HB;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < p) {
-    double* a = A + b * sA + r;
-    for (int i = 0; i < bs; ++i) {
-      const int src = sw[i], dst = J + i;
-      if (src != dst) {
-        double t = a[(long long)src * lda]; a[(long long)src * lda] = a[(long long)dst * lda];
-        a[(long long)dst * lda] = t;
-      }
+  constexpr int NM = 2 * PNB + 2;
+  const int* rec = S.swaps + (long long)b * SWL;
+  const int nm = rec[0];
+  if (nm <= 0) return;
+  __shared__ int ids[NM], pos[NM];
+  __shared__ double vals[NM][AP_T];
+  for (int t = threadIdx.x; t < nm; t += AP_T) { ids[t] = rec[1 + t]; pos[t] = rec[1 + NM + t]; }
+  __syncthreads();
+  const int r = blockIdx.x * AP_T + threadIdx.x;
+  auto apply = [&](double* base, long long ld, int nrows) {
+    if (r >= nrows) return;
+    for (int t0 = 0; t0 < nm; t0 += 8) {  // 8 independent loads in flight per thread
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = t0 + u < nm ? base[(long long)ids[t0 + u] * ld + r] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) if (t0 + u < nm) vals[t0 + u][threadIdx.x] = v[u];
     }
-  }
-  if (r < J) {  // rows of R already computed travel with their columns
-    double* rr = Rm + b * sR + r;
-    for (int i = 0; i < bs; ++i) {
-      const int src = sw[i], dst = J + i;
-      if (src != dst) {
-        double t = rr[(long long)src * ldR]; rr[(long long)src * ldR] = rr[(long long)dst * ldR];
-        rr[(long long)dst * ldR] = t;
-      }
-    }
-  }
-  if (r < kp) {  // pending U rows travel with their columns
-    double* u = S.Up + (long long)b * ldU * S.ldtn + r;
-    for (int i = 0; i < bs; ++i) {
-      const int src = sw[i], dst = J + i;
-      if (src != dst) {
-        double t = u[(long long)src * ldU]; u[(long long)src * ldU] = u[(long long)dst * ldU];
-        u[(long long)dst * ldU] = t;
-      }
-    }
-  }
-  if (r < HS) {
-    double* y = Y + b * sY + r;
-    for (int i = 0; i < bs; ++i) {
-      const int src = sw[i], dst = J + i;
-      if (src != dst) {
-        double t = y[(long long)src * ldy]; y[(long long)src * ldy] = y[(long long)dst * ldy];
-        y[(long long)dst * ldy] = t;
-      }
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int t = 0; t < nm; ++t) base[(long long)pos[t] * ld + r] = vals[t][threadIdx.x];
+  };
+  apply(A + b * sA, lda, pv[b]);
+  apply(Rm + b * sR, ldR, J);                        // R rows of earlier blocks
+  apply(S.Up + (long long)b * ldU * S.ldtn, ldU, kp);  // pending U rows
+  apply(Y + b * sY, ldy, HS);
+  if (blockIdx.x == 0) {  // index / norm vectors: thread t moves entry t
+    __shared__ int ip[NM];
+    __shared__ double d0[NM], d1[NM];
     int* pm = perm + b * ldperm;
-    double* t = S.tn + (long long)b * S.ldtn;
-    double* t0 = S.tn0 + (long long)b * S.ldtn;
-    for (int i = 0; i < bs; ++i) {
-      const int src = sw[i], dst = J + i;
-      if (src != dst) {
-        int tp = pm[src]; pm[src] = pm[dst]; pm[dst] = tp;
-        double tv = t[src]; t[src] = t[dst]; t[dst] = tv;
-        tv = t0[src]; t0[src] = t0[dst]; t0[dst] = tv;
-      }
-    }
+    double* tn = S.tn + (long long)b * S.ldtn;
+    double* tn0 = S.tn0 + (long long)b * S.ldtn;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nm; t += AP_T) { ip[t] = pm[ids[t]]; d0[t] = tn[ids[t]]; d1[t] = tn0[ids[t]]; }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nm; t += AP_T) { pm[pos[t]] = ip[t]; tn[pos[t]] = d0[t]; tn0[pos[t]] = d1[t]; }
   }
 }
 
@@ -722,7 +705,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.active = buf.get<int>(count); S.done = buf.get<int>(count); S.k = kdev;
     S.bs = buf.get<int>(count); S.nrem = buf.get<int>(count); S.pact = buf.get<int>(count);
     S.sact = buf.get<int>(count); S.pf = buf.get<int>(count);
-    S.swaps = buf.get<int>((size_t)HB * count);
+    S.swaps = buf.get<int>((size_t)SWL * count);
     S.cut = buf.get<double>(count); S.tn = buf.get<double>((size_t)maxm * count);
     S.tn0 = buf.get<double>((size_t)maxm * count);
     S.flag = buf.get<int>((size_t)maxm * count);
@@ -790,9 +773,9 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       if ((rc = sketch_select(S.Y, HS, sY, d->m, S.active, S.bs, J, maxm, count, S.swaps, st)))
         return rc;
       prof_push(st, "id.swaps");
-      k_apply_swaps<<<dim3(cdiv(std::max(std::max(maxp, HS), std::max(J, kp)), 128), count), 128,
-                      0, st>>>(d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S, Rm,
-                               sR, ldR, kp, ldU);
+      k_apply_perm<<<dim3(cdiv(std::max(std::max(maxp, HS), std::max(J, kp)), AP_T), count), AP_T,
+                     0, st>>>(d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S, Rm, sR,
+                              ldR, kp, ldU);
       g_launches += 2;
       VF_LAUNCH_CHECK("id select/swap");
       double* Vi = S.Vw + (long long)kp * maxp;
