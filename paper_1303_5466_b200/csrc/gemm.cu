@@ -232,8 +232,11 @@ static int launch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
   }
   const long long tiles = (long long)cdiv(d->N, BNT) * cdiv(d->M, BMT) * d->batch;
   int ksplit = 1, kchunk = d->K;
-  if (tiles < 148 && d->K >= 1024) {  // too few tiles to fill the GPU: split K
-    ksplit = (int)std::min<long long>(d->K / 256, std::max<long long>(1, 296 / tiles));
+  // less than one wave of output tiles (148 SMs x 3 resident CTAs) over a long K: split K
+  // so that about two waves run (partials reduced in fixed order)
+  constexpr long long WAVE = 148 * 3;
+  if (tiles < WAVE && d->K >= 1024) {
+    ksplit = (int)std::min<long long>(d->K / 256, (2 * WAVE + tiles - 1) / tiles);
     ksplit = std::min(ksplit, 65535 / d->batch);
     if (ksplit > 1) kchunk = cdiv(cdiv(d->K, ksplit), BK) * BK;
     if (ksplit > 1) ksplit = cdiv(d->K, kchunk);

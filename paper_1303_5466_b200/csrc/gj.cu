@@ -139,6 +139,136 @@ __global__ void k_fill(double* p, long long n, double v) {
   if (i < n) p[i] = v;
 }
 
+// ---------------------------------------------------------------------------
+// Small matrices (n <= 8*TG): the whole Gauss-Jordan inversion in one CTA with
+// the matrix in registers.  Thread (ty, tx) of a TG x TG grid owns the 8 x 8
+// tile rows 8ty.., columns 8tx..; per column j: the owners of column j stage
+// it, warp 0 picks the pivot (first max |.|, NaN selectable, as getrf), the
+// owners of rows p and j stage them, and every thread applies the swap +
+// Gauss-Jordan rank-1 update to its tile (2 barriers per column, double-
+// buffered staging).  The pivots equal getrf's (same elimination below the
+// diagonal), so |pivot| min/max feed the same singularity test.  Column
+// interchanges are undone on the way out (one scatter).
+template <int TG>
+__global__ void __launch_bounds__(TG * TG) k_gj_small(double* A, long long sA, int lda, int n,
+                                                      double* pivmin, double* pivmax) {
+  constexpr int NM = 8 * TG;
+  const int b = blockIdx.x;
+  const int tx = threadIdx.x % TG, ty = threadIdx.x / TG, tid = threadIdx.x;
+  __shared__ double col[2][NM], prow[2][NM], rowj[2][NM];
+  __shared__ int s_p[2];
+  __shared__ double s_r[2];
+  __shared__ int ipv[NM], cur[NM], inv[NM];
+  double* Ab = A + b * sA;
+  double a[8][8];
+  const int i0 = 8 * ty, k0 = 8 * tx;
+#pragma unroll
+  for (int ri = 0; ri < 8; ++ri)
+#pragma unroll
+    for (int ci = 0; ci < 8; ++ci) {
+      const int i = i0 + ri, k = k0 + ci;
+      a[ri][ci] = (i < n && k < n) ? Ab[(long long)k * lda + i] : 0.0;
+    }
+  double pmin = INFINITY, pmax = 0.0;  // tracked by thread 0
+  for (int j = 0; j < n; ++j) {
+    const int bf = j & 1;
+    // 1. stage column j
+    if (tx == (j >> 3)) {
+      const int cj = j & 7;
+#pragma unroll
+      for (int ri = 0; ri < 8; ++ri) {
+        double v = a[ri][0];
+#pragma unroll
+        for (int ci = 1; ci < 8; ++ci) if (ci == cj) v = a[ri][ci];
+        col[bf][i0 + ri] = v;
+      }
+    }
+    __syncthreads();
+    // 2. pivot (warp 0): first maximum of |col[i]|, i in [j, n)
+    if (tid < 32) {
+      double v = -1.0;
+      int iv = 0x7fffffff;
+      for (int i = j + tid; i < n; i += 32) {
+        double t = fabs(col[bf][i]);
+        if (t != t) t = INFINITY;
+        if (t > v) { v = t; iv = i; }
+      }
+      warp_argmax(v, iv);
+      if (iv < j || iv >= n) iv = j;
+      if (tid == 0) {
+        const double pv = col[bf][iv];
+        s_p[bf] = iv;
+        s_r[bf] = 1.0 / pv;
+        ipv[j] = iv;
+        const double ap = fabs(pv);
+        pmin = fmin(pmin, ap);
+        pmax = fmax(pmax, ap);
+      }
+    }
+    // 3. owners of rows p and j stage them (needs p: after the barrier below)
+    __syncthreads();
+    const int p = s_p[bf];
+    const double r = s_r[bf];
+    if (ty == (p >> 3)) {
+      const int rp = p & 7;
+#pragma unroll
+      for (int ci = 0; ci < 8; ++ci) {
+        double v = a[0][ci];
+#pragma unroll
+        for (int ri = 1; ri < 8; ++ri) if (ri == rp) v = a[ri][ci];
+        prow[bf][k0 + ci] = v;
+      }
+    }
+    if (ty == (j >> 3)) {
+      const int rj = j & 7;
+#pragma unroll
+      for (int ci = 0; ci < 8; ++ci) {
+        double v = a[0][ci];
+#pragma unroll
+        for (int ri = 1; ri < 8; ++ri) if (ri == rj) v = a[ri][ci];
+        rowj[bf][k0 + ci] = v;
+      }
+    }
+    __syncthreads();
+    // 4. swap rows j <-> p, then the Gauss-Jordan update of the owned tile
+    double pr[8];
+#pragma unroll
+    for (int ci = 0; ci < 8; ++ci) pr[ci] = prow[bf][k0 + ci] * r;  // scaled pivot row
+#pragma unroll
+    for (int ri = 0; ri < 8; ++ri) {
+      const int i = i0 + ri;
+      if (i == j) {
+#pragma unroll
+        for (int ci = 0; ci < 8; ++ci) a[ri][ci] = (k0 + ci == j) ? r : pr[ci];
+      } else {
+        // column j entry of row i after the swap
+        const double f = (i == p) ? col[bf][j] : col[bf][i];
+#pragma unroll
+        for (int ci = 0; ci < 8; ++ci) {
+          const double old = (i == p) ? rowj[bf][k0 + ci] : a[ri][ci];
+          a[ri][ci] = (k0 + ci == j) ? -f * r : fma(-f, pr[ci], old);
+        }
+      }
+    }
+  }
+  // undo the column interchanges: X(:, pos) = M(:, cur[pos])
+  if (tid == 0) {
+    for (int c = 0; c < n; ++c) cur[c] = c;
+    for (int j = n - 1; j >= 0; --j) { const int t = cur[j]; cur[j] = cur[ipv[j]]; cur[ipv[j]] = t; }
+    for (int c = 0; c < n; ++c) inv[cur[c]] = c;
+    pivmin[b] = pmin;
+    pivmax[b] = pmax;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int ri = 0; ri < 8; ++ri)
+#pragma unroll
+    for (int ci = 0; ci < 8; ++ci) {
+      const int i = i0 + ri, k = k0 + ci;
+      if (i < n && k < n) Ab[(long long)inv[k] * lda + i] = a[ri][ci];
+    }
+}
+
 }  // namespace vf
 
 using namespace vf;
@@ -149,6 +279,14 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
   if (batch > 65535) { set_error("inv_batched: batch too large"); return VF_EARG; }
   cudaStream_t st = (cudaStream_t)stream_;
   ensure_pool();
+  // measured: for n <= 64 (5 CTAs/SM) the register kernel beats the blocked path ~2x;
+  // the 16 x 16-thread variant (1 CTA/SM) loses to it at n = 90..128
+  if (n <= 64) {  // whole inversion in registers, one CTA per matrix
+    k_gj_small<8><<<batch, 64, 0, st>>>(A, sA, lda, n, pivmin, pivmax);
+    ++g_launches;
+    VF_LAUNCH_CHECK("gj small");
+    return VF_OK;
+  }
   const int nb = GJ_NB, NBO = GJ_NBO;
   double *Pw = nullptr, *Rw = nullptr, *Ai = nullptr, *Xw = nullptr, *Ro = nullptr;
   int* ipiv = nullptr;

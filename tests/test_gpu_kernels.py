@@ -69,7 +69,7 @@ def test_dgemv_batched(lib, tA):
     assert torch.equal(y, y2)
 
 
-@pytest.mark.parametrize("n", [1, 5, 64, 100, 257])
+@pytest.mark.parametrize("n", [1, 5, 64, 65, 100, 128, 129, 257])
 def test_inverse_batched(lib, n):
     nb = 4
     A = torch.randn(nb, n, n, dtype=torch.float64, device="cuda") + 3 * torch.eye(n, device="cuda", dtype=torch.float64)
