@@ -357,6 +357,7 @@ struct XSel {
   double y[HSK];
 };
 
+template <bool WIDE>  // WIDE: more than PT columns per CTA (two per thread per pass)
 __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, long long sY,
                                                   const int* mv, const int* active, const int* bsv,
                                                   int J, int cols_per, int* swaps) {
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
   const int n = mv[b] - J;
   extern __shared__ double sm[];
   __shared__ XSel xch[2];
-  __shared__ double Qb[PNB][HSK];
+  __shared__ double Qb[PNB][HSK + 1];  // odd row stride: lane-per-row dot products are conflict free
   __shared__ double yv[HSK], dv[PNB];
   __shared__ double redv[NW];
   __shared__ int redi[NW];
@@ -477,21 +478,55 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
     // downdate every live column's residual norm and pick the next candidate
     bv = -1.0;
     bi = 0x7fffffff;
-    const double* q = Qb[i];
-    for (int c = tid; c < nc; c += PT) {
-      const double cur = nrm[c];
-      if (cur < 0.0) continue;
-      const double* yc = Ys + c * LDY;
-      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    if constexpr (WIDE) {
+      double qv[HSK];
 #pragma unroll
-      for (int r = 0; r < HSK; r += 4) {
-        d0 = fma(q[r], yc[r], d0); d1 = fma(q[r + 1], yc[r + 1], d1);
-        d2 = fma(q[r + 2], yc[r + 2], d2); d3 = fma(q[r + 3], yc[r + 3], d3);
+      for (int r = 0; r < HSK; ++r) qv[r] = Qb[i][r];
+      // two columns per pass (c, c + PT): 8 independent FMA chains
+      for (int c = tid; c < nc; c += 2 * PT) {
+        const int c2 = c + PT;
+        const bool h2 = c2 < nc;
+        const double cur1 = nrm[c], cur2 = h2 ? nrm[c2] : -1.0;
+        const double* y1 = Ys + c * LDY;
+        const double* y2 = Ys + (h2 ? c2 : c) * LDY;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < HSK; r += 4) {
+          a0 = fma(qv[r], y1[r], a0); a1 = fma(qv[r + 1], y1[r + 1], a1);
+          a2 = fma(qv[r + 2], y1[r + 2], a2); a3 = fma(qv[r + 3], y1[r + 3], a3);
+          e0 = fma(qv[r], y2[r], e0); e1 = fma(qv[r + 1], y2[r + 1], e1);
+          e2 = fma(qv[r + 2], y2[r + 2], e2); e3 = fma(qv[r + 3], y2[r + 3], e3);
+        }
+        if (cur1 >= 0.0) {
+          const double d = (a0 + a1) + (a2 + a3);
+          const double nv = fmax(cur1 - d * d, 0.0);
+          nrm[c] = nv;
+          if (nv > bv) { bv = nv; bi = c0 + c; }
+        }
+        if (cur2 >= 0.0) {
+          const double d = (e0 + e1) + (e2 + e3);
+          const double nv = fmax(cur2 - d * d, 0.0);
+          nrm[c2] = nv;
+          if (nv > bv) { bv = nv; bi = c0 + c2; }
+        }
       }
-      const double d = (d0 + d1) + (d2 + d3);
-      const double nv = fmax(cur - d * d, 0.0);
-      nrm[c] = nv;
-      if (nv > bv) { bv = nv; bi = c0 + c; }
+    } else {
+      const double* q = Qb[i];
+      for (int c = tid; c < nc; c += PT) {
+        const double cur = nrm[c];
+        if (cur < 0.0) continue;
+        const double* yc = Ys + c * LDY;
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < HSK; r += 4) {
+          d0 = fma(q[r], yc[r], d0); d1 = fma(q[r + 1], yc[r + 1], d1);
+          d2 = fma(q[r + 2], yc[r + 2], d2); d3 = fma(q[r + 3], yc[r + 3], d3);
+        }
+        const double d = (d0 + d1) + (d2 + d3);
+        const double nv = fmax(cur - d * d, 0.0);
+        nrm[c] = nv;
+        if (nv > bv) { bv = nv; bi = c0 + c; }
+      }
     }
   }
   cl.sync();
@@ -1087,7 +1122,8 @@ int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const i
   size_t smem = ((size_t)(HSK + 1) * cols_per + (size_t)cols_per) * sizeof(double);
   void* args[] = {(void*)&Y, (void*)&ldy, (void*)&sY, (void*)&mv, (void*)&active, (void*)&bsv,
                   (void*)&J, (void*)&cols_per, (void*)&swaps};
-  return launch_cluster((const void*)k_select_cl, count, cs, smem, st, args);
+  const void* fn = cols_per > PT ? (const void*)k_select_cl<true> : (const void*)k_select_cl<false>;
+  return launch_cluster(fn, count, cs, smem, st, args);
 }
 
 }  // namespace vf
