@@ -554,30 +554,43 @@ __global__ void k_t_init(const double* Rm, long long sR, int ldR, const int* kv,
   }
 }
 
-// inverse of the upper-triangular TB x TB diagonal blocks of Rs
+// inverse of the upper-triangular TB x TB diagonal blocks of Rs.  Thread j
+// owns column j of the inverse, kept (transposed) in the unused strict lower
+// triangle of the shared U tile -- no local-memory arrays:
+// X(i, j) = -(sum_{q=i+1..j} U(i,q) X(q,j)) / U(i,i), four partial sums.
 __global__ void __launch_bounds__(TB) k_diag_inv(const double* Rs, long long sRs, int Kmax,
                                                  double* Dinv, long long sD) {
   const int b = blockIdx.y, blk = blockIdx.x, tid = threadIdx.x;
   const int r0 = blk * TB;
   const int n = min(TB, Kmax - r0);
-  __shared__ double U[TB][TB + 1];
+  __shared__ double U[TB][TB + 1];  // upper: U;  strict lower (j, i): X(i, j)
+  __shared__ double rinv[TB];
   const double* R = Rs + b * sRs;
-  for (int j = 0; j < n; ++j) U[tid][j] = tid < n ? R[(long long)(r0 + j) * Kmax + r0 + tid] : 0.0;
+  for (int j = 0; j < TB; ++j)
+    U[tid][j] = (tid < n && j < n && tid <= j) ? R[(long long)(r0 + j) * Kmax + r0 + tid] : 0.0;
+  __syncthreads();
+  rinv[tid] = tid < n ? 1.0 / U[tid][tid] : 0.0;
+  __syncthreads();
+  const int j = tid;
+  if (j < n) {
+    // X(q, j) for q > i lives at U[j][q] (q < j) and X(j, j) = rinv[j]
+    for (int i = j - 1; i >= 0; --i) {
+      double s0 = U[i][j] * rinv[j], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int q = i + 1;
+      for (; q + 3 < j; q += 4) {
+        s0 = fma(U[i][q], U[j][q], s0); s1 = fma(U[i][q + 1], U[j][q + 1], s1);
+        s2 = fma(U[i][q + 2], U[j][q + 2], s2); s3 = fma(U[i][q + 3], U[j][q + 3], s3);
+      }
+      for (; q < j; ++q) s0 = fma(U[i][q], U[j][q], s0);
+      U[j][i] = -((s0 + s1) + (s2 + s3)) * rinv[i];
+    }
+  }
   __syncthreads();
   double* D = Dinv + b * sD + (long long)blk * TB * TB;
-  if (tid < TB) {
-    const int j = tid;
-    double col[TB];
-    for (int i = 0; i < TB; ++i) col[i] = 0.0;
-    if (j < n) {
-      col[j] = 1.0 / U[j][j];
-      for (int i = j - 1; i >= 0; --i) {
-        double s = 0.0;
-        for (int q = i + 1; q <= j; ++q) s = fma(U[i][q], col[q], s);
-        col[i] = -s / U[i][i];
-      }
-    }
-    for (int i = 0; i < TB; ++i) D[(long long)j * TB + i] = col[i];
+  // D(i, c) = X(i, c): i < c -> U[c][i]; i == c -> rinv; i > c -> 0
+  for (int c = 0; c < TB; ++c) {
+    const int i = tid;
+    D[(long long)c * TB + i] = i < c ? U[c][i] : (i == c ? rinv[i] : 0.0);
   }
 }
 
@@ -613,8 +626,10 @@ static int t_solve(const vief_id_desc* d, double* Rm, long long sR, int ldR, con
   int* nT = buf.get<int>(count);
   if (!Rs || !Dinv || !tmp || !nT) { set_error("id: out of device memory (T solve)"); return VF_ENOMEM; }
   {
+    prof_push(st, "id.tsolve.init");
     dim3 g(cdiv(Kmax, 32), std::min<unsigned>(cdiv(std::max(d->maxm, Kmax), 8), 4096u), count);
     k_t_init<<<g, dim3(32, 8), 0, st>>>(Rm, sR, ldR, kdev, d->m, Kmax, d->T, d->sT, d->ldT, Rs, sRs);
+    prof_push(st, "id.tsolve.diag");
     k_diag_inv<<<dim3(nblk, count), TB, 0, st>>>(Rs, sRs, Kmax, Dinv, (long long)nblk * TB * TB);
     g_launches += 2;
     VF_LAUNCH_CHECK("t_init/diag_inv");
@@ -622,6 +637,7 @@ static int t_solve(const vief_id_desc* d, double* Rm, long long sR, int ldR, con
   // per-item column count m - k
   {
     // nT = m - k computed on host-visible path: small kernel via gather trick
+    prof_push(st, "id.tsolve.sync");
     std::vector<int> hm(count), hk(count);
     VF_CUDA(cudaMemcpyAsync(hm.data(), d->m, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
     VF_CUDA(cudaMemcpyAsync(hk.data(), kdev, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
@@ -631,6 +647,7 @@ static int t_solve(const vief_id_desc* d, double* Rm, long long sR, int ldR, con
     VF_CUDA(cudaMemcpyAsync(nT, hm.data(), sizeof(int) * count, cudaMemcpyHostToDevice, st));
     VF_CUDA(cudaStreamSynchronize(st));
     if (nmax == 0) return VF_OK;
+    prof_push(st, "id.tsolve.rec");
     // recursive back substitution over block rows [r0, r1): solve the lower
     // half first, one large GEMM update of the upper half, then recurse on it
     struct Rec {
