@@ -12,7 +12,7 @@ import numpy as np
 from .config import SolverOptions
 from .errors import ConfigError
 from .kernels import PLAIN
-from .solver_dense import compress_outer, invert_dense_block
+from .solver_dense import compress_outer, factorize, invert_dense_block
 from .tree import build_tree
 
 
@@ -42,8 +42,8 @@ def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti
     if tree is None:
         tree = build_tree(grid, opts.leaf_size)
     inv = CompressedInverse(spec, grid, tree, eps, opts, quad, ti_mode)
-    H = compress_outer(spec, grid, tree, eps, opts, quad)
-    inv.dense_delegate = invert_dense_block(H)
+    # compress_outer + invert_dense_block, levels pipelined over two streams
+    H, inv.dense_delegate = factorize(spec, grid, tree, eps, opts, quad)
     inv.dense_matvec_source = H
     return inv
 

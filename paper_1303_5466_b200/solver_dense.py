@@ -72,14 +72,24 @@ def _even(x):
     return int(x) + (int(x) & 1)
 
 
+def _h2d(a, device):
+    """Host array -> device tensor through pinned memory, asynchronously on the
+    current stream (a pageable copy would block the host until the stream
+    drains, serialising the two streams of `factorize`)."""
+    t = torch.from_numpy(a)
+    if torch.device(device).type != "cuda":
+        return t.to(device)
+    return t.pin_memory().to(device, non_blocking=True)
+
+
 def _dev_i32(a, device):
-    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=device)
+    return _h2d(np.ascontiguousarray(a, dtype=np.int32), device)
 
 
 def _ptrs(base, offsets_elems, device):
     """Device int64 array of base.data_ptr() + 8*offset (pointer arrays)."""
     off = np.asarray(offsets_elems, dtype=np.int64) * base.element_size() + base.data_ptr()
-    return torch.as_tensor(off, device=device)
+    return _h2d(np.ascontiguousarray(off), device)
 
 
 class _Level:
@@ -454,7 +464,9 @@ def _check_singular(H, L, pmin, pmax, what):
         raise SingularFactorError(where, float(lo[j]))
 
 
-def _invert_level(inv, L):
+def _invert_level(inv, L, checks=None):
+    """`checks`: if a list, singularity tests are queued there instead of being
+    run now (running them reads device data and would block the host)."""
     H = inv.H
     dev = H.device
     nb, mm = L.nb, L.mmax
@@ -478,7 +490,10 @@ def _invert_level(inv, L):
                     dstp=_ptrs(F, base + k1, dev))
     _lib.pad_identity(F, mm * mm, mm, L.m_d, mm, nb)
     pmin, pmax = _lib.inv_batched(F, mm * mm, mm, mm, nb)
-    _check_singular(H, L, pmin, pmax, "F")
+    if checks is None:
+        _check_singular(H, L, pmin, pmax, "F")
+    else:
+        checks.append((L, pmin, pmax, "F"))
     L.Finv = F
     if L.lv == 0:
         return
@@ -507,7 +522,10 @@ def _invert_level(inv, L):
     del Wp
     _lib.pad_identity(G, kk * kk, kk, L.k_d, kk, nb)
     pmin, pmax = _lib.inv_batched(G, kk * kk, kk, kk, nb)
-    _check_singular(H, L, pmin, pmax, "E")
+    if checks is None:
+        _check_singular(H, L, pmin, pmax, "E")
+    else:
+        checks.append((L, pmin, pmax, "E"))
     L.E = G
     L.W = W
     _lib.prof_mark("py.C")
@@ -587,6 +605,41 @@ def invert_dense_block(H, spill=None, free_source=False):
             else:
                 L.B12 = L.B21 = None
     return inv
+
+
+_SIDE = {}
+
+
+def factorize(spec, grid, tree, eps, opts, quad=PLAIN):
+    """compress_outer + invert_dense_block with the levels pipelined over two
+    CUDA streams: level l is inverted (side stream) while level l-1 is being
+    compressed (current stream).  Inverting level l needs only level l's
+    compression and level l+1's inversion, so this is the same computation in
+    a different order; the latency-bound panels of one stage overlap the
+    GEMMs of the other.  Singularity checks run at the end (same exception)."""
+    H = Hss2dMatrix(spec, grid, tree, eps, opts, quad)
+    pad = H.opts.resolved_proxy_layers(H.spec)
+    inv = DenseBlockInverse(H)
+    main = torch.cuda.current_stream(H.device)
+    side = _SIDE.get(H.device)
+    if side is None:
+        side = _SIDE[H.device] = torch.cuda.Stream(H.device)
+    checks = []
+    _mark("compress:start")
+    for L in reversed(_real_levels(H)):
+        _lib.prof_prefix(f"L{L.lv:02d}.")
+        _compress_level(H, L, pad, H.opts.seed)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        with torch.cuda.stream(side):
+            side.wait_event(ev)
+            _lib.prof_prefix(f"I{L.lv:02d}.")
+            _invert_level(inv, L, checks)
+        _mark(f"compress:{L.lv}")
+    main.wait_stream(side)
+    for L, pmin, pmax, what in checks:
+        _check_singular(H, L, pmin, pmax, what)
+    return H, inv
 
 
 # ---------------------------------------------------------------------------
