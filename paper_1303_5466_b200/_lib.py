@@ -11,7 +11,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libvief_b200.so")
+LIB_PATH = os.environ.get("VF_LIB") or os.path.join(_HERE, "_lib", "libvief_b200.so")  # VF_LIB: A/B builds
 
 VF_OK, VF_ECUDA, VF_EARG, VF_ESINGULAR, VF_ENOMEM = range(5)
 

@@ -18,7 +18,13 @@
 namespace vf {
 extern long long g_launches;
 
-constexpr int BK = 16, STAGES = 3, PAD = 4;
+#ifndef VF_GEMM_BK
+#define VF_GEMM_BK 8
+#endif
+#ifndef VF_GEMM_STAGES
+#define VF_GEMM_STAGES 4
+#endif
+constexpr int BK = VF_GEMM_BK, STAGES = VF_GEMM_STAGES, PAD = 4;
 
 struct GemmItem {
   const double* A; const double* B; double* C; int M, N, K;
