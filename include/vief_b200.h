@@ -37,6 +37,8 @@ int vief_version(void);
 const char* vief_last_error(void);
 /* number of kernel launches issued by this library since load (bench evidence) */
 long long vief_launch_count(void);
+/* Return cached workspace memory (the stream-ordered pool) to the driver; synchronises. */
+int vief_release_pool(void);
 /* phase profiler: CUDA-event totals per orchestration phase (synchronising; off by default) */
 void vief_prof_enable(int on);
 void vief_prof_prefix(const char* prefix);  /* tag subsequent phases (e.g. level) */

@@ -48,6 +48,7 @@ _SIGS = {
     "vief_version": [],
     "vief_last_error": [],
     "vief_launch_count": [],
+    "vief_release_pool": [],
     "vief_prof_enable": [c_int],
     "vief_prof_prefix": [ctypes.c_char_p],
     "vief_prof_mark": [ctypes.c_char_p, c_vp],
@@ -137,6 +138,14 @@ def prof_report():
     buf = ctypes.create_string_buffer(1 << 16)
     load().vief_prof_report(buf, len(buf))
     return buf.value.decode()
+
+
+def release_memory():
+    """Free cached device memory of both allocators (torch's and the library's
+    stream-ordered pool)."""
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    call("vief_release_pool")
 
 
 def launch_count():

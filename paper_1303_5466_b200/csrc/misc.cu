@@ -277,6 +277,19 @@ void ensure_pool() {
 }
 }  // namespace vf
 
+// Return the cached (stream-ordered) workspace memory of the default pool to
+// the driver, e.g. before a phase whose allocations go through another
+// allocator (torch).  Synchronises the device.
+extern "C" int vief_release_pool(void) {
+  int dev = 0;
+  VF_CUDA(cudaGetDevice(&dev));
+  VF_CUDA(cudaDeviceSynchronize());
+  cudaMemPool_t pool;
+  VF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  VF_CUDA(cudaMemPoolTrimTo(pool, 0));
+  return VF_OK;
+}
+
 // phases marked from the host orchestration (Python): closes the open phase
 extern "C" void vief_prof_mark(const char* name, void* stream) {
   vf::prof_push((cudaStream_t)stream, name);
