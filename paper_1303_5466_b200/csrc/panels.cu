@@ -814,13 +814,14 @@ struct XQr2 {
   double rowj[PNB];
 };
 
-template <int RPT>
-__global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long long sA, int lda,
+template <int RPT, int NT = PT>
+__global__ void __launch_bounds__(NT, 1) k_qr_panel_rr(const double* A, long long sA, int lda,
                                                        const int* pv, const int* active,
                                                        const int* bsv, int J, double* Vw,
                                                        long long sV, int ldv, double* Tt,
                                                        double* Rt) {
-  constexpr int RP = PT * RPT;
+  constexpr int RP = NT * RPT;
+  constexpr int NWt = NT / 32;
   cg::cluster_group cl = cg::this_cluster();
   const int cs = cl.num_blocks(), cr = cl.block_rank();
   const int b = blockIdx.x / cs;
@@ -829,13 +830,13 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
   const int bs = bsv[b];
   const int p = pv[b] - J;  // panel rows J..p-1 (Householder form: rows < J are finished)
   __shared__ XQr2 xch[2];
-  __shared__ double red[NW][PNB];
-  __shared__ double Sp[2 * NW][PNB];
+  __shared__ double red[NWt][PNB];
+  __shared__ double Sp[16][PNB];
   __shared__ double w[PNB], tau[PNB];
   __shared__ double s_sc;
   __shared__ double Rl[PNB][PNB + 1], Gm[PNB][PNB + 1], Tm[PNB][PNB + 1], V1[PNB][PNB + 1];
   const int r0 = cr * RP;
-  for (int idx = tid; idx < PNB * PNB; idx += PT) {
+  for (int idx = tid; idx < PNB * PNB; idx += NT) {
     const int i = idx % PNB, c = idx / PNB;
     Rl[i][c] = 0.0; Gm[i][c] = 0.0; V1[i][c] = 0.0; Tm[i][c] = 0.0;
   }
@@ -844,7 +845,7 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
   double a[RPT][PNB];
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
-    const int g = r0 + tid + q * PT;
+    const int g = r0 + tid + q * NT;
 #pragma unroll
     for (int l = 0; l < PNB; ++l) a[q][l] = (g < p && l < bs) ? Ab[(long long)l * lda + g] : 0.0;
   }
@@ -863,7 +864,7 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
       for (int t = 0; t < 16; ++t) v[t] = 0.0;
 #pragma unroll
       for (int q = 0; q < RPT; ++q) {
-        const int g = r0 + tid + q * PT;
+        const int g = r0 + tid + q * NT;
         if (g > j && g < p) {
           const double xr = a[q][u];
 #pragma unroll
@@ -881,14 +882,12 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
     if (warp == 0) {
       double s = 0.0;
 #pragma unroll
-      for (int ww = 0; ww < NW; ++ww) s += red[ww][lane];
+      for (int ww = 0; ww < NWt; ++ww) s += red[ww][lane];
       x.S[lane] = s;
     }
     cl.sync();
-    // warp w fetches ranks 2w, 2w+1 (all remote loads in flight together)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      if (2 * warp + h < cs) Sp[2 * warp + h][lane] = remote(cl, &x, 2 * warp + h)->S[lane];
+    // warp w fetches ranks w, w + NWt, ... (all remote loads in flight together)
+    for (int q = warp; q < cs; q += NWt) Sp[q][lane] = remote(cl, &x, q)->S[lane];
     __syncthreads();
     if (warp == 0) {  // lane t: slot t summed over ranks in fixed order
       const int t = lane;
@@ -927,7 +926,7 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
     const double sc = s_sc;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-      const int g = r0 + tid + q * PT;
+      const int g = r0 + tid + q * NT;
       if (g > j && g < p) {
         const double xv = a[q][u] * sc;
         a[q][u] = xv;
@@ -975,7 +974,7 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
   double* Vo = Vw + b * sV + J;
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
-    const int g = r0 + tid + q * PT;
+    const int g = r0 + tid + q * NT;
     if (g < p)
 #pragma unroll
       for (int t = 0; t < PNB; ++t) {
@@ -985,14 +984,14 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
   }
   if (cr == 0) {
     double* To = Tt + (long long)b * PNB * PNB;
-    for (int idx = tid; idx < PNB * PNB; idx += PT) {
+    for (int idx = tid; idx < PNB * PNB; idx += NT) {
       const int i = idx % PNB, c = idx / PNB;
       To[c * PNB + i] = Tm[i][c];
     }
   }
   if (cr == 0) {
     double* Rr = Rt + (long long)b * PNB * PNB;
-    for (int idx = tid; idx < PNB * PNB; idx += PT) {
+    for (int idx = tid; idx < PNB * PNB; idx += NT) {
       int i = idx % PNB, c = idx / PNB;
       Rr[c * PNB + i] = Rl[i][c];
     }
@@ -1004,10 +1003,10 @@ __global__ void __launch_bounds__(PT, 1) k_qr_panel_rr(const double* A, long lon
 // launch helpers
 
 static int launch_cluster(const void* fn, int count, int cs, size_t smem, cudaStream_t st,
-                          void** args) {
+                          void** args, int threads = PT) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * cs);
-  cfg.blockDim = dim3(PT);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1093,6 +1092,15 @@ int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* a
              const int* bsv, int J, int maxp, int count, double* Vw, long long sV, int ldv,
              double* Tt, double* Rt, cudaStream_t st) {
   const int rows = maxp - J;  // panel rows J..p-1
+  if (rows <= 2 * 128 && panel_mode() != 1) {  // short panels: small CTAs, several per SM
+    void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
+                    (void*)&J, (void*)&Vw, (void*)&sV, (void*)&ldv, (void*)&Tt, (void*)&Rt};
+    const int nt = rows <= 128 ? 64 : 128;
+    const void* fn = rows <= 64 ? (const void*)k_qr_panel_rr<1, 64>
+                   : rows <= 128 ? (const void*)k_qr_panel_rr<2, 64>
+                                 : (const void*)k_qr_panel_rr<2, 128>;
+    return launch_cluster(fn, count, 1, 0, st, args, nt);
+  }
   if (rows <= 16 * 3 * PT && panel_mode() != 1) {
     const int rpt = rows <= PT ? 1 : (rows <= 16 * 2 * PT ? 2 : 3);
     const int cs = (rows + rpt * PT - 1) / (rpt * PT);
