@@ -664,25 +664,63 @@ def factorize(spec, grid, tree, eps, opts, quad=PLAIN):
 
 
 def _factorize_levels(H, inv, pad, main, side):
+    """Compression on this thread (main stream); the inversion work is
+    enqueued on the side stream by a worker thread.  Enqueueing a large
+    Gauss-Jordan inversion blocks the host for as long as the GPU runs it (the
+    launch queue fills), and the ID loop synchronises with the host once per
+    block, so a single host thread would serialise the two streams."""
+    import queue
+    import threading
     checks = inv._checks = []
-    _mark("compress:start")
-    for L in reversed(_real_levels(H)):
-        _lib.prof_prefix(f"L{L.lv:02d}.")
-        # F of this level needs only its D/B blocks and the children's E: its
-        # inversion overlaps this level's IDs
-        _compress_level_blocks(H, L)
-        ev = torch.cuda.Event()
-        ev.record(main)
-        with torch.cuda.stream(side):
-            side.wait_event(ev)
-            _invert_level_F(inv, L, checks)
-        _compress_level_id(H, L, pad, H.opts.seed)
-        ev = torch.cuda.Event()
-        ev.record(main)
-        with torch.cuda.stream(side):
-            side.wait_event(ev)
-            _invert_level_rest(inv, L, checks)
-        _mark(f"compress:{L.lv}")
+    tasks = queue.Queue()
+    errors = []
+
+    dev_index = torch.cuda.current_device() if H.device.index is None else H.device.index
+    done = []
+
+    def worker():
+        try:
+            torch.cuda.set_device(dev_index)
+            with torch.cuda.stream(side):
+                while True:
+                    item = tasks.get()
+                    if item is None:
+                        return
+                    fn, L, ev = item
+                    if errors:
+                        continue
+                    side.wait_event(ev)
+                    fn(inv, L, checks)
+                    done.append(L.lv)
+        except BaseException as e:  # re-raised on the caller's thread
+            errors.append(e)
+
+    th = threading.Thread(target=worker, name="vief-invert", daemon=True)
+    th.start()
+    try:
+        _mark("compress:start")
+        for L in reversed(_real_levels(H)):
+            _lib.prof_prefix(f"L{L.lv:02d}.")
+            # F of this level needs only its D/B blocks and the children's E:
+            # its inversion overlaps this level's IDs
+            _compress_level_blocks(H, L)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            tasks.put((_invert_level_F, L, ev))
+            _compress_level_id(H, L, pad, H.opts.seed)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            tasks.put((_invert_level_rest, L, ev))
+            _mark(f"compress:{L.lv}")
+            if errors:
+                break
+    finally:
+        tasks.put(None)
+        th.join()
+    if errors:
+        raise errors[0]
+    if len(done) != 2 * len(_real_levels(H)):
+        raise RuntimeError("factorize: inversion worker did not complete")
 
 
 # ---------------------------------------------------------------------------
