@@ -49,6 +49,9 @@ class BoxNode:
         return f"Box({self.idx}, lvl={self.level}, [{self.x0},{self.x1})x[{self.y0},{self.y1}))"
 
 
+_OWNED_CACHE = {}
+
+
 class BoxTree:
     """Nodes in breadth-first order plus per-level arrays.
 
@@ -58,15 +61,38 @@ class BoxTree:
     def __init__(self, grid, n_max):
         self.grid = grid
         self.n_max = n_max
-        self.nodes = []
-        self.levels = []
+        self._nodes = None
+        self._levels = None
         self.rects = []
         self.ids = []
+        self.parents = []
         self.layers = 0
+
+    # The node objects and id lists mirror the reference's API; the solver only
+    # reads the per-level arrays, so they are materialised on first use.
+    @property
+    def nodes(self):
+        if self._nodes is None:
+            nodes = []
+            for lv, (r, ids_l, par) in enumerate(zip(self.rects, self.ids, self.parents)):
+                for i, row, p in zip(ids_l.tolist(), r.tolist(), par.tolist()):
+                    nodes.append(BoxNode(i, lv, p, row[0], row[1], row[2], row[3]))
+            for lv in range(1, len(self.ids)):
+                kid = self.ids[lv].tolist()
+                for j, pid in enumerate(self.ids[lv - 1].tolist()):
+                    nodes[pid].children = (kid[2 * j], kid[2 * j + 1])
+            self._nodes = nodes
+        return self._nodes
+
+    @property
+    def levels(self):
+        if self._levels is None:
+            self._levels = [ids_l.tolist() for ids_l in self.ids]
+        return self._levels
 
     @property
     def depth(self):
-        return len(self.levels) - 1
+        return len(self.ids) - 1
 
     @property
     def root(self):
@@ -90,6 +116,19 @@ class BoxTree:
         return (np.arange(box.y0, box.y1)[:, None] * n + np.arange(box.x0, box.x1)[None, :]).ravel()
 
     def owned_level(self, lv):
+        """(n_l, w*h) int64 owned indices of every box of level `lv`; memoised
+        per (grid side, leaf size, level) -- trees are deterministic."""
+        key = (self.grid.n_side, self.n_max, lv)
+        out = _OWNED_CACHE.get(key)
+        if out is None:
+            out = self._owned_level(lv)
+            out.setflags(write=False)
+            if len(_OWNED_CACHE) > 64:
+                _OWNED_CACHE.clear()
+            _OWNED_CACHE[key] = out
+        return out
+
+    def _owned_level(self, lv):
         """(n_l, w*h) int64 owned indices of every box of level `lv` (all boxes
         of the leaf level share one shape for the trees build_tree accepts,
         otherwise rows are padded with -1)."""
@@ -140,14 +179,7 @@ def build_tree(grid, n_max):
         idss.append(ids)
     tree.rects = rects
     tree.ids = idss
-    for lv, (r, ids_l, par) in enumerate(zip(rects, idss, parents)):
-        tree.levels.append([int(i) for i in ids_l])
-        for i, row, p in zip(ids_l, r, par):
-            tree.nodes.append(BoxNode(int(i), lv, int(p), int(row[0]), int(row[1]),
-                                      int(row[2]), int(row[3])))
-    for lv in range(1, len(idss)):
-        for j, pid in enumerate(idss[lv - 1]):
-            tree.nodes[pid].children = (int(idss[lv][2 * j]), int(idss[lv][2 * j + 1]))
+    tree.parents = parents
     return tree
 
 
@@ -187,6 +219,17 @@ def proxy_count(w, h, layers):
     for j in range(1, layers + 1):
         W, H = w + 2 * j, h + 2 * j
         tot += H if W == 1 else W if H == 1 else 2 * (W - 1) + 2 * (H - 1)
+    return tot
+
+
+def proxy_count_v(w, h, layers):
+    """Vectorised proxy_count over arrays of box widths/heights."""
+    w = np.asarray(w, dtype=np.int64)
+    h = np.asarray(h, dtype=np.int64)
+    tot = np.zeros(w.shape, dtype=np.int64)
+    for j in range(1, layers + 1):
+        W, H = w + 2 * j, h + 2 * j
+        tot += np.where(W == 1, H, np.where(H == 1, W, 2 * (W - 1) + 2 * (H - 1)))
     return tot
 
 
