@@ -202,16 +202,43 @@ class Hss2dMatrix:
             self.levels.append(L)
         self.sharded = level_slices is not None
         self._lvl_of_cache = None
-        nonroot = lambda: [i for i in self._lvl_of if i != 0]
-        nonleaf = lambda: [i for i in self._lvl_of if not self.levels[self._lvl_of[i][0].lv].leaf]
-        leaves = lambda: [i for i in self._lvl_of if self._lvl_of[i][0].leaf]
-        self.row_skel = _BoxView(self, lambda i: self._skel(i, "rskel"), nonroot)
-        self.col_skel = _BoxView(self, lambda i: self._skel(i, "cskel"), nonroot)
-        self.Lfac = _BoxView(self, lambda i: self._interp(i, "row"), nonroot)
-        self.Rfac = _BoxView(self, lambda i: self._interp(i, "col"), nonroot)
-        self.D = _BoxView(self, self._dblock, leaves)
-        self.B = _BoxView(self, self._bblock, nonleaf)
         self._interp_cache = {}
+
+    # dict-like host views (created on access: a stored view would close a
+    # reference cycle through its getter and keep the HBM buffers alive until
+    # the cyclic GC runs)
+    def _nonroot(self):
+        return [i for i in self._lvl_of if i != 0]
+
+    def _nonleaf(self):
+        return [i for i in self._lvl_of if not self._lvl_of[i][0].leaf]
+
+    def _leaves(self):
+        return [i for i in self._lvl_of if self._lvl_of[i][0].leaf]
+
+    @property
+    def row_skel(self):
+        return _BoxView(self, lambda i: self._skel(i, "rskel"), self._nonroot)
+
+    @property
+    def col_skel(self):
+        return _BoxView(self, lambda i: self._skel(i, "cskel"), self._nonroot)
+
+    @property
+    def Lfac(self):
+        return _BoxView(self, lambda i: self._interp(i, "row"), self._nonroot)
+
+    @property
+    def Rfac(self):
+        return _BoxView(self, lambda i: self._interp(i, "col"), self._nonroot)
+
+    @property
+    def D(self):
+        return _BoxView(self, self._dblock, self._leaves)
+
+    @property
+    def B(self):
+        return _BoxView(self, self._bblock, self._nonleaf)
 
     @property
     def _lvl_of(self):
@@ -637,10 +664,17 @@ class DenseBlockInverse:
     def __init__(self, H):
         self.H = H
         self.tree = H.tree
-        levels = _real_levels(H)
-        ids = lambda pred: [int(i) for L in levels if pred(L) for i in L.ids]
-        self.E = _BoxView(self, lambda i: self._get(i, "E"), lambda: ids(lambda L: L.lv > 0))
-        self.Finv = _BoxView(self, lambda i: self._get(i, "Finv"), lambda: ids(lambda L: True))
+
+    def _ids(self, nonroot):
+        return [int(i) for L in _real_levels(self.H) if (L.lv > 0 or not nonroot) for i in L.ids]
+
+    @property
+    def E(self):
+        return _BoxView(self, lambda i: self._get(i, "E"), lambda: self._ids(True))
+
+    @property
+    def Finv(self):
+        return _BoxView(self, lambda i: self._get(i, "Finv"), lambda: self._ids(False))
 
     def _get(self, i, which):
         L, j = self.H._lvl_of[i]
@@ -723,7 +757,8 @@ def factorize(spec, grid, tree, eps, opts, quad=PLAIN):
         side = _SIDE[H.device] = torch.cuda.Stream(H.device)
     _factorize_levels(H, inv, pad, main, side)
     main.wait_stream(side)
-    for L, pmin, pmax, what in inv._checks:
+    checks, inv._checks = inv._checks, []
+    for L, pmin, pmax, what in checks:
         _check_singular(H, L, pmin, pmax, what)
     return H, inv
 
@@ -747,7 +782,10 @@ class _Worker:
             while True:
                 fn, args, ev, box = self.tasks.get()
                 if box.get("error") is not None:
-                    box["pending"] -= 1
+                    fn = args = ev = None
+                    with box["cv"]:
+                        box["pending"] -= 1
+                        box["cv"].notify_all()
                     continue
                 try:
                     if ev is not None:
@@ -755,9 +793,12 @@ class _Worker:
                     fn(*args)
                 except BaseException as e:  # re-raised on the caller's thread
                     box["error"] = e
+                # drop the task's references (the factor object) before idling
+                fn = args = ev = None
                 with box["cv"]:
                     box["pending"] -= 1
                     box["cv"].notify_all()
+                box = None
 
     def submit(self, box, fn, args, ev):
         with box["cv"]:
