@@ -239,7 +239,7 @@ struct HState;
 __global__ void k_norm_downdate(const int* pv, const int* mv, const int* active, const int* bsv,
                                 int J, const double* Rm, long long sR, int ldR, double* tn,
                                 const double* tn0, int* flag, int ldt, const double* cutv,
-                                int* any) {
+                                int* certany, int* flagany) {
   const int b = blockIdx.y;
   if (!active[b]) return;
   const int bs = bsv[b];
@@ -256,8 +256,20 @@ __global__ void k_norm_downdate(const int* pv, const int* mv, const int* active,
   const double nv = cur * cur - w;
   const bool bad = !(nv > fmax(1e-12 * ref * ref, 4.0 * cut * cut));
   tn[o] = sqrt(fmax(nv, 0.0));
-  flag[o] = bad;
-  if (bad) atomicOr(any, 1);
+  flag[o] = bad;  // monotone: nv only decreases until an exact recompute resets ref
+  if (bad) atomicOr(flagany + b, 1);
+  else atomicOr(certany + b, 1);
+}
+
+// Exact norms are needed only when they can change a decision: termination
+// (and the in-block rank) is decided on max residual <= cut, which cannot hold
+// while some column is certainly above the cut.  So an item asks for a flush +
+// exact recompute only when it has flagged columns and no certain one.
+__global__ void k_need_exact(const int* active, const int* certany, const int* flagany, int count,
+                             int* any) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= count || !active[b]) return;
+  if (flagany[b] && !certany[b]) atomicOr(any, 1);
 }
 
 __global__ void k_norm_exact(const double* A, long long sA, int lda, const int* pv, const int* mv,
@@ -295,6 +307,8 @@ struct HState {
   double* tn0;    // last exactly computed norm of each column (downdating reference)
   int* flag;      // count x maxm: column needs an exact norm
   int* pf;        // p - Jf (rows touched by the pending reflectors) if active else 0
+  int* certany;   // count: some trailing column certainly above the cut (this block)
+  int* flagany;   // count (follows certany): some trailing column flagged
   double* Rt;     // count x HB x HB block R (upper)
   double* Tt;     // count x HB x HB block reflector T (upper)
   double* Vw;     // count x maxp x (HB*D): Householder vectors of the pending blocks
@@ -722,6 +736,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.active = buf.get<int>(count); S.done = buf.get<int>(count); S.k = kdev;
     S.bs = buf.get<int>(count); S.nrem = buf.get<int>(count); S.pact = buf.get<int>(count);
     S.sact = buf.get<int>(count); S.pf = buf.get<int>(count);
+    S.certany = buf.get<int>(2 * (size_t)count); S.flagany = S.certany + count;
     S.swaps = buf.get<int>((size_t)SWL * count);
     S.cut = buf.get<double>(count); S.tn = buf.get<double>((size_t)maxm * count);
     S.tn0 = buf.get<double>((size_t)maxm * count);
@@ -897,9 +912,12 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       // which are only formed on a current A (after a flush)
       prof_push(st, "id.norms+rank");
       VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
+      VF_CUDA(cudaMemsetAsync(S.certany, 0, sizeof(int) * 2 * count, st));
       k_norm_downdate<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(
-          d->p, d->m, S.active, S.bs, J, Rm, sR, ldR, S.tn, S.tn0, S.flag, maxm, S.cut, S.any);
-      ++g_launches;
+          d->p, d->m, S.active, S.bs, J, Rm, sR, ldR, S.tn, S.tn0, S.flag, maxm, S.cut,
+          S.certany, S.flagany);
+      k_need_exact<<<cdiv(count, 128), 128, 0, st>>>(S.active, S.certany, S.flagany, count, S.any);
+      g_launches += 2;
       int need = 0;
       VF_CUDA(cudaMemcpyAsync(&need, S.any, sizeof(int), cudaMemcpyDeviceToHost, st));
       VF_CUDA(cudaStreamSynchronize(st));
