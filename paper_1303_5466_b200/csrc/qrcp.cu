@@ -31,6 +31,7 @@
 //  inverses + DMMA GEMM updates), identical for both paths.
 #include <vector>
 #include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 #include "panels.cuh"
 #include "../../include/vief_b200.h"
@@ -744,6 +745,10 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.Rt = buf.get<double>((size_t)HB * HB * count);
     S.Tt = buf.get<double>((size_t)HB * HB * count);
     S.D = maxm >= 4096 ? 8 : (maxm >= 2048 ? 4 : (maxm >= 512 ? 2 : 1));
+    if (const char* e = getenv("VF_ID_DPOLICY")) {  // A/B timing of the delay depth
+      if (e[0] == '1') S.D = maxm >= 1024 ? 8 : (maxm >= 256 ? 4 : (maxm >= 128 ? 2 : 1));
+      if (e[0] == '2') S.D = maxm >= 512 ? 8 : (maxm >= 128 ? 4 : 2);
+    }
     const int D = S.D, ldU = HB * D;
     S.Vw = buf.get<double>((size_t)maxp * HB * D * count);
     S.Up = buf.get<double>((size_t)ldU * maxm * count);
