@@ -439,12 +439,20 @@ def run_ours(a):
         Fh = F.cpu().pin_memory()
         Xh = torch.empty_like(Fh).pin_memory()
 
+        copy_stream = torch.cuda.Stream()
+
         def e2e_step():
+            # the step's RHS upload is issued first on its own stream, so it
+            # overlaps the factorization (it is still inside the timed region)
+            with torch.cuda.stream(copy_stream):
+                Fd = Fh.to("cuda", non_blocking=True)
             inv2 = compress_inverse(spec, grid, eps=1e-10, opts=opts, quad=CELL)
-            Xd = inv2.apply(Fh.to("cuda", non_blocking=True))
+            torch.cuda.current_stream().wait_stream(copy_stream)
+            Fd.record_stream(torch.cuda.current_stream())
+            Xd = inv2.apply(Fd)
             Xh.copy_(Xd, non_blocking=True)
             torch.cuda.synchronize()
-            del inv2, Xd
+            del inv2, Xd, Fd
 
         for _ in range(a.warmup):
             e2e_step()
@@ -461,7 +469,8 @@ def run_ours(a):
         out["e2e"] = {"value": world * N / te, "unit": UNIT, "h2d_bytes_per_step": int(N * nrhs * 8),
                       "d2h_bytes_per_step": int(N * nrhs * 8), "ms_per_step": te * 1e3,
                       "api": "solver_compressed.compress_inverse(k_cut=None) + .apply(pinned host "
-                             "RHS -> device) + device->pinned host copy of the solution"}
+                             "RHS -> device, upload issued on a copy stream before the factor) + "
+                             "device->pinned host copy of the solution"}
 
     # CPU baseline (oracle port), rank 0, single GPU only
     if rank == 0 and world == 1 and not a.no_cpu:
