@@ -4,7 +4,9 @@ Metric (BASELINE.json): factor & solve unknowns/sec at N=1024^2, tol 1e-10.
 One step = build_tree + compress_outer + invert_dense_block (the factor) and a
 256-RHS solve, on config 4 (Laplace log-kernel VIE, float64, leaf 64,
 eps 1e-10, BASELINE bump on the rows, cell-integral diagonal; synthetic
-seeded N(0,1) right-hand sides).  value = N / step time, RHS resident in HBM.
+seeded N(0,1) right-hand sides), run as solver_dense.factor_solve (levels
+pipelined over streams; same results as the three calls back to back).
+value = N / step time, RHS resident in HBM.
 e2e = the same step through the public API (compress_inverse + apply) with the
 256 RHS copied from pinned host memory and the solution copied back.
 
@@ -320,35 +322,36 @@ def run_ours(a):
     stage = {}
 
     def step(record=False):
-        """One step: build_tree + factorize (compress_outer + invert_dense_block,
-        levels pipelined over two streams) + 256-RHS solve."""
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        """One step: build_tree + factor_solve (compress_outer + invert_dense_block
+        with the levels pipelined over two streams, the solve's up sweep
+        overlapping the coarser levels' factorization) of the 256 RHS."""
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ev[0].record()
         tree = build_tree(grid, 64)
-        H, inv = sd.factorize(spec, grid, tree, 1e-10, opts, CELL)
+        H, inv, X = sd.factor_solve(spec, grid, tree, 1e-10, opts, F, CELL)
         ev[1].record()
-        X = inv.apply(F)
-        ev[2].record()
         if record:
             torch.cuda.synchronize()
-            stage.setdefault("factor", []).append(ev[0].elapsed_time(ev[1]))
-            stage.setdefault("solve", []).append(ev[1].elapsed_time(ev[2]))
+            stage.setdefault("step", []).append(ev[0].elapsed_time(ev[1]))
         return H, inv, X
 
     def staged_step():
         """Untimed diagnostic step with the stages run back to back (no overlap),
-        for the per-stage rooflines."""
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        for the per-stage split and rooflines."""
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record()
         tree = build_tree(grid, 64)
         H = sd.compress_outer(spec, grid, tree, 1e-10, opts, CELL)
         ev[1].record()
         inv = sd.invert_dense_block(H)
         ev[2].record()
+        X = inv.apply(F)
+        ev[3].record()
         torch.cuda.synchronize()
         stage.setdefault("compress", []).append(ev[0].elapsed_time(ev[1]))
         stage.setdefault("invert", []).append(ev[1].elapsed_time(ev[2]))
-        del H, inv
+        stage.setdefault("solve", []).append(ev[2].elapsed_time(ev[3]))
+        del H, inv, X
 
     for _ in range(a.warmup):
         H, inv, X = step()
@@ -382,9 +385,9 @@ def run_ours(a):
     del H, inv, X
     _lib.release_memory()  # the pipelined steps cached blocks on their own streams
     staged_step()          # warms the allocator for the back-to-back schedule
-    stage.pop("compress"), stage.pop("invert")
+    stage.pop("compress"), stage.pop("invert"), stage.pop("solve")
     staged_step()
-    t_f = statistics.mean(stage["factor"]) / 1e3
+    t_step = statistics.mean(stage["step"]) / 1e3
     t_c = statistics.mean(stage["compress"]) / 1e3
     t_i = statistics.mean(stage["invert"]) / 1e3
     t_s = statistics.mean(stage["solve"]) / 1e3
@@ -424,10 +427,10 @@ def run_ours(a):
            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": _config(n, nrhs, world),
-           "factor_s": t_f, "solve_s": t_s,
-           "factor_unknowns_per_s": N / t_f,
+           "step_s": t_step,
+           "stage_seconds_unpipelined": {"compress_outer": t_c, "invert_dense_block": t_i,
+                                         "apply": t_s},
            "solve_unknown_rhs_per_s": N * nrhs / t_s,
-           "stage_seconds_unpipelined": {"compress_outer": t_c, "invert_dense_block": t_i},
            "approx_residual_E": float(r), "max_rank": max_rank,
            "factor_bytes": fbytes, "roofline": roof, "roofline_stages": stages,
            "gpu_launches": int(launches)}

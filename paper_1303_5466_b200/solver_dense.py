@@ -739,7 +739,24 @@ def invert_dense_block(H, spill=None, free_source=False):
 _SIDE = {}
 
 
+def factor_solve(spec, grid, tree, eps, opts, f, quad=PLAIN):
+    """factorize() and the solve of f in one pass: the up sweep of level l runs
+    (third stream) as soon as level l is inverted, overlapping the
+    factorization of the coarser levels; the down sweep follows.  Returns
+    (H, inv, x) with x = inv.apply(f) (bitwise: same kernels, same order per
+    level)."""
+    H, inv, (fd, single, phi, ups) = _factorize(spec, grid, tree, eps, opts, quad, rhs=f)
+    out = torch.zeros_like(fd)
+    _sweep_down(H, phi, ups, out)
+    return H, inv, _from_device(out, f, single, H.realified)
+
+
 def factorize(spec, grid, tree, eps, opts, quad=PLAIN):
+    H, inv, _ = _factorize(spec, grid, tree, eps, opts, quad)
+    return H, inv
+
+
+def _factorize(spec, grid, tree, eps, opts, quad=PLAIN, rhs=None):
     """compress_outer + invert_dense_block with the levels pipelined over two
     CUDA streams: level l is inverted (side stream) while level l-1 is being
     compressed (current stream).  Inverting level l needs only level l's
@@ -752,15 +769,20 @@ def factorize(spec, grid, tree, eps, opts, quad=PLAIN):
     # compression on the caller's stream, inversions on a second stream (a
     # high-priority compression stream was measured slower: 2.54 vs 2.46 s)
     main = torch.cuda.current_stream(H.device)
-    side = _SIDE.get(H.device)
-    if side is None:
-        side = _SIDE[H.device] = torch.cuda.Stream(H.device)
-    _factorize_levels(H, inv, pad, main, side)
+    if H.device not in _SIDE:
+        _SIDE[H.device] = (torch.cuda.Stream(H.device), torch.cuda.Stream(H.device))
+    side, third = _SIDE[H.device]
+    solve = None
+    if rhs is not None:
+        fd, single = _as_device_rhs(rhs, grid.n, H.device, H.realified)
+        solve = (fd, single, {}, {})
+    _factorize_levels(H, inv, pad, main, side, third, solve)
     main.wait_stream(side)
+    main.wait_stream(third)
     checks, inv._checks = inv._checks, []
     for L, pmin, pmax, what in checks:
         _check_singular(H, L, pmin, pmax, what)
-    return H, inv
+    return H, inv, solve
 
 
 class _Worker:
@@ -814,7 +836,15 @@ class _Worker:
 _WORKERS = {}
 
 
-def _factorize_levels(H, inv, pad, main, side):
+def _up_level_on(stream, H, L, fd, phi, ups):
+    """Worker task: the up sweep of level L on `stream`, after the side
+    stream's inversion of L (the task runs on the worker right after it)."""
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        _sweep_up_level(H, L, fd, phi, ups)
+
+
+def _factorize_levels(H, inv, pad, main, side, third=None, solve=None):
     """Compression on this thread (main stream); the inversion work is
     enqueued on the side stream by a worker thread.  Enqueueing a large
     Gauss-Jordan inversion blocks the host for as long as the GPU runs it (the
@@ -841,6 +871,9 @@ def _factorize_levels(H, inv, pad, main, side):
             ev = torch.cuda.Event()
             ev.record(main)
             w.submit(box, _invert_level_rest, (inv, L, checks), ev)
+            if solve is not None:
+                fd, _, phi, ups = solve
+                w.submit(box, _up_level_on, (third, H, L, fd, phi, ups), None)
             _mark(f"compress:{L.lv}")
             if box["error"] is not None:
                 break
@@ -918,36 +951,43 @@ def _real_levels(H):
     return [L for L in H.levels if L is not None and not getattr(L, "virtual", False)]
 
 
+def _sweep_up_level(H, L, fd, phi, ups):
+    """One level of the up sweep: phi = F^{-1} u, ups = C phi."""
+    dev = H.device
+    r, n = fd.shape
+    nb, mm = L.nb, L.mmax
+    ldv = nb * mm
+    U = torch.zeros((r, ldv), dtype=_F64, device=dev)
+    if L.leaf:
+        _lib.gather_rows(fd, 0, n, L.rows, mm, U, mm, ldv, L.m_d, mm, None, r, nb)
+    else:
+        C = H.levels[L.lv + 1]
+        _lib.gather_rows(ups[C.lv], 2 * C.kmax, C.nb * C.kmax, L.cat_idx, mm, U, mm, ldv,
+                         L.m_d, mm, None, r, nb)
+    Phi = torch.zeros((r, ldv), dtype=_F64, device=dev)
+    if getattr(L, "rb", None) is not None:
+        _root_block_solve(L, U, ldv, r, Phi, ldv)
+    else:
+        _mv(L.Finv, mm * mm, mm, U, mm, ldv, Phi, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r,
+            1.0, 0.0)
+    del U
+    phi[L.lv] = Phi
+    if L.lv == 0:
+        return
+    kk = L.kmax
+    Ups = torch.zeros((r, nb * kk), dtype=_F64, device=dev)
+    _mv(L.C, mm * kk, kk, Phi, mm, ldv, Ups, kk, nb * kk, kk, mm, L.k_d, L.m_d, nb, r,
+        1.0, 0.0)
+    ups[L.lv] = Ups
+
+
 def _sweep_up(H, fd, phi, ups):
     """Up sweep (solver_dense.py:303-310): phi = F^{-1} u, ups = C phi = E R phi.
     ups of a virtual child level must be present in `ups` beforehand."""
-    dev = H.device
-    r, n = fd.shape
     for L in reversed(_real_levels(H)):
-        nb, mm = L.nb, L.mmax
-        ldv = nb * mm
-        U = torch.zeros((r, ldv), dtype=_F64, device=dev)
-        if L.leaf:
-            _lib.gather_rows(fd, 0, n, L.rows, mm, U, mm, ldv, L.m_d, mm, None, r, nb)
-        else:
-            C = H.levels[L.lv + 1]
-            _lib.gather_rows(ups[C.lv], 2 * C.kmax, C.nb * C.kmax, L.cat_idx, mm, U, mm, ldv,
-                             L.m_d, mm, None, r, nb)
-        Phi = torch.zeros((r, ldv), dtype=_F64, device=dev)
-        if getattr(L, "rb", None) is not None:
-            _root_block_solve(L, U, ldv, r, Phi, ldv)
-        else:
-            _mv(L.Finv, mm * mm, mm, U, mm, ldv, Phi, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r,
-                1.0, 0.0)
-        del U
-        phi[L.lv] = Phi
+        _sweep_up_level(H, L, fd, phi, ups)
         if L.lv == 0:
             break
-        kk = L.kmax
-        Ups = torch.zeros((r, nb * kk), dtype=_F64, device=dev)
-        _mv(L.C, mm * kk, kk, Phi, mm, ldv, Ups, kk, nb * kk, kk, mm, L.k_d, L.m_d, nb, r,
-            1.0, 0.0)
-        ups[L.lv] = Ups
 
 
 def _phi_dn(H, L, phi, r):

@@ -179,6 +179,23 @@ def test_kcut_none_delegates_bitwise():
     np.testing.assert_array_equal(inv.apply(v), ref.apply(v))
 
 
+@pytest.mark.parametrize("n_side,nrhs", [(28, 1), (64, 7)])
+def test_factor_solve_matches_factorize_apply_bitwise(n_side, nrhs):
+    """The pipelined factor_solve (up sweep overlapping the factorization) is
+    the same computation as compress_outer + invert_dense_block + apply."""
+    P, sd = _api()
+    spec = laplace_nti()
+    grid = P.Grid(n_side)
+    tree = P.build_tree(grid, 49 if n_side == 28 else 64)
+    opts = P.SolverOptions(eps=1e-10, k_cut=None)
+    rng = np.random.default_rng(5)
+    f = rng.standard_normal(grid.n) if nrhs == 1 else rng.standard_normal((grid.n, nrhs))
+    H, inv, x = sd.factor_solve(spec, grid, tree, 1e-10, opts, f)
+    ref = sd.invert_dense_block(sd.compress_outer(spec, grid, tree, 1e-10, opts))
+    np.testing.assert_array_equal(x, ref.apply(f))
+    np.testing.assert_array_equal(inv.apply(f), x)
+
+
 def test_batch_vs_sequential_rhs():
     _, sd = _api()
     spec, grid, tree, H = setup(28)
