@@ -363,13 +363,16 @@ extern "C" int vief_dgemm_batched(const vief_gemm_desc* d, void* stream) {
   if (tile < 0) {
     const char* e = getenv("VF_GEMM_TILE");
     tile = !e ? 0 : !strcmp(e, "64x64w16") ? 1 : !strcmp(e, "64x64w32") ? 2
-         : !strcmp(e, "128x64w16") ? 3 : !strcmp(e, "64x128w16") ? 4 : 0;
+         : !strcmp(e, "128x64w16") ? 3 : !strcmp(e, "64x128w16") ? 4
+         : !strcmp(e, "64x128w64") ? 5 : !strcmp(e, "128x64w64") ? 6 : 0;
   }
   int rc;
   if (d->M <= 32) rc = dispatch_gemm<32, 128>(d, st);
   else if (tile == 1) rc = dispatch_gemm<64, 64, 32, 16>(d, st);
   else if (tile == 3) rc = dispatch_gemm<128, 64, 32, 32>(d, st);
   else if (tile == 4) rc = dispatch_gemm<64, 128, 32, 16>(d, st);
+  else if (tile == 5) rc = dispatch_gemm<64, 128, 32, 64>(d, st);
+  else if (tile == 6) rc = dispatch_gemm<128, 64, 64, 32>(d, st);
   else rc = dispatch_gemm<64, 64, 32, 32>(d, st);
   if (rc) return rc;
   ++g_launches;
