@@ -438,8 +438,10 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
         sel[i] = ci;
         if (ci >= c0 && ci < c1) nrm[ci - c0] = -1.0;
       }
-      // classical Gram-Schmidt against Qb[0..i), twice
-      for (int pass = 0; pass < 2; ++pass) {
+      // classical Gram-Schmidt against Qb[0..i); a second pass only when the
+      // first removed more than half of the vector ("twice is enough")
+      double nn_prev = warp_sum(y0 * y0 + y1 * y1);
+      for (int pass = 0; pass < 2 && i > 0; ++pass) {
         yv[lane] = y0;
         if (lane + 32 < HSK) yv[lane + 32] = y1;
         __syncwarp();
@@ -468,6 +470,9 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
         y0 -= a0 + a1;
         y1 -= b0 + b1;
         __syncwarp();
+        const double nn_now = warp_sum(y0 * y0 + y1 * y1);
+        if (nn_now > 0.25 * nn_prev) break;  // uniform across the warp
+        nn_prev = nn_now;
       }
       const double nn = warp_sum(y0 * y0 + y1 * y1);
       const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
