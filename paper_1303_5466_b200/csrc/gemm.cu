@@ -275,59 +275,117 @@ static int dispatch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
-// GEMV.  notrans: y(m) = alpha*sum_k A(m,k) x(k) + beta*y(m): CTA = 128 rows x
-// all columns of one item, 4 column-groups of 32 threads?  Layout: 256 threads,
-// thread (r = tid&63, cg = tid>>6): rows m0+r and m0+64+r, columns cg, cg+4, ...
-// A column chunk of 128 rows is 1 KiB contiguous -> coalesced.
-constexpr int GV_ROWS = 128;
+// GEMV, notrans: y(m) = alpha * A x + beta * y, A column-major (M x K, lda).
+// HBM-streaming design (the 1-RHS solve sweeps read every stored factor once):
+// a CTA owns a 64-row tile and a K chunk; each of its 8 warps reads every 8th
+// column of the chunk as one 512-byte coalesced row segment (lane = 2 rows,
+// one 16-byte streaming load), 8 columns unrolled -> 128 B in flight per
+// thread.  The K chunks of one row tile form a thread-block cluster (<= 8
+// CTAs, grid.y); partials are summed warp by warp in shared memory and then
+// across the cluster through DSMEM by rank 0, in a fixed order, so results
+// are bitwise deterministic for a given shape (solver_dense.py:293-329).
+// The split is chosen so that about 4 CTAs per SM are in flight.
+constexpr int GV_ROWS = 64, GV_WARPS = 8, GV_UNROLL = 8;
 
-__global__ void __launch_bounds__(256) k_dgemv_n(vief_gemm_desc d) {
-  const int b = blockIdx.y;
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  return __ldcs(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double ld_stream1(const double* p) { return __ldcs(p); }
+
+__global__ void __launch_bounds__(256) k_dgemv_n(vief_gemm_desc d, int kchunk) {
+  const int b = blockIdx.z;
   GemmItem it = gemm_item(d, b);
   const int m0 = blockIdx.x * GV_ROWS;
-  if (m0 >= it.M) return;
+  if (m0 >= it.M) return;  // uniform over the cluster (same row tile and item)
+  const int k0 = blockIdx.y * kchunk, k1 = min(it.K, k0 + kchunk);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int r = m0 + 2 * lane;
   const double* x = it.B;
-  double* y = it.C;
-  const int tid = threadIdx.x, r = tid & 63, cg = tid >> 6;
-  __shared__ double xs[1024];
-  __shared__ double part[4][GV_ROWS];
+  const bool vec = ((reinterpret_cast<uintptr_t>(it.A) & 15) == 0) && !(d.lda & 1);
   double s0 = 0.0, s1 = 0.0;
-  const int r0 = m0 + r, r1 = m0 + 64 + r;
-  const bool v0 = r0 < it.M, v1 = r1 < it.M;
-  for (int kc = 0; kc < it.K; kc += 1024) {
-    int kn = min(1024, it.K - kc);
-    __syncthreads();
-    for (int i = tid; i < kn; i += 256) xs[i] = x[kc + i];
-    __syncthreads();
-    const double* Ac = it.A + (long long)kc * d.lda;
-    int k = cg;
-    for (; k + 12 < kn; k += 16) {
-      const double* a0 = Ac + (long long)k * d.lda;
-      const double* a1 = a0 + 4LL * d.lda;
-      const double* a2 = a1 + 4LL * d.lda;
-      const double* a3 = a2 + 4LL * d.lda;
-      double x0 = xs[k], x1 = xs[k + 4], x2 = xs[k + 8], x3 = xs[k + 12];
-      if (v0) { s0 = fma(a0[r0], x0, s0); s0 = fma(a1[r0], x1, s0); s0 = fma(a2[r0], x2, s0); s0 = fma(a3[r0], x3, s0); }
-      if (v1) { s1 = fma(a0[r1], x0, s1); s1 = fma(a1[r1], x1, s1); s1 = fma(a2[r1], x2, s1); s1 = fma(a3[r1], x3, s1); }
-    }
-    for (; k < kn; k += 4) {
-      const double* a0 = Ac + (long long)k * d.lda;
-      if (v0) s0 = fma(a0[r0], xs[k], s0);
-      if (v1) s1 = fma(a0[r1], xs[k], s1);
+  if (r < it.M) {
+    const bool two = r + 1 < it.M;
+    int k = k0 + w;
+    if (vec && two) {
+      for (; k + (GV_UNROLL - 1) * GV_WARPS < k1; k += GV_UNROLL * GV_WARPS) {
+        const double* p0 = it.A + (long long)k * d.lda + r;
+        const long long st = (long long)GV_WARPS * d.lda;
+        double a[2 * GV_UNROLL];
+        // all eight 16-byte streaming loads issued back to back (one asm block,
+        // so the scheduler cannot interleave them with the dependent FMAs)
+        asm volatile(
+            "ld.global.cs.v2.f64 {%0, %1}, [%16];\n\t"
+            "ld.global.cs.v2.f64 {%2, %3}, [%17];\n\t"
+            "ld.global.cs.v2.f64 {%4, %5}, [%18];\n\t"
+            "ld.global.cs.v2.f64 {%6, %7}, [%19];\n\t"
+            "ld.global.cs.v2.f64 {%8, %9}, [%20];\n\t"
+            "ld.global.cs.v2.f64 {%10, %11}, [%21];\n\t"
+            "ld.global.cs.v2.f64 {%12, %13}, [%22];\n\t"
+            "ld.global.cs.v2.f64 {%14, %15}, [%23];"
+            : "=d"(a[0]), "=d"(a[1]), "=d"(a[2]), "=d"(a[3]), "=d"(a[4]), "=d"(a[5]),
+              "=d"(a[6]), "=d"(a[7]), "=d"(a[8]), "=d"(a[9]), "=d"(a[10]), "=d"(a[11]),
+              "=d"(a[12]), "=d"(a[13]), "=d"(a[14]), "=d"(a[15])
+            : "l"(p0), "l"(p0 + st), "l"(p0 + 2 * st), "l"(p0 + 3 * st), "l"(p0 + 4 * st),
+              "l"(p0 + 5 * st), "l"(p0 + 6 * st), "l"(p0 + 7 * st));
+        double xv[GV_UNROLL];
+#pragma unroll
+        for (int u = 0; u < GV_UNROLL; ++u) xv[u] = __ldg(x + k + u * GV_WARPS);
+#pragma unroll
+        for (int u = 0; u < GV_UNROLL; ++u) { s0 = fma(a[2 * u], xv[u], s0); s1 = fma(a[2 * u + 1], xv[u], s1); }
+      }
+      for (; k < k1; k += GV_WARPS) {
+        double2 a = ld_stream2(it.A + (long long)k * d.lda + r);
+        double xv = __ldg(x + k);
+        s0 = fma(a.x, xv, s0);
+        s1 = fma(a.y, xv, s1);
+      }
+    } else {
+      for (; k < k1; k += GV_WARPS) {
+        const double* a = it.A + (long long)k * d.lda + r;
+        double xv = __ldg(x + k);
+        s0 = fma(ld_stream1(a), xv, s0);
+        if (two) s1 = fma(ld_stream1(a + 1), xv, s1);
+      }
     }
   }
-  part[cg][r] = s0;
-  part[cg][64 + r] = s1;
+  __shared__ double part[GV_WARPS][GV_ROWS];
+  __shared__ double tot[GV_ROWS];
+  part[w][2 * lane] = s0;
+  part[w][2 * lane + 1] = s1;
   __syncthreads();
   if (tid < GV_ROWS) {
-    int gm = m0 + tid;
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < GV_WARPS; ++i) t += part[i][tid];
+    tot[tid] = t;
+  }
+  const int cs = gridDim.y;  // cluster = all K chunks of this row tile
+  if (cs > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
+  if (blockIdx.y == 0 && tid < GV_ROWS) {
+    double t = tot[tid];
+    if (cs > 1) {
+      unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&tot[tid]));
+      for (int q = 1; q < cs; ++q) {
+        unsigned ra;
+        double v;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(q));
+        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+        t += v;
+      }
+    }
+    const int gm = m0 + tid;
     if (gm < it.M) {
-      double s = (part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]);
-      double v = d.alpha * s;
-      if (d.beta != 0.0) v = fma(d.beta, y[gm], v);
-      y[gm] = v;
+      double v = d.alpha * t;
+      if (d.beta != 0.0) v = fma(d.beta, it.C[gm], v);
+      it.C[gm] = v;
     }
   }
+  if (cs > 1)  // keep every CTA's shared memory alive until rank 0 has read it
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // trans: y(n) = alpha * sum_k A(k,n) x(k) + beta*y(n) (A is K x M stored, op = T,
@@ -380,12 +438,38 @@ extern "C" int vief_dgemm_batched(const vief_gemm_desc* d, void* stream) {
   return VF_OK;
 }
 
+// CTAs in flight the notrans GEMV aims for (VF_GEMV_CTAS overrides, for A/B timing)
+static int gv_target_ctas() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VF_GEMV_CTAS");
+    v = e ? std::max(1, atoi(e)) : 8 * 148;
+  }
+  return v;
+}
+
 extern "C" int vief_dgemv_batched(const vief_gemm_desc* d, void* stream) {
   if (!d || d->batch <= 0 || d->M <= 0) return VF_OK;
   if (d->batch > 65535) { set_error("dgemv: batch %d > 65535", d->batch); return VF_EARG; }
   if (!d->transA) {
-    dim3 grid(cdiv(d->M, GV_ROWS), d->batch);
-    k_dgemv_n<<<grid, 256, 0, (cudaStream_t)stream>>>(*d);
+    const int tiles = (int)cdiv(d->M, GV_ROWS) * d->batch;
+    // K split (cluster size) so that ~4 CTAs per SM stream concurrently; each
+    // CTA keeps at least 8 columns per warp
+    int cs = std::max(1, std::min(8, (int)cdiv(gv_target_ctas(), tiles)));
+    cs = std::max(1, std::min(cs, d->K / (8 * GV_WARPS)));
+    const int kchunk = (int)cdiv(cdiv(d->K, cs), GV_WARPS) * GV_WARPS;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cdiv(d->M, GV_ROWS), cs, d->batch);
+    cfg.blockDim = dim3(256);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = cs;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VF_CUDA(cudaLaunchKernelEx(&cfg, k_dgemv_n, *d, kchunk));
   } else {
     dim3 grid(cdiv(d->M, 8), d->batch);
     k_dgemv_t<<<grid, 256, 0, (cudaStream_t)stream>>>(*d);
