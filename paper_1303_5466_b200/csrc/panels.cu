@@ -29,9 +29,17 @@ extern long long g_launches;
 constexpr int PT = 256;  // threads per CTA
 constexpr int NW = PT / 32;
 
+// Single-CTA "clusters" (short panels, many matrices) skip the cluster
+// machinery: a cluster barrier carries a GPU-scope release fence (MEMBAR) and
+// an L1 invalidate, and DSMEM addressing is slower than plain shared memory.
 template <typename T>
 __device__ __forceinline__ T* remote(cg::cluster_group& cl, T* local, int rank) {
+  if (cl.num_blocks() == 1) return local;
   return static_cast<T*>(cl.map_shared_rank(static_cast<void*>(local), rank));
+}
+__device__ __forceinline__ void csync(cg::cluster_group& cl) {
+  if (cl.num_blocks() == 1) __syncthreads();
+  else cl.sync();
 }
 
 // ---------------------------------------------------------------------------
@@ -84,7 +92,7 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(const double* A, long long s
       for (int l = tid; l < nbs; l += PT) x.cand_row[l] = P[l * ldp + (iv - r0)];
     if (cr == oj)
       for (int l = tid; l < nbs; l += PT) x.rowj[l] = P[l * ldp + (j - r0)];
-    cl.sync();
+    csync(cl);
     if (tid < 32) {  // lanes read one rank's candidate each; ties -> smaller row
       double cv = -2.0;
       int ci = 0x7fffffff;
@@ -121,7 +129,7 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(const double* A, long long s
     if (cr == 0 && tid == 0) ipiv[b * sPiv + c0 + j] = c0 + piv;
     __syncthreads();
   }
-  cl.sync();  // no CTA may exit while others could still read its exchange area
+  csync(cl);  // no CTA may exit while others could still read its exchange area
   if (cr != 0) return;
   // pivot block (rows 0..nbs-1) lives in CTA 0 (rows_per >= nbs)
   for (int idx = tid; idx < nbs * nbs; idx += PT) {
@@ -224,7 +232,7 @@ __global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long s
     }
     if (cr == oj)
       for (int l = j + 1 + tid; l < bs; l += PT) x.rowj[l] = P[l * ldp + (j - r0)];
-    cl.sync();
+    csync(cl);
     if (tid < 32) {
       double v = tid < cs ? remote(cl, &x, tid)->ss : 0.0;
       v = warp_sum(v);
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long s
       const int r = idx % bs, c = idx / bs;
       xg.V1[c * PNB + r] = r < nr ? P[c * ldp + r] : 0.0;
     }
-  cl.sync();
+  csync(cl);
   // T (upper, dlarft forward columnwise) from tau and G; M = T V1^T
   for (int idx = tid; idx < bs * bs; idx += PT) {
     const int a = idx % bs, c = idx / bs;
@@ -330,7 +338,7 @@ __global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long s
     }
   }
   __syncthreads();
-  cl.sync();  // remote reads done before any CTA may exit / reuse
+  csync(cl);  // remote reads done before any CTA may exit / reuse
   // V (already unit lower trapezoidal in P) at absolute rows J.., T and R from CTA 0
   double* Vo = Vw + b * sV + J;
   for (int idx = tid; idx < nr * bs; idx += PT) {
@@ -351,6 +359,56 @@ __global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long s
 // ---------------------------------------------------------------------------
 // QRCP on the sketch Y(:, J:m) (HSK rows) selecting bs pivots; columns split
 // over the cluster.  Output: swap list (dst = J+i, src position).
+// Net permutation of the column window (warp 0 of cluster rank 0): the
+// sequence of transpositions (J+i <-> current position of the chosen column)
+// is tracked as (id, pos) pairs of moved columns; lookups are warp ballots.
+// Output per item: [nm, id[0..nm), pos[0..nm)] -- column originally at id
+// ends at pos.
+constexpr int NM = 2 * PNB + 2;
+__device__ __noinline__ void emit_swaps(const int* sel, int bs, int J, int b, int* swaps, int lane,
+                                        int* mid, int* mpos) {
+  int nm = 0;
+  for (int i = 0; i < bs; ++i) {
+    const int id = J + sel[i], dst = J + i;
+    int src = id, at_dst = dst;
+    unsigned f_id = 0, f_dst = 0;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      const int t = lane + 32 * h;
+      const bool live = t < nm;
+      const unsigned bid = __ballot_sync(0xffffffffu, live && mid[t] == id);
+      const unsigned bds = __ballot_sync(0xffffffffu, live && mpos[t] == dst);
+      if (bid && !f_id) { src = mpos[32 * h + __ffs(bid) - 1]; f_id = 1; }
+      if (bds && !f_dst) { at_dst = mid[32 * h + __ffs(bds) - 1]; f_dst = 1; }
+    }
+    bool f1 = false, f2 = false;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      const int t = lane + 32 * h;
+      bool m1 = false, m2 = false;
+      if (t < nm) {
+        if (mid[t] == at_dst) { mpos[t] = src; m1 = true; }
+        else if (mid[t] == id) { mpos[t] = dst; m2 = true; }
+      }
+      f1 |= __any_sync(0xffffffffu, m1);
+      f2 |= __any_sync(0xffffffffu, m2);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (!f1 && at_dst != src) { mid[nm] = at_dst; mpos[nm] = src; }
+      if (!f2 && id != dst) {
+        const int k = nm + ((!f1 && at_dst != src) ? 1 : 0);
+        mid[k] = id; mpos[k] = dst;
+      }
+    }
+    nm += ((!f1 && at_dst != src) ? 1 : 0) + ((!f2 && id != dst) ? 1 : 0);
+    __syncwarp();
+  }
+  int* out = swaps + (long long)b * SWL;
+  if (lane == 0) out[0] = nm;
+  for (int t = lane; t < nm; t += 32) { out[1 + t] = mid[t]; out[1 + NM + t] = mpos[t]; }
+}
+
 struct XSel {
   double cand_v;
   int cand_i;
@@ -424,7 +482,7 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
         if (lane + 32 < HSK) x.y[lane + 32] = Ys[(ci - c0) * LDY + lane + 32];
       }
     }
-    cl.sync();
+    csync(cl);
     if (warp == 0) {
       double cv = -2.0;
       int ci = 0x7fffffff;
@@ -534,55 +592,12 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
       }
     }
   }
-  cl.sync();
+  csync(cl);
   if (cr != 0 || warp != 0) return;
-  // net permutation of the column window: the sequence of transpositions
-  // (J+i <-> current position of the chosen column) is tracked as (id, pos)
-  // pairs of moved columns; lookups are warp ballots.  Output per item:
-  // [nm, id[0..nm), pos[0..nm)] -- column originally at id ends at pos.
-  constexpr int NM = 2 * PNB + 2;
   __shared__ int mid[NM], mpos[NM];
-  int nm = 0;
-  for (int i = 0; i < bs; ++i) {
-    const int id = J + sel[i], dst = J + i;
-    int src = id, at_dst = dst;
-    unsigned f_id = 0, f_dst = 0;
-#pragma unroll
-    for (int h = 0; h < 3; ++h) {
-      const int t = lane + 32 * h;
-      const bool live = t < nm;
-      const unsigned bid = __ballot_sync(0xffffffffu, live && mid[t] == id);
-      const unsigned bds = __ballot_sync(0xffffffffu, live && mpos[t] == dst);
-      if (bid && !f_id) { src = mpos[32 * h + __ffs(bid) - 1]; f_id = 1; }
-      if (bds && !f_dst) { at_dst = mid[32 * h + __ffs(bds) - 1]; f_dst = 1; }
-    }
-    bool f1 = false, f2 = false;
-#pragma unroll
-    for (int h = 0; h < 3; ++h) {
-      const int t = lane + 32 * h;
-      bool m1 = false, m2 = false;
-      if (t < nm) {
-        if (mid[t] == at_dst) { mpos[t] = src; m1 = true; }
-        else if (mid[t] == id) { mpos[t] = dst; m2 = true; }
-      }
-      f1 |= __any_sync(0xffffffffu, m1);
-      f2 |= __any_sync(0xffffffffu, m2);
-    }
-    __syncwarp();
-    if (lane == 0) {
-      if (!f1 && at_dst != src) { mid[nm] = at_dst; mpos[nm] = src; }
-      if (!f2 && id != dst) {
-        const int k = nm + ((!f1 && at_dst != src) ? 1 : 0);
-        mid[k] = id; mpos[k] = dst;
-      }
-    }
-    nm += ((!f1 && at_dst != src) ? 1 : 0) + ((!f2 && id != dst) ? 1 : 0);
-    __syncwarp();
-  }
-  int* out = swaps + (long long)b * SWL;
-  if (lane == 0) out[0] = nm;
-  for (int t = lane; t < nm; t += 32) { out[1 + t] = mid[t]; out[1 + NM + t] = mpos[t]; }
+  emit_swaps(sel, bs, J, b, swaps, lane, mid, mpos);
 }
+
 
 // ---------------------------------------------------------------------------
 // Register-resident panels.  Each thread keeps RPT whole panel rows (32
@@ -712,7 +727,7 @@ __global__ void __launch_bounds__(PT, 1) k_lu_panel_rr(const double* A, long lon
       x.cand_row[lane] = bv >= 0.0 ? wrow[bw][lane] : 0.0;
       if (lane == 0) { x.cand_v = bv; x.cand_i = bi; }
     }
-    cl.sync();
+    csync(cl);
     if (warp == 0) {  // lanes read one rank's candidate each; ties -> smaller row
       double cv = -2.0;
       int ci = 0x7fffffff;
@@ -774,7 +789,7 @@ __global__ void __launch_bounds__(PT, 1) k_lu_panel_rr(const double* A, long lon
   if (cr == 0 && tid < nbs)
 #pragma unroll
     for (int t = 0; t < PNB; ++t) M[tid][(nbs + t) & (PNB - 1)] = a[0][t];
-  cl.sync();  // no CTA may exit while others could still read its exchange area
+  csync(cl);  // no CTA may exit while others could still read its exchange area
   if (cr != 0) return;
   __syncthreads();
   if (tid < nbs) {
@@ -890,7 +905,7 @@ __global__ void __launch_bounds__(NT, 1) k_qr_panel_rr(const double* A, long lon
       for (int ww = 0; ww < NWt; ++ww) s += red[ww][lane];
       x.S[lane] = s;
     }
-    cl.sync();
+    csync(cl);
     // warp w fetches ranks w, w + NWt, ... (all remote loads in flight together)
     for (int q = warp; q < cs; q += NWt) Sp[q][lane] = remote(cl, &x, q)->S[lane];
     __syncthreads();
@@ -1001,7 +1016,7 @@ __global__ void __launch_bounds__(NT, 1) k_qr_panel_rr(const double* A, long lon
       Rr[c * PNB + i] = Rl[i][c];
     }
   }
-  cl.sync();  // remote reads of this CTA's exchange area are done before it exits
+  csync(cl);  // remote reads of this CTA's exchange area are done before it exits
 }
 
 // ---------------------------------------------------------------------------
@@ -1097,7 +1112,9 @@ int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* a
              const int* bsv, int J, int maxp, int count, double* Vw, long long sV, int ldv,
              double* Tt, double* Rt, cudaStream_t st) {
   const int rows = maxp - J;  // panel rows J..p-1
-  if (rows <= 2 * 128 && panel_mode() != 1) {  // short panels: small CTAs, several per SM
+  static int short_ok = -1;  // VF_QR_SHORT=0 disables the small-CTA path (A/B timing)
+  if (short_ok < 0) { const char* e = getenv("VF_QR_SHORT"); short_ok = !(e && e[0] == '0'); }
+  if (short_ok && rows <= 2 * 128 && panel_mode() != 1) {  // short panels: small CTAs, several per SM
     void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
                     (void*)&J, (void*)&Vw, (void*)&sV, (void*)&ldv, (void*)&Tt, (void*)&Rt};
     const int nt = rows <= 128 ? 64 : 128;
