@@ -316,3 +316,42 @@ def test_helmholtz_matches_reference_solution():
     x = inv.apply(g["f"])
     assert np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"]) <= 1e-9
     assert np.linalg.norm(g["f"] - H.matvec(x)) / np.linalg.norm(g["f"]) <= 1e-9
+
+
+# ---- exact residual at sizes the dense oracle cannot reach (FFT operator) --
+
+@pytest.mark.parametrize("n,nrhs", [(256, 1), (256, 4), (512, 2)])
+def test_true_residual_fft_config_family(n, nrhs):
+    """BASELINE config family (BUMP rows, cell diagonal, leaf 64, eps 1e-10):
+    ||f - A x|| / ||f|| <= 10 eps with A applied exactly by FFT."""
+    P, sd = _api()
+    from paper_1303_5466_b200.verify import FFTOperator, true_residual
+    spec = P.KernelSpec("laplace2d", b_field=P.make_field("centre_bump", scale=math.pi / 2),
+                        c_field=P.make_field("one"))
+    grid = P.Grid(n)
+    eps = 1e-10
+    opts = P.SolverOptions(eps=eps, leaf_size=64, k_cut=None)
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    inv = compress_inverse(spec, grid, eps=eps, opts=opts, quad=P.CELL)
+    f = np.random.default_rng(n + nrhs).standard_normal((grid.n, nrhs) if nrhs > 1 else grid.n)
+    x = inv.apply(f)
+    r = true_residual(spec, grid, P.CELL, f, x, FFTOperator(spec, grid, P.CELL, "cuda"))
+    assert np.all(np.asarray(r) <= 10 * eps), r
+
+
+def test_true_residual_fft_helmholtz():
+    """Lippmann-Schwinger (complex128 through the realified path) at 64^2."""
+    P, sd = _api()
+    from paper_1303_5466_b200.verify import true_residual
+    spec = P.KernelSpec("helmholtz2d", k=20.0, b_field=P.make_field("gaussian_bump"),
+                        c_field=P.make_field("one"))
+    grid = P.Grid(64)
+    eps = 1e-8
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    inv = compress_inverse(spec, grid, eps=eps, opts=P.SolverOptions(eps=eps, leaf_size=64, k_cut=None),
+                           quad=P.PLAIN)
+    xy = grid.points()
+    f = np.exp(1j * 20.0 * (xy[:, 0] + 1.0))
+    x = inv.apply(f)
+    assert np.iscomplexobj(x)
+    assert true_residual(spec, grid, P.PLAIN, f, x) <= 10 * eps

@@ -1,0 +1,3 @@
+VF_PROF=1 python tools/stage_profile.py --n 1024 > gpurun_out/prof_a.txt 2>&1
+VF_QR_SHORT=0 VF_PROF=1 python tools/stage_profile.py --n 1024 > gpurun_out/prof_b.txt 2>&1
+python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo rc=$? >> gpurun_out/gpu_tests.log
