@@ -658,6 +658,12 @@ __device__ __forceinline__ void rotate_left(double (&a)[RPT][PNB]) {
 template <int V>
 struct IC { static constexpr int value = V; };
 
+// measured: one step per loop trip (rotate by one) beats the 4-step unrolled
+// body for both panels -- fewer live registers, no spills (QR panel 199 -> 182 ms
+// over a 1024^2 factorization)
+#ifndef LU_UNROLL4
+#define LU_UNROLL4 0
+#endif
 template <int RPT>
 __global__ void __launch_bounds__(PT, 1) k_lu_panel_rr(const double* A, long long sA, int lda,
                                                        int n, int c0, int nbs, int* ipiv,
@@ -773,7 +779,7 @@ __global__ void __launch_bounds__(PT, 1) k_lu_panel_rr(const double* A, long lon
   };
   int j = 0;
 #pragma unroll 1
-  for (; j + 4 <= nbs; j += 4) {
+  for (; j + 4 <= nbs && LU_UNROLL4; j += 4) {
     step(j, j, IC<0>{});
     step(j + 1, j, IC<1>{});
     step(j + 2, j, IC<2>{});
@@ -834,6 +840,9 @@ struct XQr2 {
   double rowj[PNB];
 };
 
+#ifndef QR_UNROLL4
+#define QR_UNROLL4 0
+#endif
 template <int RPT, int NT = PT>
 __global__ void __launch_bounds__(NT, 1) k_qr_panel_rr(const double* A, long long sA, int lda,
                                                        const int* pv, const int* active,
@@ -960,7 +969,7 @@ __global__ void __launch_bounds__(NT, 1) k_qr_panel_rr(const double* A, long lon
   };
   int j = 0;
 #pragma unroll 1
-  for (; j + 4 <= jmax; j += 4) {
+  for (; j + 4 <= jmax && QR_UNROLL4; j += 4) {
     step(j, j, IC<0>{});
     step(j + 1, j, IC<1>{});
     step(j + 2, j, IC<2>{});
