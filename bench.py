@@ -41,7 +41,7 @@ def _args():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--n", "--side", dest="n", type=int, default=1024)  # --side under torchrun
     ap.add_argument("--nrhs", type=int, default=256)
     ap.add_argument("--cpu-n", type=int, default=128, help="oracle sample grid side")
     ap.add_argument("--no-e2e", action="store_true")
@@ -62,7 +62,7 @@ def _config(n, nrhs, world):
             "n_side": n, "N": n * n, "nrhs": nrhs, "leaf": 64, "eps": 1e-10,
             "kernel": "laplace2d (1/2pi) log r on [-1,1]^2, b = (pi/2)(1+0.5 exp(-|x|^2/0.08)) "
                       "rows, c = 1, cell-integral diagonal",
-            "l2": "inputs and factors (~60 GB) far exceed the 126 MB L2 between steps",
+            "l2": "inputs and factors (~60 GB at 1024^2) far exceed the 126 MB L2 between steps",
             "parallelism": "replicas" if world > 1 else "single GPU"}
 
 
@@ -204,8 +204,10 @@ def run_sharded(a):
     import torch
     import torch.distributed as dist
     rank, world, local = _dist()
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl")
+    torch.cuda.set_device(local % torch.cuda.device_count())
+    # VF_DIST_BACKEND=gloo: host-staged collectives, used only to exercise this
+    # path with several ranks on one GPU (no rank's kernels wait on another's)
+    dist.init_process_group(os.environ.get("VF_DIST_BACKEND", "nccl"))
     from paper_1303_5466_b200 import CELL, Grid, KernelSpec, SolverOptions, build_tree, make_field, _lib
     from paper_1303_5466_b200.distributed import ShardedInverse, TorchComm
     comm = TorchComm()
