@@ -1,6 +1,7 @@
 // Shared device helpers for the vief_b200 sm_100a kernels.
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 

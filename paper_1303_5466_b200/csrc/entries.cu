@@ -13,7 +13,7 @@
 #include "../../include/vief_b200.h"
 
 namespace vf {
-extern long long g_launches;
+extern std::atomic<long long> g_launches;
 
 struct cd { double re, im; };
 

@@ -16,7 +16,7 @@
 #include "../../include/vief_b200.h"
 
 namespace vf {
-extern long long g_launches;
+extern std::atomic<long long> g_launches;
 
 #ifndef VF_GEMM_BK
 #define VF_GEMM_BK 8

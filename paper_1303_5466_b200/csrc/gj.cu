@@ -28,7 +28,7 @@
 #include "../../include/vief_b200.h"
 
 namespace vf {
-extern long long g_launches;
+extern std::atomic<long long> g_launches;
 
 constexpr int GJ_NB = 32;    // inner panel
 constexpr int GJ_NBO = 256;  // outer block (K of the big update GEMM)

@@ -11,7 +11,7 @@
 #include "../../include/vief_b200.h"
 
 namespace vf {
-long long g_launches = 0;
+std::atomic<long long> g_launches{0};
 static thread_local char g_err[512] = "";
 
 void set_error(const char* fmt, ...) {

@@ -24,7 +24,7 @@
 namespace cg = cooperative_groups;
 
 namespace vf {
-extern long long g_launches;
+extern std::atomic<long long> g_launches;
 
 constexpr int PT = 256;  // threads per CTA
 constexpr int NW = PT / 32;

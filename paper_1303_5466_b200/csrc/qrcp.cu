@@ -37,7 +37,7 @@
 #include "../../include/vief_b200.h"
 
 namespace vf {
-extern long long g_launches;
+extern std::atomic<long long> g_launches;
 
 // ---------------------------------------------------------------------------
 // small path: classical QRCP in shared memory

@@ -24,7 +24,9 @@ instead of F (m x m).  All per-box blocks of a level live in one padded HBM
 buffer (column-major, leading dimension = level maximum).
 """
 
+import contextlib
 import ctypes
+import gc
 import os
 import math
 
@@ -447,10 +449,8 @@ def _compress_level_id(H, L, pad, seed):
     rank = torch.zeros(count, dtype=_I32, device=dev)
     perm = torch.zeros((count, mm), dtype=_I32, device=dev)
     T = torch.zeros((count, mm, mm), dtype=_F64, device=dev)
-    d = _lib.IdDesc(_lib.ptr(A), mm * ldA, ldA, _lib.ptr(pv), _lib.ptr(mv), int(p.max()), mm, count, g,
-                    float(H.eps), _lib.ptr(rank), _lib.ptr(perm), _lib.ptr(T), mm * mm, mm,
-                    int(seed) * 1000003 + L.lv, int(getattr(H, "_force_blocked", 0)))
-    _lib.call("vief_id_batched", ctypes.byref(d), st())
+    _id_batched(dev, A, mm * ldA, ldA, pv, mv, int(p.max()), mm, count, g, float(H.eps), rank,
+                perm, T, int(seed) * 1000003 + L.lv, int(getattr(H, "_force_blocked", 0)))
     del A
     L.k = rank[0::g].cpu().numpy().astype(np.int32)
     L.kmax = max(int(L.k.max()), 1)
@@ -482,6 +482,53 @@ def _compress_level_id(H, L, pad, seed):
         L.cskel = L.rskel
 
 
+# The IDs of a level run as two half batches on two streams, each driven by
+# its own host thread (the blocked ID synchronises its stream twice per
+# column block, and ctypes releases the GIL): one half's latency-bound panel
+# and pivot-selection kernels overlap the other half's GEMMs.  Every item's
+# arithmetic is unchanged except for batch-wide choices (GEMM split-K, the
+# shared flush schedule), so results are deterministic for a given split.
+# VF_ID_SPLIT=0 runs one batch.
+_ID_SPLIT = os.environ.get("VF_ID_SPLIT", "1") != "0"
+_ID_SIDE = {}
+
+
+def _id_side(dev):
+    idx = torch.cuda.current_device() if dev.index is None else dev.index
+    ent = _ID_SIDE.get(idx)
+    if ent is None:
+        from concurrent.futures import ThreadPoolExecutor
+        pool = ThreadPoolExecutor(1, thread_name_prefix="vief-id",
+                                  initializer=torch.cuda.set_device, initargs=(idx,))
+        ent = (pool, torch.cuda.Stream(device=idx))
+        _ID_SIDE[idx] = ent
+    return ent
+
+
+def _id_batched(dev, A, sA, ldA, pv, mv, maxp, mm, count, g, eps, rank, perm, T, seed, forced):
+    """vief_id_batched over `count` items (groups of g share a rank)."""
+    def desc(lo, n):
+        return _lib.IdDesc(_lib.ptr(A) + 8 * lo * sA, sA, ldA, _lib.ptr(pv) + 4 * lo,
+                           _lib.ptr(mv) + 4 * lo, maxp, mm, n, g, eps, _lib.ptr(rank) + 4 * lo,
+                           _lib.ptr(perm) + 4 * lo * mm, _lib.ptr(T) + 8 * lo * mm * mm, mm * mm,
+                           mm, seed, forced)
+    nb = count // g
+    if not _ID_SPLIT or nb < 2:
+        _lib.call("vief_id_batched", ctypes.byref(desc(0, count)), _lib.stream_handle())
+        return
+    h = (nb // 2) * g
+    d1, d2 = desc(0, h), desc(h, count - h)
+    pool, side = _id_side(dev)
+    main = torch.cuda.current_stream(dev)
+    side.wait_stream(main)
+    fut = pool.submit(_lib.call, "vief_id_batched", ctypes.byref(d2), side.cuda_stream)
+    try:
+        _lib.call("vief_id_batched", ctypes.byref(d1), main.cuda_stream)
+    finally:
+        fut.result()
+        main.wait_stream(side)
+
+
 def compress_outer(spec, grid, tree, eps, opts, quad=PLAIN, spill=None):
     """Skeletonize all boxes fine-to-coarse, one batch per level
     (solver_dense.py:234-272).  `spill` is accepted for signature
@@ -495,10 +542,11 @@ def compress_levels(H):
     coarse); sharded objects (distributed.py) call this directly."""
     pad = H.opts.resolved_proxy_layers(H.spec)
     _mark("compress:start")
-    for L in reversed(_real_levels(H)):
-        _lib.prof_prefix(f"L{L.lv:02d}.")
-        _compress_level(H, L, pad, H.opts.seed)
-        _mark(f"compress:{L.lv}")
+    with _gc_paused():
+        for L in reversed(_real_levels(H)):
+            _lib.prof_prefix(f"L{L.lv:02d}.")
+            _compress_level(H, L, pad, H.opts.seed)
+            _mark(f"compress:{L.lv}")
     return H
 
 
@@ -782,15 +830,16 @@ def invert_dense_block(H, spill=None, free_source=False):
     (solver_dense.py:332-368).  `free_source` drops D/B once consumed."""
     inv = DenseBlockInverse(H)
     _mark("invert:start")
-    for L in reversed(_real_levels(H)):
-        _lib.prof_prefix(f"L{L.lv:02d}.")
-        _invert_level(inv, L)
-        _mark(f"invert:{L.lv}")
-        if free_source:
-            if L.leaf:
-                L.D = None
-            else:
-                L.B12 = L.B21 = None
+    with _gc_paused():
+        for L in reversed(_real_levels(H)):
+            _lib.prof_prefix(f"L{L.lv:02d}.")
+            _invert_level(inv, L)
+            _mark(f"invert:{L.lv}")
+            if free_source:
+                if L.leaf:
+                    L.D = None
+                else:
+                    L.B12 = L.B21 = None
     return inv
 
 
@@ -799,20 +848,41 @@ _SIDE = {}
 _BLOCK_F = os.environ.get("VF_BLOCK_F", "1") != "0"
 
 
+_GC_PAUSE = os.environ.get("VF_GC_PAUSE", "1") != "0"
+
+
+@contextlib.contextmanager
+def _gc_paused():
+    """Hold Python's cyclic garbage collector while the level loops enqueue
+    GPU work: a collection stops every thread at the GIL, the streams drain and
+    the GPU idles for its duration.  The loops create no reference cycles, so
+    nothing accumulates; collection resumes when they return."""
+    if not _GC_PAUSE or not gc.isenabled():
+        yield
+        return
+    gc.disable()
+    try:
+        yield
+    finally:
+        gc.enable()
+
+
 def factor_solve(spec, grid, tree, eps, opts, f, quad=PLAIN):
     """factorize() and the solve of f in one pass: the up sweep of level l runs
     (third stream) as soon as level l is inverted, overlapping the
     factorization of the coarser levels; the down sweep follows.  Returns
     (H, inv, x) with x = inv.apply(f) (bitwise: same kernels, same order per
     level)."""
-    H, inv, (fd, single, phi, ups) = _factorize(spec, grid, tree, eps, opts, quad, rhs=f)
-    out = torch.zeros_like(fd)
-    _sweep_down(H, phi, ups, out)
-    return H, inv, _from_device(out, f, single, H.realified)
+    with _gc_paused():
+        H, inv, (fd, single, phi, ups) = _factorize(spec, grid, tree, eps, opts, quad, rhs=f)
+        out = torch.zeros_like(fd)
+        _sweep_down(H, phi, ups, out)
+        return H, inv, _from_device(out, f, single, H.realified)
 
 
 def factorize(spec, grid, tree, eps, opts, quad=PLAIN):
-    H, inv, _ = _factorize(spec, grid, tree, eps, opts, quad)
+    with _gc_paused():
+        H, inv, _ = _factorize(spec, grid, tree, eps, opts, quad)
     return H, inv
 
 
@@ -1095,8 +1165,9 @@ def _apply_device(inv, fd):
 
 def _apply(inv, f):
     H = inv.H
-    fd, single = _as_device_rhs(f, H.grid.n, H.device, H.realified)
-    return _from_device(_apply_device(inv, fd), f, single, H.realified)
+    with _gc_paused():
+        fd, single = _as_device_rhs(f, H.grid.n, H.device, H.realified)
+        return _from_device(_apply_device(inv, fd), f, single, H.realified)
 
 
 def apply_inverse_dense_block(inv, f):

@@ -33,7 +33,7 @@ def wrap(name):
 
 for nm in ["_compress_level_blocks", "_compress_level_id", "_invert_level_F", "_invert_level_rest"]:
     wrap(nm)
-for rep in range(2):
+for rep in range(int(os.environ.get("REPS", "3"))):
     rec.clear()
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -44,8 +44,13 @@ for rep in range(2):
     t1 = torch.cuda.Event(enable_timing=True)
     t1.record()
     torch.cuda.synchronize()
+    print(f"rep {rep}: {t0.elapsed_time(t1):.1f} ms", flush=True)
     del H, inv
-print(f"total {t0.elapsed_time(t1):.1f} ms")
+ms = torch.cuda.memory_stats()
+print(f"total {t0.elapsed_time(t1):.1f} ms; torch reserved {torch.cuda.memory_reserved() / 1e9:.1f} GB "
+      f"(max {torch.cuda.max_memory_reserved() / 1e9:.1f}), max allocated "
+      f"{torch.cuda.max_memory_allocated() / 1e9:.1f} GB, alloc retries {ms.get('num_alloc_retries')}, "
+      f"cudaMalloc calls {ms.get('num_device_alloc')}, cudaFree calls {ms.get('num_device_free')}")
 short = {"_compress_level_blocks": "blocks", "_compress_level_id": "ID", "_invert_level_F": "F^-1", "_invert_level_rest": "WGEC"}
 for name, lv, e0, e1, h0, h1 in rec:
     print(f"L{lv:02d} {short[name]:>6s}  gpu {t0.elapsed_time(e0):8.1f} -> {t0.elapsed_time(e1):8.1f}  ({e0.elapsed_time(e1):7.1f})"
