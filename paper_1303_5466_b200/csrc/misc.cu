@@ -272,6 +272,12 @@ void ensure_pool() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     unsigned long long thr = ~0ULL;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // The ID slices and the inversion run on different streams: a workspace
+    // allocation must never be satisfied by making its stream wait for
+    // another stream's pending free (the driver's default may insert such a
+    // dependency, serialising the streams for as long as the other one runs).
+    int no = 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
   }
   done = true;
 }

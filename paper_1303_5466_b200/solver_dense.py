@@ -482,25 +482,25 @@ def _compress_level_id(H, L, pad, seed):
         L.cskel = L.rskel
 
 
-# The IDs of a level run as two half batches on two streams, each driven by
-# its own host thread (the blocked ID synchronises its stream twice per
-# column block, and ctypes releases the GIL): one half's latency-bound panel
-# and pivot-selection kernels overlap the other half's GEMMs.  Every item's
-# arithmetic is unchanged except for batch-wide choices (GEMM split-K, the
-# shared flush schedule), so results are deterministic for a given split.
-# VF_ID_SPLIT=0 runs one batch.
-_ID_SPLIT = os.environ.get("VF_ID_SPLIT", "1") != "0"
+# The IDs of a level run as VF_ID_SPLIT (default 2) slices of the batch on as
+# many streams, each driven by its own host thread (the blocked ID
+# synchronises its stream twice per column block; ctypes releases the GIL):
+# one slice's latency-bound panel and pivot-selection kernels overlap the
+# others' GEMMs.  Every item's arithmetic is unchanged except for batch-wide
+# choices (GEMM split-K, the shared flush schedule), so results are
+# deterministic for a given split.  VF_ID_SPLIT=1 runs one batch.
+_ID_SPLIT = max(1, int(os.environ.get("VF_ID_SPLIT", "2")))
 _ID_SIDE = {}
 
 
-def _id_side(dev):
+def _id_side(dev, n):
     idx = torch.cuda.current_device() if dev.index is None else dev.index
     ent = _ID_SIDE.get(idx)
-    if ent is None:
+    if ent is None or len(ent[1]) < n:
         from concurrent.futures import ThreadPoolExecutor
-        pool = ThreadPoolExecutor(1, thread_name_prefix="vief-id",
+        pool = ThreadPoolExecutor(n, thread_name_prefix="vief-id",
                                   initializer=torch.cuda.set_device, initargs=(idx,))
-        ent = (pool, torch.cuda.Stream(device=idx))
+        ent = (pool, [torch.cuda.Stream(device=idx) for _ in range(n)])
         _ID_SIDE[idx] = ent
     return ent
 
@@ -513,20 +513,25 @@ def _id_batched(dev, A, sA, ldA, pv, mv, maxp, mm, count, g, eps, rank, perm, T,
                            _lib.ptr(perm) + 4 * lo * mm, _lib.ptr(T) + 8 * lo * mm * mm, mm * mm,
                            mm, seed, forced)
     nb = count // g
-    if not _ID_SPLIT or nb < 2:
+    parts = min(_ID_SPLIT, nb)
+    if parts < 2:
         _lib.call("vief_id_batched", ctypes.byref(desc(0, count)), _lib.stream_handle())
         return
-    h = (nb // 2) * g
-    d1, d2 = desc(0, h), desc(h, count - h)
-    pool, side = _id_side(dev)
+    cut = [(nb * i // parts) * g for i in range(parts + 1)]
+    descs = [desc(cut[i], cut[i + 1] - cut[i]) for i in range(parts)]
+    pool, sides = _id_side(dev, parts - 1)
     main = torch.cuda.current_stream(dev)
-    side.wait_stream(main)
-    fut = pool.submit(_lib.call, "vief_id_batched", ctypes.byref(d2), side.cuda_stream)
+    futs = []
     try:
-        _lib.call("vief_id_batched", ctypes.byref(d1), main.cuda_stream)
+        for d, st in zip(descs[1:], sides):
+            st.wait_stream(main)
+            futs.append(pool.submit(_lib.call, "vief_id_batched", ctypes.byref(d), st.cuda_stream))
+        _lib.call("vief_id_batched", ctypes.byref(descs[0]), main.cuda_stream)
     finally:
-        fut.result()
-        main.wait_stream(side)
+        for f in futs:
+            f.result()
+        for st in sides[:parts - 1]:
+            main.wait_stream(st)
 
 
 def compress_outer(spec, grid, tree, eps, opts, quad=PLAIN, spill=None):
@@ -542,7 +547,7 @@ def compress_levels(H):
     coarse); sharded objects (distributed.py) call this directly."""
     pad = H.opts.resolved_proxy_layers(H.spec)
     _mark("compress:start")
-    with _gc_paused():
+    with _host_quiet():
         for L in reversed(_real_levels(H)):
             _lib.prof_prefix(f"L{L.lv:02d}.")
             _compress_level(H, L, pad, H.opts.seed)
@@ -830,7 +835,7 @@ def invert_dense_block(H, spill=None, free_source=False):
     (solver_dense.py:332-368).  `free_source` drops D/B once consumed."""
     inv = DenseBlockInverse(H)
     _mark("invert:start")
-    with _gc_paused():
+    with _host_quiet():
         for L in reversed(_real_levels(H)):
             _lib.prof_prefix(f"L{L.lv:02d}.")
             _invert_level(inv, L)
@@ -848,23 +853,50 @@ _SIDE = {}
 _BLOCK_F = os.environ.get("VF_BLOCK_F", "1") != "0"
 
 
-_GC_PAUSE = os.environ.get("VF_GC_PAUSE", "1") != "0"
+_HOST_QUIET = os.environ.get("VF_HOST_QUIET", "1") != "0"
+_QUIET_DEPTH = [0]
+
+
+_TPC = [None, -1]
+
+
+def _threadpools():
+    """threadpoolctl controller of the loaded BLAS/OpenMP libraries (rebuilt
+    when modules were imported since: a fresh scan costs ~1 ms)."""
+    import sys
+    if _TPC[0] is None or _TPC[1] != len(sys.modules):
+        from threadpoolctl import ThreadpoolController
+        _TPC[0], _TPC[1] = ThreadpoolController(), len(sys.modules)
+    return _TPC[0]
 
 
 @contextlib.contextmanager
-def _gc_paused():
-    """Hold Python's cyclic garbage collector while the level loops enqueue
-    GPU work: a collection stops every thread at the GIL, the streams drain and
-    the GPU idles for its duration.  The loops create no reference cycles, so
-    nothing accumulates; collection resumes when they return."""
-    if not _GC_PAUSE or not gc.isenabled():
+def _host_quiet():
+    """Keep the host quiet while the level loops drive the GPU from several
+    threads (caller, ID slices, inversion worker), each of which waits on its
+    stream once per ID column block:
+      * host BLAS / OpenMP pools limited to one thread -- their idle workers
+        spin after every call and starved the stream-driving threads (measured
+        at 1024^2: random 100-480 ms stalls of a level, none with one thread);
+      * Python's cyclic GC held (a collection stops every thread at the GIL;
+        the loops create no reference cycles).
+    VF_HOST_QUIET=0 disables both."""
+    if not _HOST_QUIET or _QUIET_DEPTH[0] > 0:
         yield
         return
-    gc.disable()
+    gc_was = gc.isenabled()
+    nthr = torch.get_num_threads()
+    _QUIET_DEPTH[0] += 1
     try:
-        yield
+        with _threadpools().limit(limits=1):
+            torch.set_num_threads(1)
+            gc.disable()
+            yield
     finally:
-        gc.enable()
+        _QUIET_DEPTH[0] -= 1
+        torch.set_num_threads(nthr)
+        if gc_was:
+            gc.enable()
 
 
 def factor_solve(spec, grid, tree, eps, opts, f, quad=PLAIN):
@@ -873,7 +905,7 @@ def factor_solve(spec, grid, tree, eps, opts, f, quad=PLAIN):
     factorization of the coarser levels; the down sweep follows.  Returns
     (H, inv, x) with x = inv.apply(f) (bitwise: same kernels, same order per
     level)."""
-    with _gc_paused():
+    with _host_quiet():
         H, inv, (fd, single, phi, ups) = _factorize(spec, grid, tree, eps, opts, quad, rhs=f)
         out = torch.zeros_like(fd)
         _sweep_down(H, phi, ups, out)
@@ -881,7 +913,7 @@ def factor_solve(spec, grid, tree, eps, opts, f, quad=PLAIN):
 
 
 def factorize(spec, grid, tree, eps, opts, quad=PLAIN):
-    with _gc_paused():
+    with _host_quiet():
         H, inv, _ = _factorize(spec, grid, tree, eps, opts, quad)
     return H, inv
 
@@ -1165,7 +1197,7 @@ def _apply_device(inv, fd):
 
 def _apply(inv, f):
     H = inv.H
-    with _gc_paused():
+    with _host_quiet():
         fd, single = _as_device_rhs(f, H.grid.n, H.device, H.realified)
         return _from_device(_apply_device(inv, fd), f, single, H.realified)
 

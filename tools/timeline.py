@@ -33,6 +33,7 @@ def wrap(name):
 
 for nm in ["_compress_level_blocks", "_compress_level_id", "_invert_level_F", "_invert_level_rest"]:
     wrap(nm)
+reps = []
 for rep in range(int(os.environ.get("REPS", "3"))):
     rec.clear()
     torch.cuda.synchronize()
@@ -45,6 +46,7 @@ for rep in range(int(os.environ.get("REPS", "3"))):
     t1.record()
     torch.cuda.synchronize()
     print(f"rep {rep}: {t0.elapsed_time(t1):.1f} ms", flush=True)
+    reps.append({(name, lv): e0.elapsed_time(e1) for name, lv, e0, e1, h0, h1 in rec})
     del H, inv
 ms = torch.cuda.memory_stats()
 print(f"total {t0.elapsed_time(t1):.1f} ms; torch reserved {torch.cuda.memory_reserved() / 1e9:.1f} GB "
@@ -55,3 +57,11 @@ short = {"_compress_level_blocks": "blocks", "_compress_level_id": "ID", "_inver
 for name, lv, e0, e1, h0, h1 in rec:
     print(f"L{lv:02d} {short[name]:>6s}  gpu {t0.elapsed_time(e0):8.1f} -> {t0.elapsed_time(e1):8.1f}  ({e0.elapsed_time(e1):7.1f})"
           f"   host {(h0 - hs) * 1e3:8.1f} -> {(h1 - hs) * 1e3:8.1f}")
+
+# phases whose duration varies across the warm reps (> 20 ms spread)
+if len(reps) > 2:
+    print("unstable phases (gpu ms per rep 1..):")
+    for key in reps[1]:
+        vals = [r.get(key, 0.0) for r in reps[1:]]
+        if max(vals) - min(vals) > 20.0:
+            print(f"  L{key[1]:02d} {key[0]:>24s} " + " ".join(f"{v:7.1f}" for v in vals))
