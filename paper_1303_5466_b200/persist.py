@@ -1,0 +1,278 @@
+"""Factor persistence: save a factorization once, solve with it in later runs
+(SURVEY.md §8(f) row 4).
+
+The reference has two related mechanisms: `_Spill` (solver_dense.py:37-55)
+backs large blocks by `.npy` memmaps in a temporary directory, and the 1-D HSS
+debug blob `to_blob`/`from_blob` (hss1d/ops.py:218-267) writes a JSON
+structure header plus the blocks.  Here the factors live in HBM as per-level
+batches, so the file is a dump of those batches, not of per-box blocks:
+
+    [0:8)    magic  b"VIEFB200"
+    [8:16)   u64 little-endian length of the JSON header
+    [16:..)  JSON header, then zero padding to a 4096-byte boundary
+    ...      storages, each starting on a 4096-byte boundary
+
+The header records the problem (spec, quadrature rule, options, eps, grid side,
+leaf size, level slices -- pickled, base64), every storage (file offset, byte
+count, whether it lives on the device) and, per tree level, every attribute
+of the level's state: tensors and numpy arrays as (storage, offset, shape,
+stride, dtype) views -- aliasing between tensors (the root's block-form factors
+are views of level buffers) is preserved exactly -- and plain scalars/tuples
+as JSON.  Device storages stream through one pinned staging buffer in
+`_CHUNK`-byte pieces, so saving/loading the ~50 GB 1024^2 factorization needs
+no host copy of the whole thing.
+
+Loading rebuilds the host objects (grid, tree, assembler) from the problem
+description and uploads the storages; `load(...).apply(f)` is bitwise
+identical to the saved object's `apply(f)` (tests).  The header's pickle is
+trusted input: load only files you wrote.
+"""
+
+import base64
+import json
+import os
+import pickle
+import struct
+
+import numpy as np
+import torch
+
+from . import _lib
+
+MAGIC = b"VIEFB200"
+VERSION = 1
+_ALIGN = 4096
+_CHUNK = 256 << 20
+
+_DT = {torch.float64: "float64", torch.float32: "float32", torch.int64: "int64",
+       torch.int32: "int32", torch.int16: "int16", torch.int8: "int8",
+       torch.uint8: "uint8", torch.bool: "bool", torch.complex128: "complex128"}
+_TD = {v: k for k, v in _DT.items()}
+
+
+def _align(x):
+    return (x + _ALIGN - 1) // _ALIGN * _ALIGN
+
+
+class _Writer:
+    """Collects the storages behind every tensor / array of the state."""
+
+    def __init__(self):
+        self.storages = []      # (kind, object) in file order
+        self._seen = {}
+
+    def _sid(self, key, kind, obj):
+        sid = self._seen.get(key)
+        if sid is None:
+            sid = self._seen[key] = len(self.storages)
+            self.storages.append((kind, obj))
+        return sid
+
+    def encode(self, v):
+        if v is None or isinstance(v, (bool, int, float, str)):
+            return {"t": "py", "v": v}
+        if isinstance(v, (np.integer, np.floating, np.bool_)):
+            return {"t": "py", "v": v.item()}
+        if isinstance(v, torch.Tensor):
+            st = v.untyped_storage()
+            sid = self._sid(("t", st.data_ptr(), st.device.type), "dev" if v.is_cuda else "host",
+                            st)
+            return {"t": "tensor", "s": sid, "o": v.storage_offset(), "shape": list(v.shape),
+                    "stride": list(v.stride()), "dtype": _DT[v.dtype]}
+        if isinstance(v, np.ndarray):
+            a = np.ascontiguousarray(v)
+            sid = self._sid(("n", id(v)), "nd", a)
+            return {"t": "nd", "s": sid, "shape": list(a.shape), "dtype": a.dtype.str}
+        if isinstance(v, (tuple, list)):
+            return {"t": "tuple" if isinstance(v, tuple) else "list",
+                    "v": [self.encode(x) for x in v]}
+        raise TypeError(f"cannot persist a {type(v).__name__}")
+
+
+def _level_state(L):
+    # attributes starting with "_" are caches rebuilt on demand
+    return {k: v for k, v in vars(L).items() if not k.startswith("_")}
+
+
+def _nbytes(kind, obj):
+    return obj.nbytes() if kind in ("dev", "host") else obj.nbytes
+
+
+def _write_storage(f, kind, obj, stage):
+    if kind == "nd":
+        f.write(memoryview(obj).cast("B"))
+        return
+    src = torch.empty(0, dtype=torch.uint8, device=obj.device).set_(obj)
+    n = src.numel()
+    if kind == "host":
+        f.write(src.numpy().data)
+        return
+    for lo in range(0, n, _CHUNK):
+        hi = min(n, lo + _CHUNK)
+        stage[:hi - lo].copy_(src[lo:hi])        # device -> pinned (synchronous)
+        f.write(stage[:hi - lo].numpy().data)
+
+
+def write_state(path, problem, kind, levels):
+    """Write `levels` (list of per-level attribute dicts or None) and the
+    picklable `problem` description to `path`."""
+    w = _Writer()
+    enc_levels = [None if st is None else {k: w.encode(v) for k, v in st.items()}
+                  for st in levels]
+    sizes = [_nbytes(k, o) for k, o in w.storages]
+    header = {"version": VERSION, "kind": kind,
+              "problem": base64.b64encode(pickle.dumps(problem)).decode(),
+              "levels": enc_levels, "storages": []}
+    # offsets depend on the header length; iterate until it is stable
+    hlen = 0
+    while True:
+        off = _align(16 + hlen)
+        header["storages"] = []
+        for (k, _), nb in zip(w.storages, sizes):
+            header["storages"].append({"offset": off, "nbytes": nb, "device": k == "dev"})
+            off = _align(off + nb)
+        blob = json.dumps(header).encode()
+        if len(blob) == hlen:
+            break
+        hlen = len(blob)
+    need_stage = any(k == "dev" for k, _ in w.storages)
+    stage = torch.empty(min(_CHUNK, max(sizes + [1])), dtype=torch.uint8,
+                        pin_memory=True) if need_stage else None
+    if need_stage:
+        torch.cuda.synchronize()
+    tmp = f"{path}.tmp{os.getpid()}"
+    with open(tmp, "wb") as f:
+        f.write(MAGIC)
+        f.write(struct.pack("<Q", hlen))
+        f.write(blob)
+        for (k, o), s in zip(w.storages, header["storages"]):
+            f.seek(s["offset"])
+            _write_storage(f, k, o, stage)
+        f.truncate(_align(f.tell()))
+    os.replace(tmp, path)
+
+
+def read_header(path):
+    with open(path, "rb") as f:
+        if f.read(8) != MAGIC:
+            raise ValueError(f"{path}: not a vief_b200 factor file")
+        (hlen,) = struct.unpack("<Q", f.read(8))
+        header = json.loads(f.read(hlen).decode())
+    if header.get("version") != VERSION:
+        raise ValueError(f"{path}: factor file version {header.get('version')}, "
+                         f"this build reads {VERSION}")
+    return header
+
+
+def read_state(path, device):
+    """-> (kind, problem, levels) with device storages uploaded to `device`."""
+    header = read_header(path)
+    device = torch.device(device)
+    stor = []
+    with open(path, "rb") as f:
+        dev_sizes = [s["nbytes"] for s in header["storages"] if s["device"]]
+        stage = None
+        if dev_sizes and device.type == "cuda":
+            stage = torch.empty(min(_CHUNK, max(dev_sizes)), dtype=torch.uint8, pin_memory=True)
+        for s in header["storages"]:
+            f.seek(s["offset"])
+            nb = s["nbytes"]
+            if s["device"]:
+                buf = torch.empty(nb, dtype=torch.uint8, device=device)
+                if stage is None:
+                    f.readinto(buf.numpy().data)
+                else:
+                    for lo in range(0, nb, _CHUNK):
+                        hi = min(nb, lo + _CHUNK)
+                        f.readinto(stage[:hi - lo].numpy().data)
+                        buf[lo:hi].copy_(stage[:hi - lo])      # pinned -> device (synchronous)
+            else:
+                buf = np.empty(nb, dtype=np.uint8)
+                f.readinto(buf.data)
+            stor.append(buf)
+
+    def decode(e):
+        t = e["t"]
+        if t == "py":
+            return e["v"]
+        if t in ("tuple", "list"):
+            v = [decode(x) for x in e["v"]]
+            return tuple(v) if t == "tuple" else v
+        if t == "nd":
+            return stor[e["s"]].view(np.dtype(e["dtype"])).reshape(e["shape"])
+        if t == "tensor":
+            base = stor[e["s"]]
+            if isinstance(base, np.ndarray):
+                base = torch.from_numpy(base)
+            typed = base.view(_TD[e["dtype"]])
+            return torch.as_strided(typed, e["shape"], e["stride"], e["o"])
+        raise ValueError(f"bad entry type {t!r}")
+
+    levels = [None if st is None else {k: decode(v) for k, v in st.items()}
+              for st in header["levels"]]
+    return header["kind"], pickle.loads(base64.b64decode(header["problem"])), levels
+
+
+# ---------------------------------------------------------------------------
+# solver objects
+
+def _problem_of(H):
+    sl = None
+    if H.sharded:
+        sl = {L.lv: tuple(int(x) for x in L.sl) for L in H.levels if L is not None}
+    return {"spec": H.spec, "quad": H.quad, "opts": H.opts, "eps": H.eps,
+            "n_side": H.grid.n_side, "n_max": H.tree.n_max, "level_slices": sl}
+
+
+def save(obj, path):
+    """Write an `Hss2dMatrix`, a `DenseBlockInverse` or a `CompressedInverse`
+    (k_cut=None) to `path`.  The factors stay where they are (HBM)."""
+    from .solver_compressed import CompressedInverse
+    from .solver_dense import DenseBlockInverse, Hss2dMatrix
+    if isinstance(obj, CompressedInverse):
+        kind, H = "CompressedInverse", obj.dense_matvec_source
+    elif isinstance(obj, DenseBlockInverse):
+        kind, H = "DenseBlockInverse", obj.H
+    elif isinstance(obj, Hss2dMatrix):
+        kind, H = "Hss2dMatrix", obj
+    else:
+        raise TypeError(f"cannot save a {type(obj).__name__}")
+    torch.cuda.synchronize(H.device)
+    problem = _problem_of(H)
+    if kind == "CompressedInverse":
+        problem["ti_mode"] = obj.ti_mode
+    write_state(path, problem, kind,
+                [None if L is None else _level_state(L) for L in H.levels])
+
+
+def load(path, device=None):
+    """Read a file written by `save`; returns an object of the saved type with
+    its factors resident on `device` (default: the current CUDA device)."""
+    from .kernels import Grid
+    from .solver_compressed import CompressedInverse
+    from .solver_dense import DenseBlockInverse, Hss2dMatrix
+    from .tree import build_tree
+    _lib.require_cuda()
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    kind, pb, levels = read_state(path, device)
+    grid = Grid(pb["n_side"])
+    tree = build_tree(grid, pb["n_max"])
+    with torch.cuda.device(device):
+        H = Hss2dMatrix(pb["spec"], grid, tree, pb["eps"], pb["opts"], pb["quad"],
+                        level_slices=pb["level_slices"])
+    for L, st in zip(H.levels, levels):
+        if (L is None) != (st is None):
+            raise ValueError(f"{path}: level layout does not match the rebuilt tree")
+        if L is not None:
+            for k, v in st.items():
+                setattr(L, k, v)
+    if kind == "Hss2dMatrix":
+        return H
+    inv = DenseBlockInverse(H)
+    if kind == "DenseBlockInverse":
+        return inv
+    ci = CompressedInverse(pb["spec"], grid, tree, pb["eps"], pb["opts"], pb["quad"],
+                           pb.get("ti_mode", False))
+    ci.dense_delegate, ci.dense_matvec_source = inv, H
+    return ci

@@ -29,6 +29,17 @@ class CompressedInverse:
     def apply(self, f):
         return self.dense_delegate.apply(f)
 
+    def save(self, path):
+        """Write the factors to `path` (persist.py): factor once, solve in
+        later runs."""
+        from . import persist
+        persist.save(self, path)
+
+    @staticmethod
+    def load(path, device=None):
+        from . import persist
+        return persist.load(path, device)
+
 
 def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti_mode=False,
                      support_mask=None):

@@ -323,6 +323,16 @@ class Hss2dMatrix:
     def matvec(self, x):
         return _matvec(self, x)
 
+    def save(self, path):
+        """Write the compression to `path` (persist.py)."""
+        from . import persist
+        persist.save(self, path)
+
+    @staticmethod
+    def load(path, device=None):
+        from . import persist
+        return persist.load(path, device)
+
     def densify(self):
         """Dense reconstruction (tests, small N)."""
         n = self.grid.n
@@ -828,6 +838,16 @@ class DenseBlockInverse:
 
     def apply(self, f):
         return _apply(self, f)
+
+    def save(self, path):
+        """Write the factors to `path` (persist.py); `load` restores them."""
+        from . import persist
+        persist.save(self, path)
+
+    @staticmethod
+    def load(path, device=None):
+        from . import persist
+        return persist.load(path, device)
 
 
 def invert_dense_block(H, spill=None, free_source=False):

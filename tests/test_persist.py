@@ -1,0 +1,123 @@
+"""Factor persistence (persist.py, the analogue of the
+reference's _Spill memmaps solver_dense.py:37-55 and hss1d to_blob/from_blob
+hss1d/ops.py:218-267).  CPU tests cover the file format with host tensors;
+GPU tests check that a loaded factorization solves bitwise like the saved one."""
+import numpy as np
+import pytest
+import torch
+
+from paper_1303_5466_b200 import persist
+
+
+def _roundtrip(tmp_path, levels, problem=None):
+    path = str(tmp_path / "f.vief")
+    persist.write_state(path, problem or {"x": 1}, "test", levels)
+    return persist.read_state(path, "cpu")
+
+
+def test_format_roundtrip_cpu(tmp_path):
+    base = torch.randn(5, 7, 3, dtype=torch.float64)
+    view = base[2]                                  # aliases base
+    strided = base[:, 1:, 0].t()                    # non-contiguous view
+    ints = torch.arange(11, dtype=torch.int32)
+    arr = np.arange(12, dtype=np.int64).reshape(3, 4)
+    levels = [None,
+              {"B": base, "root": (view, 3, 4.5, strided), "k": arr, "leaf": True,
+               "ids": ints, "kmax": np.int64(9), "none": None},
+              {"lst": [1, 2, "a"], "f": np.float64(0.25)}]
+    kind, pb, out = _roundtrip(tmp_path, levels, {"n_side": 8, "eps": 1e-10})
+    assert kind == "test" and pb == {"n_side": 8, "eps": 1e-10}
+    assert out[0] is None
+    L = out[1]
+    assert torch.equal(L["B"], base)
+    v, a, b, s = L["root"]
+    assert torch.equal(v, view) and (a, b) == (3, 4.5) and torch.equal(s, strided)
+    assert s.stride() == strided.stride()
+    # aliasing is preserved: the view shares the loaded base's storage
+    assert v.untyped_storage().data_ptr() == L["B"].untyped_storage().data_ptr()
+    v.fill_(7.0)
+    assert torch.all(L["B"][2] == 7.0)
+    assert np.array_equal(L["k"], arr) and L["k"].dtype == np.int64
+    assert torch.equal(L["ids"], ints) and L["leaf"] is True and L["none"] is None
+    assert L["kmax"] == 9
+    assert out[2] == {"lst": [1, 2, "a"], "f": 0.25}
+
+
+def test_format_alignment_and_magic(tmp_path):
+    path = str(tmp_path / "f.vief")
+    persist.write_state(path, {}, "test", [{"a": torch.ones(3, dtype=torch.float64),
+                                            "b": np.zeros(5, dtype=np.int32)}])
+    h = persist.read_header(path)
+    assert [s["offset"] % 4096 for s in h["storages"]] == [0, 0]
+    assert [s["nbytes"] for s in h["storages"]] == [24, 20]
+    with open(path, "r+b") as f:
+        f.write(b"XXXXXXXX")
+    with pytest.raises(ValueError):
+        persist.read_header(path)
+
+
+def test_format_rejects_unknown_types(tmp_path):
+    with pytest.raises(TypeError):
+        persist.write_state(str(tmp_path / "f"), {}, "test", [{"a": object()}])
+
+
+# ---------------------------------------------------------------------------
+
+def _problem(n_side, complex_=False):
+    import paper_1303_5466_b200 as P
+    if complex_:
+        spec = P.KernelSpec("helmholtz2d", k=6.0, b_field=P.make_field("gaussian_bump"))
+    else:
+        spec = P.KernelSpec("laplace2d", b_field=P.make_field("gaussian_bump"))
+    grid = P.Grid(n_side)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=None)
+    return spec, grid, opts
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("complex_", [False, True])
+def test_inverse_save_load_bitwise(tmp_path, complex_):
+    from paper_1303_5466_b200 import solver_compressed as sc
+    from paper_1303_5466_b200.solver_compressed import CompressedInverse
+    spec, grid, opts = _problem(64 if not complex_ else 32, complex_)
+    inv = sc.compress_inverse(spec, grid, eps=1e-10, opts=opts)
+    rng = np.random.default_rng(3)
+    f = rng.standard_normal((grid.n, 3))
+    if complex_:
+        f = f + 1j * rng.standard_normal((grid.n, 3))
+    x0 = inv.apply(f)
+    path = str(tmp_path / "inv.vief")
+    inv.save(path)
+    inv2 = CompressedInverse.load(path)
+    assert isinstance(inv2, CompressedInverse)
+    x1 = inv2.apply(f)
+    assert x1.dtype == x0.dtype and np.array_equal(x0, x1)
+    assert inv2.nbytes() == inv.nbytes()
+    H0, H1 = inv.dense_matvec_source, inv2.dense_matvec_source
+    for i in list(H0.row_skel)[:20]:
+        assert np.array_equal(H0.row_skel[i], H1.row_skel[i])
+    assert np.array_equal(H0.matvec(f), H1.matvec(f))
+    assert np.array_equal(inv.apply(f[:, 0]), inv2.apply(f[:, 0]))
+
+
+@pytest.mark.gpu
+def test_dense_inverse_and_matrix_save_load(tmp_path):
+    from paper_1303_5466_b200 import solver_dense as sd
+    import paper_1303_5466_b200 as P
+    spec, grid, opts = _problem(64)
+    tree = P.build_tree(grid, 64)
+    H = sd.compress_outer(spec, grid, tree, 1e-10, opts)
+    pH = str(tmp_path / "H.vief")
+    H.save(pH)
+    inv = sd.invert_dense_block(H)
+    pI = str(tmp_path / "inv.vief")
+    inv.save(pI)
+    H2 = sd.Hss2dMatrix.load(pH)
+    inv2 = sd.DenseBlockInverse.load(pI)
+    x = np.random.default_rng(0).standard_normal(grid.n)
+    assert np.array_equal(H.matvec(x), H2.matvec(x))
+    assert np.array_equal(inv.apply(x), inv2.apply(x))
+    assert H2.nbytes() == H.nbytes()
+    for i in list(inv.E)[:10]:
+        assert np.array_equal(inv.E[i], inv2.E[i])
+    assert np.array_equal(inv.Finv[0], inv2.Finv[0])
