@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 #include "common.cuh"
@@ -110,8 +111,11 @@ __global__ void k_pad_identity(double* A, long long sA, int lda, const int* nb, 
 static bool g_prof = false;
 static std::map<std::string, std::pair<double, long long>> g_prof_acc;
 struct ProfEv { std::string name; cudaEvent_t e0, e1; };
-static std::vector<ProfEv> g_prof_pending;
-static int g_prof_open = -1;
+// per host thread: the ID slices and the inversion worker profile their own
+// streams; the accumulated totals are shared
+static thread_local std::vector<ProfEv> g_prof_pending;
+static thread_local int g_prof_open = -1;
+static std::mutex g_prof_mu;
 
 bool prof_on() { return g_prof; }
 static std::string g_prof_prefix;
@@ -121,7 +125,12 @@ void prof_push(cudaStream_t st, const char* name) {
   cudaEventCreate(&e);
   cudaEventRecord(e, st);
   if (g_prof_open >= 0) g_prof_pending[g_prof_open].e1 = e;
-  ProfEv pe{g_prof_prefix + name, e, nullptr};
+  std::string pre;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    pre = g_prof_prefix;
+  }
+  ProfEv pe{pre + name, e, nullptr};
   cudaEvent_t e2;
   cudaEventCreate(&e2);
   cudaEventRecord(e2, st);
@@ -138,6 +147,7 @@ void prof_flush(cudaStream_t st) {
     g_prof_pending[g_prof_open].e1 = e;
   }
   cudaStreamSynchronize(st);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   for (auto& pe : g_prof_pending) {
     float ms = 0.f;
     if (pe.e1) cudaEventElapsedTime(&ms, pe.e0, pe.e1);
@@ -155,7 +165,10 @@ void prof_flush(cudaStream_t st) {
 
 using namespace vf;
 
-extern "C" void vief_prof_prefix(const char* p) { g_prof_prefix = p ? p : ""; }
+extern "C" void vief_prof_prefix(const char* p) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_prefix = p ? p : "";
+}
 extern "C" void vief_prof_enable(int on) {
   g_prof = on != 0;
   g_prof_acc.clear();

@@ -18,9 +18,10 @@ count, whether it lives on the device) and, per tree level, every attribute
 of the level's state: tensors and numpy arrays as (storage, offset, shape,
 stride, dtype) views -- aliasing between tensors (the root's block-form factors
 are views of level buffers) is preserved exactly -- and plain scalars/tuples
-as JSON.  Device storages stream through one pinned staging buffer in
-`_CHUNK`-byte pieces, so saving/loading the ~50 GB 1024^2 factorization needs
-no host copy of the whole thing.
+as JSON.  Device storages stream through two pinned staging buffers in
+`_CHUNK`-byte pieces (the copy of one overlaps the file I/O of the other), so
+saving/loading the ~50 GB 1024^2 factorization needs no host copy of the
+whole thing.
 
 Loading rebuilds the host objects (grid, tree, assembler) from the problem
 description and uploads the storages; `load(...).apply(f)` is bitwise
@@ -98,19 +99,65 @@ def _nbytes(kind, obj):
     return obj.nbytes() if kind in ("dev", "host") else obj.nbytes
 
 
+class _Stager:
+    """Two pinned staging buffers on a private stream: the device<->host copy
+    of one chunk overlaps the file I/O of the other."""
+
+    def __init__(self, nbytes):
+        n = min(_CHUNK, max(nbytes, 1))
+        self.buf = [torch.empty(n, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        self.ev = [torch.cuda.Event(), torch.cuda.Event()]
+        self.stream = torch.cuda.Stream()
+        self.busy = [False, False]
+
+    def write(self, f, src):
+        """src: uint8 CUDA tensor -> file, chunk by chunk."""
+        n = src.numel()
+        chunks = [(lo, min(n, lo + _CHUNK)) for lo in range(0, n, _CHUNK)]
+
+        def issue(c):
+            lo, hi = chunks[c]
+            with torch.cuda.stream(self.stream):
+                self.buf[c % 2][:hi - lo].copy_(src[lo:hi], non_blocking=True)
+                self.ev[c % 2].record(self.stream)
+
+        self.stream.wait_stream(torch.cuda.current_stream())
+        if chunks:
+            issue(0)
+        for c, (lo, hi) in enumerate(chunks):
+            if c + 1 < len(chunks):
+                issue(c + 1)
+            self.ev[c % 2].synchronize()
+            f.write(self.buf[c % 2][:hi - lo].numpy().data)
+
+    def read(self, f, dst):
+        """file -> dst (uint8 CUDA tensor), chunk by chunk."""
+        n = dst.numel()
+        for c, lo in enumerate(range(0, n, _CHUNK)):
+            hi = min(n, lo + _CHUNK)
+            i = c % 2
+            if self.busy[i]:
+                self.ev[i].synchronize()          # the buffer's previous upload is done
+            f.readinto(self.buf[i][:hi - lo].numpy().data)
+            with torch.cuda.stream(self.stream):
+                dst[lo:hi].copy_(self.buf[i][:hi - lo], non_blocking=True)
+                self.ev[i].record(self.stream)
+            self.busy[i] = True
+
+    def finish(self):
+        self.stream.synchronize()
+        self.busy = [False, False]
+
+
 def _write_storage(f, kind, obj, stage):
     if kind == "nd":
         f.write(memoryview(obj).cast("B"))
         return
     src = torch.empty(0, dtype=torch.uint8, device=obj.device).set_(obj)
-    n = src.numel()
     if kind == "host":
         f.write(src.numpy().data)
         return
-    for lo in range(0, n, _CHUNK):
-        hi = min(n, lo + _CHUNK)
-        stage[:hi - lo].copy_(src[lo:hi])        # device -> pinned (synchronous)
-        f.write(stage[:hi - lo].numpy().data)
+    stage.write(f, src)
 
 
 def write_state(path, problem, kind, levels):
@@ -136,8 +183,7 @@ def write_state(path, problem, kind, levels):
             break
         hlen = len(blob)
     need_stage = any(k == "dev" for k, _ in w.storages)
-    stage = torch.empty(min(_CHUNK, max(sizes + [1])), dtype=torch.uint8,
-                        pin_memory=True) if need_stage else None
+    stage = _Stager(max(sizes + [1])) if need_stage else None
     if need_stage:
         torch.cuda.synchronize()
     tmp = f"{path}.tmp{os.getpid()}"
@@ -173,7 +219,8 @@ def read_state(path, device):
         dev_sizes = [s["nbytes"] for s in header["storages"] if s["device"]]
         stage = None
         if dev_sizes and device.type == "cuda":
-            stage = torch.empty(min(_CHUNK, max(dev_sizes)), dtype=torch.uint8, pin_memory=True)
+            with torch.cuda.device(device):
+                stage = _Stager(max(dev_sizes))
         for s in header["storages"]:
             f.seek(s["offset"])
             nb = s["nbytes"]
@@ -182,14 +229,13 @@ def read_state(path, device):
                 if stage is None:
                     f.readinto(buf.numpy().data)
                 else:
-                    for lo in range(0, nb, _CHUNK):
-                        hi = min(nb, lo + _CHUNK)
-                        f.readinto(stage[:hi - lo].numpy().data)
-                        buf[lo:hi].copy_(stage[:hi - lo])      # pinned -> device (synchronous)
+                    stage.read(f, buf)
             else:
                 buf = np.empty(nb, dtype=np.uint8)
                 f.readinto(buf.data)
             stor.append(buf)
+        if stage is not None:
+            stage.finish()
 
     def decode(e):
         t = e["t"]
