@@ -160,6 +160,158 @@ __global__ void __launch_bounds__(QS_THREADS) k_qrcp_smem(
   }
 }
 
+// Same factorization (dlaqp2 semantics) with two CTA barriers per column
+// instead of ~10: warp 0 alone does the pivot swap and the reflector
+// (p <= ~200 rows: a warp reduction, no block reduction), then every warp
+// applies the reflector to its own columns four at a time (four independent
+// dot-product chains and reductions in flight instead of one) and downdates
+// those columns' norms itself (it holds the new R(i, j)), leaving a per-warp
+// first-maximum for the next pivot.
+constexpr int QS_CH = 4;
+__global__ void __launch_bounds__(QS_THREADS) k_qrcp_smem2(
+    const double* A, long long sA, int lda, const int* pv, const int* mv, int* perm, int ldperm,
+    double* Rm, long long sR, int ldR, double* diag, int lddiag, double* colmax) {
+  extern __shared__ double sm[];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = QS_THREADS / 32;
+  const int p = pv[b], m = mv[b];
+  const int ld = p | 1;
+  double* a = sm;
+  double* vn1 = a + (long long)ld * m;
+  double* vn2 = vn1 + m;
+  __shared__ double redv[nw];
+  __shared__ int redi[nw];
+  __shared__ double s_tau;
+  int* pm = perm + b * ldperm;
+  const double* Ab = A + b * sA;
+  for (int idx = tid; idx < p * m; idx += QS_THREADS) {
+    int i = idx % p, j = idx / p;
+    a[j * ld + i] = Ab[(long long)j * lda + i];
+  }
+  for (int j = tid; j < m; j += QS_THREADS) pm[j] = j;
+  __syncthreads();
+  {
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int j = warp; j < m; j += nw) {
+      double s = 0.0;
+      for (int i = lane; i < p; i += 32) s = fma(a[j * ld + i], a[j * ld + i], s);
+      s = sqrt(warp_sum(s));
+      if (lane == 0) { vn1[j] = s; vn2[j] = s; }
+      if (s > bv) { bv = s; bi = j; }
+    }
+    if (lane == 0) { redv[warp] = bv; redi[warp] = bi; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int w = 0; w < nw; ++w) mx = fmax(mx, redv[w]);
+    colmax[b] = mx;
+  }
+  const int kmax = min(p, m);
+  const double tol3z = sqrt(2.220446049250313e-16);
+  double* Rb = Rm + b * sR;
+  double* db = diag + b * lddiag;
+  for (int i = 0; i < kmax; ++i) {
+    if (warp == 0) {
+      // pivot: first maximum over the per-warp candidates of vn1[i:m]
+      double bv = redv[0];
+      int pvt = redi[0];
+      for (int w = 1; w < nw; ++w)
+        if (redv[w] > bv || (redv[w] == bv && redi[w] < pvt)) { bv = redv[w]; pvt = redi[w]; }
+      if (pvt != i && pvt < m) {
+        for (int r = lane; r < p; r += 32) {
+          double t = a[pvt * ld + r]; a[pvt * ld + r] = a[i * ld + r]; a[i * ld + r] = t;
+        }
+        if (lane == 0) {
+          int t = pm[pvt]; pm[pvt] = pm[i]; pm[i] = t;
+          vn1[pvt] = vn1[i]; vn2[pvt] = vn2[i];
+        }
+      }
+      __syncwarp();
+      // dlarfg on a(i:p, i)
+      double s = 0.0;
+      for (int r = i + 1 + lane; r < p; r += 32) s = fma(a[i * ld + r], a[i * ld + r], s);
+      s = warp_sum(s);
+      const double alpha = a[i * ld + i];
+      double tau = 0.0, beta = alpha;
+      if (s != 0.0) {
+        beta = -copysign(hypot(alpha, sqrt(s)), alpha);
+        tau = (beta - alpha) / beta;
+        const double sc = 1.0 / (alpha - beta);
+        for (int r = i + 1 + lane; r < p; r += 32) a[i * ld + r] *= sc;
+      }
+      if (lane == 0) { a[i * ld + i] = beta; db[i] = fabs(beta); s_tau = tau; }
+    }
+    __syncthreads();
+    const double tau = s_tau;
+    const double* v = a + i * ld;  // v(0) = 1 implicit (a(i,i) holds beta)
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int j0 = i + 1 + warp; j0 < m; j0 += nw * QS_CH) {
+      int jc[QS_CH];
+      bool ok[QS_CH];
+#pragma unroll
+      for (int c = 0; c < QS_CH; ++c) { jc[c] = j0 + c * nw; ok[c] = jc[c] < m; }
+      if (tau != 0.0) {
+        double w[QS_CH];
+#pragma unroll
+        for (int c = 0; c < QS_CH; ++c) w[c] = 0.0;
+        for (int r = i + lane; r < p; r += 32) {
+          const double vr = (r == i) ? 1.0 : v[r];
+#pragma unroll
+          for (int c = 0; c < QS_CH; ++c)
+            if (ok[c]) w[c] = fma(vr, a[jc[c] * ld + r], w[c]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int c = 0; c < QS_CH; ++c) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+#pragma unroll
+        for (int c = 0; c < QS_CH; ++c) w[c] *= tau;
+        for (int r = i + lane; r < p; r += 32) {
+          const double vr = (r == i) ? 1.0 : v[r];
+#pragma unroll
+          for (int c = 0; c < QS_CH; ++c)
+            if (ok[c]) a[jc[c] * ld + r] = fma(-w[c], vr, a[jc[c] * ld + r]);
+        }
+        __syncwarp();
+      }
+      // partial column norm update (dlaqp2) of this warp's columns
+#pragma unroll
+      for (int c = 0; c < QS_CH; ++c) {
+        if (!ok[c]) continue;
+        const int j = jc[c];
+        const double nv1 = vn1[j];
+        double nv = nv1;
+        if (nv1 != 0.0) {
+          const double t = fabs(a[j * ld + i]) / nv1;
+          const double temp = fmax(1.0 - t * t, 0.0);
+          const double rr = nv1 / vn2[j];
+          if (temp * rr * rr <= tol3z) {
+            double ss = 0.0;
+            for (int r = i + 1 + lane; r < p; r += 32) ss = fma(a[j * ld + r], a[j * ld + r], ss);
+            nv = sqrt(warp_sum(ss));
+            if (lane == 0) vn2[j] = nv;
+          } else {
+            nv = nv1 * sqrt(temp);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) vn1[j] = nv;
+        if (nv > bv || (nv == bv && j < bi)) { bv = nv; bi = j; }
+      }
+    }
+    if (lane == 0) { redv[warp] = bv; redi[warp] = bi; }
+    __syncthreads();
+  }
+  for (int i = kmax + tid; i < m; i += QS_THREADS) db[i] = 0.0;
+  for (int idx = tid; idx < kmax * m; idx += QS_THREADS) {
+    int i = idx % kmax, j = idx / kmax;
+    Rb[(long long)j * ldR + i] = (i <= j) ? a[j * ld + i] : 0.0;
+  }
+}
+
 // rank of small-path items: reference rule on |R_jj| (dense_core.py:81-89)
 __global__ void k_rank_small(const double* diag, int lddiag, const int* pv, const int* mv,
                              int count, double eps, int* kout) {
@@ -724,10 +876,12 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   if (small) {
     prof_push(st, "id.small_qrcp");
     double* diag = buf.get<double>((size_t)maxm * count);
-    VF_CUDA(cudaFuncSetAttribute(k_qrcp_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem_small));
-    k_qrcp_smem<<<count, QS_THREADS, smem_small, st>>>(d->A, d->sA, d->lda, d->p, d->m, d->perm,
-                                                       maxm, Rm, sR, ldR, diag, maxm, colmax);
+    static int old_kernel = -1;  // VF_QRCP_OLD=1: the previous one-warp-per-column kernel (A/B)
+    if (old_kernel < 0) { const char* e = getenv("VF_QRCP_OLD"); old_kernel = e && e[0] == '1'; }
+    auto fn = old_kernel ? k_qrcp_smem : k_qrcp_smem2;
+    VF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small));
+    fn<<<count, QS_THREADS, smem_small, st>>>(d->A, d->sA, d->lda, d->p, d->m, d->perm, maxm, Rm,
+                                              sR, ldR, diag, maxm, colmax);
     k_rank_small<<<cdiv(count, 128), 128, 0, st>>>(diag, maxm, d->p, d->m, count, d->eps, kdev);
     k_group_max<<<cdiv(count / d->group, 128), 128, 0, st>>>(kdev, count, d->group);
     g_launches += 3;
