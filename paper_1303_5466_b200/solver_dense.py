@@ -1068,32 +1068,49 @@ def _factorize_levels(H, inv, pad, main, side, third=None, solve=None):
 # ---------------------------------------------------------------------------
 # solve sweeps
 
+class _Split:
+    """Layout marker: a complex right-hand side of a real system, solved as
+    its real and imaginary parts stacked as 2r real right-hand sides."""
+
+    def __init__(self, single, r):
+        self.single, self.r = single, r
+
+
 def _as_device_rhs(x, n, device, realified=False):
     """(N,) or (N, r) numpy/torch -> ((r, N') float64 device tensor, single).
-    Realified (complex) systems interleave (Re, Im) per point: N' = 2N."""
+    Realified (complex) systems interleave (Re, Im) per point: N' = 2N.  The
+    result dtype follows np.result_type(spec.dtype, f.dtype) as in the
+    reference (solver_dense.py:296): a complex f on a real system is solved
+    as Re and Im (2r real columns) and returned complex."""
     if isinstance(x, torch.Tensor):
-        if x.is_complex() and not realified:
-            raise TypeError("complex right-hand side for a real system")
-        t = x.to(device=device, dtype=torch.complex128 if realified else _F64)
+        cplx = x.is_complex()
+        t = x.to(device=device, dtype=torch.complex128 if (realified or cplx) else _F64)
     else:
         arr = np.asarray(x)
-        if np.iscomplexobj(arr) and not realified:
-            raise TypeError("complex right-hand side for a real system")
-        dt = np.complex128 if realified else np.float64
+        cplx = np.iscomplexobj(arr)
+        dt = np.complex128 if (realified or cplx) else np.float64
         t = torch.from_numpy(np.ascontiguousarray(arr, dtype=dt)).to(device)
     single = t.dim() == 1
     t2 = t[:, None] if single else t
-    if t2.shape[0] != n:
-        raise ValueError(f"rhs has {t2.shape[0]} rows, expected {n}")
+    if t2.dim() != 2 or t2.shape[0] != n:
+        raise ValueError(f"rhs has shape {tuple(t.shape)}, expected ({n},) or ({n}, nrhs)")
     tt = t2.t().contiguous()
     if realified:
         tt = torch.view_as_real(tt).reshape(tt.shape[0], 2 * n)
+    elif cplx:
+        r = tt.shape[0]
+        tt = torch.cat([tt.real, tt.imag], dim=0).contiguous()
+        return tt, _Split(single, r)
     return tt, single
 
 
 def _from_device(out, like, single, realified):
     """(r, N') device result -> the caller's layout/type (solver_dense.py:296-329)."""
-    if realified:
+    if isinstance(single, _Split):
+        r = single.r
+        out = torch.complex(out[:r], out[r:])
+        single = single.single
+    elif realified:
         out = torch.view_as_complex(out.reshape(out.shape[0], -1, 2).contiguous())
     res = out.t()
     if isinstance(like, torch.Tensor):
@@ -1219,6 +1236,8 @@ def _apply(inv, f):
     H = inv.H
     with _host_quiet():
         fd, single = _as_device_rhs(f, H.grid.n, H.device, H.realified)
+        if fd.shape[0] == 0:  # no right-hand sides
+            return _from_device(fd, f, single, H.realified)
         return _from_device(_apply_device(inv, fd), f, single, H.realified)
 
 
@@ -1347,6 +1366,8 @@ def _scatter_add_children(t, L, C, wc, r, dev):
 
 def _matvec(H, x):
     xd, single = _as_device_rhs(x, H.grid.n, H.device, H.realified)
+    if xd.shape[0] == 0:
+        return _from_device(xd, x, single, H.realified)
     return _from_device(_matvec_device(H, xd), x, single, H.realified)
 
 

@@ -355,3 +355,40 @@ def test_true_residual_fft_helmholtz():
     x = inv.apply(f)
     assert np.iscomplexobj(x)
     assert true_residual(spec, grid, P.PLAIN, f, x) <= 10 * eps
+
+
+def test_rhs_dtypes_follow_result_type():
+    """Result dtype = np.result_type(spec.dtype, f.dtype) (solver_dense.py:296):
+    a complex f on a real system is solved as its real and imaginary parts;
+    integer / float32 inputs are promoted; nrhs = 0 returns an empty result."""
+    P, sd = _api()
+    spec, grid, tree, H = setup(28)
+    inv = sd.invert_dense_block(H)
+    rng = np.random.default_rng(9)
+    a, b = rng.standard_normal((grid.n, 2)), rng.standard_normal((grid.n, 2))
+    xc = inv.apply(a + 1j * b)
+    assert xc.dtype == np.complex128 and xc.shape == (grid.n, 2)
+    # same columns, solved in a wider batch: equal up to the GEMM's
+    # N-dependent reduction schedule
+    close = lambda x, y: np.testing.assert_allclose(x, y, rtol=0, atol=1e-13 * np.abs(y).max())
+    close(xc.real, inv.apply(a))
+    close(xc.imag, inv.apply(b))
+    x1 = inv.apply(a[:, 0] + 1j * b[:, 0])
+    assert x1.shape == (grid.n,) and x1.dtype == np.complex128
+    close(x1.real, inv.apply(a[:, 0]))
+    yc = H.matvec(a + 1j * b)
+    close(yc.imag, H.matvec(b))
+    xt = inv.apply(torch.as_tensor(a + 1j * b, device="cuda"))
+    assert xt.is_complex() and xt.is_cuda
+    np.testing.assert_array_equal(xt.cpu().numpy(), xc)
+    ints = rng.integers(-5, 5, grid.n)
+    xi = inv.apply(ints)
+    assert xi.dtype == np.float64
+    np.testing.assert_array_equal(xi, inv.apply(ints.astype(np.float64)))
+    f32 = a[:, 0].astype(np.float32)
+    np.testing.assert_array_equal(inv.apply(f32), inv.apply(f32.astype(np.float64)))
+    e = inv.apply(np.zeros((grid.n, 0)))
+    assert e.shape == (grid.n, 0) and e.dtype == np.float64
+    assert H.matvec(np.zeros((grid.n, 0))).shape == (grid.n, 0)
+    with pytest.raises(ValueError):
+        inv.apply(np.zeros(grid.n + 1))
