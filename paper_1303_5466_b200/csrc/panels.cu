@@ -1152,6 +1152,133 @@ int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* a
   return launch_cluster((const void*)k_qr_panel_cl, count, cs, smem, st, args);
 }
 
+// Same selection as k_select_cl (QRCP of the sketch), with the chosen
+// columns eliminated by Householder reflections applied to every live sketch
+// column instead of Gram-Schmidt of each new pivot against the chosen basis:
+// warp 0's serial part per step shrinks to one reflector of length HSK - i
+// (the others no longer wait for an i-term orthogonalisation); each thread
+// then reflects its own column (thread per column: cols_per <= PT) and
+// downdates its residual norm by the new R(i, c)^2.
+template <int NT>  // threads = columns per CTA slot (cols_per <= NT); <= 128 registers
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) k_select_hh(const double* Yg, int ldy, long long sY,
+                                                  const int* mv, const int* active, const int* bsv,
+                                                  int J, int cols_per, int* swaps) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = cl.num_blocks(), cr = cl.block_rank();
+  const int b = blockIdx.x / cs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (!active[b] || bsv[b] <= 0) {
+    if (cr == 0 && tid == 0) swaps[(long long)b * SWL] = 0;
+    return;
+  }
+  const int bs = bsv[b];
+  const int n = mv[b] - J;
+  __shared__ XSel xch[2];
+  __shared__ double hv[HSK];
+  constexpr int NWt = NT / 32;
+  __shared__ double wcol[NWt][HSK];
+  __shared__ double s_tau;
+  __shared__ double redv[NWt];
+  __shared__ int redi[NWt];
+  __shared__ int sel[PNB];
+  const int c0 = cr * cols_per, c1 = min(n, c0 + cols_per), nc = max(c1 - c0, 0);
+  // this thread's sketch column in registers (thread per column)
+  const bool own = tid < nc;
+  double y[HSK];
+  double nrm = -1.0;
+  {
+    const double* Y = Yg + b * sY + (long long)(J + c0 + (own ? tid : 0)) * ldy;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int r = 0; r < HSK; r += 4) {
+      y[r] = own ? Y[r] : 0.0; y[r + 1] = own ? Y[r + 1] : 0.0;
+      y[r + 2] = own ? Y[r + 2] : 0.0; y[r + 3] = own ? Y[r + 3] : 0.0;
+      s0 = fma(y[r], y[r], s0); s1 = fma(y[r + 1], y[r + 1], s1);
+      s2 = fma(y[r + 2], y[r + 2], s2); s3 = fma(y[r + 3], y[r + 3], s3);
+    }
+    if (own) nrm = (s0 + s1) + (s2 + s3);
+  }
+  for (int i = 0; i < bs; ++i) {
+    XSel& x = xch[i & 1];
+    double v = nrm;
+    int iv = own && nrm >= 0.0 ? c0 + tid : 0x7fffffff;
+    if (!(nrm >= 0.0)) v = -1.0;
+    const double myv = v;
+    const int myi = iv;
+    warp_argmax(v, iv);
+    // each warp's winning lane stages its column in the warp's slot
+    if (myv >= 0.0 && myi == iv) {
+#pragma unroll
+      for (int r = 0; r < HSK; ++r) wcol[warp][r] = y[r];
+    }
+    if (lane == 0) { redv[warp] = v; redi[warp] = iv; }
+    __syncthreads();
+    if (warp == 0) {  // CTA candidate: fixed warp order, ties -> smaller column
+      double bv = redv[0];
+      int bi = redi[0], bw = 0;
+#pragma unroll
+      for (int ww = 1; ww < NWt; ++ww)
+        if (redv[ww] > bv || (redv[ww] == bv && redi[ww] < bi)) { bv = redv[ww]; bi = redi[ww]; bw = ww; }
+      if (bv >= 0.0) {
+        x.y[lane] = wcol[bw][lane];
+        if (lane + 32 < HSK) x.y[lane + 32] = wcol[bw][lane + 32];
+      }
+      if (lane == 0) { x.cand_v = bv; x.cand_i = bi; }
+    }
+    csync(cl);
+    if (warp == 0) {
+      double cv = -2.0;
+      int ci = 0x7fffffff;
+      if (lane < cs) { XSel* xr = remote(cl, &x, lane); cv = xr->cand_v; ci = xr->cand_i; }
+      warp_argmax(cv, ci);
+      if (ci < 0 || ci >= n) ci = min(i, n - 1);  // defensive (NaN data): stay in range
+      const XSel* xo = remote(cl, &x, ci / cols_per);
+      const double y0 = (lane >= i) ? xo->y[lane] : 0.0;
+      const double y1 = (lane + 32 < HSK && lane + 32 >= i) ? xo->y[lane + 32] : 0.0;
+      // dlarfg on rows i..HSK-1 of the pivot column
+      const double alpha = __shfl_sync(0xffffffffu, i < 32 ? y0 : y1, i & 31);
+      const double ss = warp_sum((lane > i ? y0 * y0 : 0.0) +
+                                 (lane + 32 > i && lane + 32 < HSK ? y1 * y1 : 0.0));
+      double tau = 0.0, sc = 0.0;
+      if (ss != 0.0) {
+        const double beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+        tau = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+      }
+      hv[lane] = lane < i ? 0.0 : (lane == i ? 1.0 : y0 * sc);
+      if (lane + 32 < HSK) hv[lane + 32] = lane + 32 < i ? 0.0 : (lane + 32 == i ? 1.0 : y1 * sc);
+      if (lane == 0) { s_tau = tau; sel[i] = ci; }
+    }
+    __syncthreads();
+    if (own && nrm >= 0.0) {
+      if (c0 + tid == sel[i]) {
+        nrm = -1.0;  // chosen
+      } else {
+        const double tau = s_tau;
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < HSK; r += 4) {
+          d0 = fma(hv[r], y[r], d0); d1 = fma(hv[r + 1], y[r + 1], d1);
+          d2 = fma(hv[r + 2], y[r + 2], d2); d3 = fma(hv[r + 3], y[r + 3], d3);
+        }
+        const double w = tau * ((d0 + d1) + (d2 + d3));
+        const volatile double* hvv = hv;
+#pragma unroll
+        for (int r = 0; r < HSK; ++r) y[r] = fma(-w, hvv[r], y[r]);  // re-read: keeps hv out of registers
+        // R(i, c) = y[i] after the reflection: residual norm^2 loses y[i]^2
+        double ri = 0.0;
+#pragma unroll
+        for (int r = 0; r < HSK; ++r) ri = (r == i) ? y[r] : ri;
+        nrm = fmax(nrm - ri * ri, 0.0);
+      }
+    }
+  }
+  csync(cl);
+  if (cr != 0 || warp != 0) return;
+  __shared__ int mid[NM], mpos[NM];
+  emit_swaps(sel, bs, J, b, swaps, lane, mid, mpos);
+}
+
 int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const int* active,
                   const int* bsv, int J, int maxm, int count, int* swaps, cudaStream_t st) {
   const int n = maxm - J;
@@ -1161,6 +1288,14 @@ int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const i
   size_t smem = ((size_t)(HSK + 1) * cols_per + (size_t)cols_per) * sizeof(double);
   void* args[] = {(void*)&Y, (void*)&ldy, (void*)&sY, (void*)&mv, (void*)&active, (void*)&bsv,
                   (void*)&J, (void*)&cols_per, (void*)&swaps};
+  static int hh = -1;  // VF_SELECT_HH=0: Gram-Schmidt selection everywhere (A/B)
+  if (hh < 0) { const char* e = getenv("VF_SELECT_HH"); hh = !(e && e[0] == '0'); }
+  if (hh && cols_per <= 512) {
+    const int nt = cols_per <= 128 ? 128 : (cols_per <= 256 ? 256 : 512);
+    const void* fn = nt == 128 ? (const void*)k_select_hh<128>
+                   : nt == 256 ? (const void*)k_select_hh<256> : (const void*)k_select_hh<512>;
+    return launch_cluster(fn, count, cs, 0, st, args, nt);
+  }
   const void* fn = cols_per > PT ? (const void*)k_select_cl<true> : (const void*)k_select_cl<false>;
   return launch_cluster(fn, count, cs, smem, st, args);
 }

@@ -318,6 +318,41 @@ def test_helmholtz_matches_reference_solution():
     assert np.linalg.norm(g["f"] - H.matvec(x)) / np.linalg.norm(g["f"]) <= 1e-9
 
 
+@pytest.mark.parametrize("n", [256, 512])
+def test_solution_matches_reference_large(n):
+    """Config c1 at 256^2 / 512^2 side by side with the reference (SURVEY.md
+    §8(c) item 2; fixtures from tests/golden/make_golden_big.py, RHS
+    regenerated from its seed): relative error vs the reference's solution
+    <= 10 eps, true residual (exact FFT operator) <= 10 eps, reference-layout
+    storage within 2 %, per-level maximum skeleton sizes within 2 %."""
+    P, sd = _api()
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    from paper_1303_5466_b200.verify import FFTOperator, true_residual
+    path = os.path.join(G, f"solve_c1_{n}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"fixture {path} not generated")
+    g = np.load(path)
+    spec = P.KernelSpec("laplace2d", b_field=P.make_field("centre_bump", scale=math.pi / 2),
+                        c_field=P.make_field("one"))
+    grid = P.Grid(n)
+    eps = 1e-10
+    inv = compress_inverse(spec, grid, eps=eps,
+                           opts=P.SolverOptions(eps=eps, leaf_size=64, k_cut=None), quad=P.CELL)
+    f = np.random.default_rng(int(g["seed"])).standard_normal(grid.n)
+    x = inv.apply(f)
+    xr = g["x"]
+    assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 10 * eps
+    r = true_residual(spec, grid, P.CELL, f, x, FFTOperator(spec, grid, P.CELL, "cuda"))
+    assert r <= 10 * eps, r
+    H = inv.dense_matvec_source
+    ref_nb = int(g["nbytes_inv"])
+    assert abs(inv.dense_delegate.nbytes_reference_layout() - ref_nb) <= 0.02 * ref_nb
+    rk = g["rank"]
+    for L in H.levels[1:]:
+        kref = max(int(rk[i]) for i in L.ids)
+        assert abs(int(L.kmax) - kref) <= 0.02 * kref + 2, (L.lv, int(L.kmax), kref)
+
+
 # ---- exact residual at sizes the dense oracle cannot reach (FFT operator) --
 
 @pytest.mark.parametrize("n,nrhs", [(256, 1), (256, 4), (512, 2)])
