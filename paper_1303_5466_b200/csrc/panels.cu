@@ -661,10 +661,7 @@ struct IC { static constexpr int value = V; };
 // measured: one step per loop trip (rotate by one) beats the 4-step unrolled
 // body for both panels -- fewer live registers, no spills (QR panel 199 -> 182 ms
 // over a 1024^2 factorization)
-#ifndef LU_UNROLL4
-#define LU_UNROLL4 0
-#endif
-template <int RPT>
+template <int RPT, int UNR = 1>
 __global__ void __launch_bounds__(PT, 1) k_lu_panel_rr(const double* A, long long sA, int lda,
                                                        int n, int c0, int nbs, int* ipiv,
                                                        long long sPiv, double* Ainv,
@@ -778,13 +775,23 @@ __global__ void __launch_bounds__(PT, 1) k_lu_panel_rr(const double* A, long lon
     if (cr == 0 && tid == 0) ipiv[b * sPiv + c0 + j] = c0 + piv;
   };
   int j = 0;
+  if constexpr (UNR == 4) {
 #pragma unroll 1
-  for (; j + 4 <= nbs && LU_UNROLL4; j += 4) {
-    step(j, j, IC<0>{});
-    step(j + 1, j, IC<1>{});
-    step(j + 2, j, IC<2>{});
-    step(j + 3, j, IC<3>{});
-    rotate_left<RPT, 4>(a);
+    for (; j + 4 <= nbs; j += 4) {
+      step(j, j, IC<0>{});
+      step(j + 1, j, IC<1>{});
+      step(j + 2, j, IC<2>{});
+      step(j + 3, j, IC<3>{});
+      rotate_left<RPT, 4>(a);
+    }
+  }
+  if constexpr (UNR == 2) {  // half the register rotation moves per column
+#pragma unroll 1
+    for (; j + 2 <= nbs; j += 2) {
+      step(j, j, IC<0>{});
+      step(j + 1, j, IC<1>{});
+      rotate_left<RPT, 2>(a);
+    }
   }
 #pragma unroll 1
   for (; j < nbs; ++j) {
@@ -1101,8 +1108,18 @@ int lu_panel(const double* A, long long sA, int lda, int n, int c0, int nbs, int
       void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&n, (void*)&c0, (void*)&nbs,
                       (void*)&ipiv, (void*)&sPiv, (void*)&Ainv, (void*)&sAi,
                       (void*)&pivmin, (void*)&pivmax};
-      const void* fn = rpt == 1 ? (const void*)k_lu_panel_rr<1>
-                     : rpt == 2 ? (const void*)k_lu_panel_rr<2> : (const void*)k_lu_panel_rr<3>;
+      static int unr = -1;  // VF_LU_UNR = 1 | 2 | 4: column steps per register rotation (2: measured 1-2 % faster GJ)
+      if (unr < 0) { const char* e = getenv("VF_LU_UNR"); unr = e ? atoi(e) : 2; }
+      const void* fn;
+      if (unr == 2)
+        fn = rpt == 1 ? (const void*)k_lu_panel_rr<1, 2>
+           : rpt == 2 ? (const void*)k_lu_panel_rr<2, 2> : (const void*)k_lu_panel_rr<3, 2>;
+      else if (unr == 4)
+        fn = rpt == 1 ? (const void*)k_lu_panel_rr<1, 4>
+           : rpt == 2 ? (const void*)k_lu_panel_rr<2, 4> : (const void*)k_lu_panel_rr<3, 4>;
+      else
+        fn = rpt == 1 ? (const void*)k_lu_panel_rr<1>
+           : rpt == 2 ? (const void*)k_lu_panel_rr<2> : (const void*)k_lu_panel_rr<3>;
       return launch_cluster(fn, batch, cs, 0, st, args);
     }
   }
