@@ -119,6 +119,11 @@ typedef struct {
   double* T; long long sT; int ldT;   /* out, k x (m-k) interpolation matrices */
   unsigned long long seed;            /* sketch seed (blocked path) */
   int force_blocked;                  /* testing: 1 = always the blocked randomized path */
+  const int* kfix;                    /* optional (device, count): fixed skeleton sizes.  No
+                                         pivoting; rank = kfix and T = R11^-1 R12 is the least-
+                                         squares solution of A(:, :k) T = A(:, k:m)
+                                         (solver_compressed.py:223-266 _interp_lowrank, full
+                                         rank).  Requires p >= min(m, 32*ceil(k/32)). */
 } vief_id_desc;
 int vief_id_batched(const vief_id_desc* d, void* stream); /* synchronises stream */
 

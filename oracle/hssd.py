@@ -576,3 +576,92 @@ def solve(P, n_max, eps, f, pad=None):
     H = compress(P, tree, eps, pad)
     inv = invert(H)
     return apply_inverse(inv, f), H, inv
+
+
+# ---------------------------------------------------------------------------
+# compressed path with a-priori skeletons, dense blocks
+# (tree.py:141-269 annotate_skeletons; solver_compressed.py:223-266
+#  _interp_lowrank at full rank; 437-483 _dense_factors / _dense_E_from_lu;
+#  560-577 dense root).  Restated as the dense oracle the reference's own
+#  tests use (test_solver_compressed.py:88-126 dense_box_F): T from
+#  lstsq(K(Z, X_sk), K(Z, X_rs)) with the field scalings.
+
+def _ring_dist(dx, dy, w, h):
+    return np.minimum(np.minimum(dx, w - 1 - dx), np.minimum(dy, h - 1 - dy))
+
+
+def _walk_order(idx, rect, n_side):
+    """Band points by (t on own ring, ring, dx, dy) (tree.py:148-180)."""
+    x0, x1, y0, y1 = (int(v) for v in rect)
+    w, h = x1 - x0, y1 - y0
+    dx, dy = idx % n_side - x0, idx // n_side - y0
+    r = _ring_dist(dx, dy, w, h)
+    rw, rh, lx, ly = w - 2 * r, h - 2 * r, dx - r, dy - r
+    pos = np.where(ly == 0, lx, np.where(
+        lx == rw - 1, rw - 1 + ly, np.where(
+            ly == rh - 1, 2 * (rw - 1) + (rh - 1) - lx,
+            2 * (rw - 1) + 2 * (rh - 1) - ly)))
+    per = np.maximum(2 * (rw - 1) + 2 * (rh - 1), 1)
+    return idx[np.lexsort((dy, dx, r, pos / per))]
+
+
+def annotate(tree, layers):
+    """{box: (sk, rs, work_perm)} fine to coarse (tree.py:198-269; no
+    support mask, no interior retention)."""
+    n = tree.n_side
+    out = {}
+    for b in tree.fine_to_coarse():
+        if tree.is_leaf(b):
+            full = tree.owned(b)
+        else:
+            c1, c2 = tree.kids[b]
+            full = np.concatenate([out[c1][0], out[c2][0]])
+        x0, x1, y0, y1 = (int(v) for v in tree.rect[b])
+        dx, dy = full % n - x0, full // n - y0
+        band = _ring_dist(dx, dy, x1 - x0, y1 - y0) < layers
+        sk = _walk_order(full[band], tree.rect[b], n)
+        rs = full[~band]
+        rdx, rdy = rs % n - x0, rs // n - y0
+        rs = rs[np.lexsort((rdx, rdy) if tree.level[b] % 2 == 0 else (rdy, rdx))]
+        where = {g: i for i, g in enumerate(full.tolist())}
+        perm = np.array([where[g] for g in np.concatenate([sk, rs]).tolist()], np.int64)
+        out[b] = (sk, rs, perm)
+    return out
+
+
+def compress_apriori(P, tree, layers):
+    """A Compressed object whose skeletons are the a-priori bands and whose
+    interpolations are the proxy least-squares fits; invert() / apply_inverse()
+    then give the compressed path's solution with dense blocks."""
+    ann = annotate(tree, layers)
+    H = Compressed(P, tree, {}, {}, {}, {}, {}, {})
+    for b in tree.fine_to_coarse():
+        rows = H.rows(b)
+        if tree.is_leaf(b):
+            H.D[b] = entries(P, rows, rows)
+        else:
+            c1, c2 = tree.kids[b]
+            H.B[b] = (entries(P, H.rskel[c1], H.cskel[c2]),
+                      entries(P, H.rskel[c2], H.cskel[c1]))
+        if b == 0:
+            continue
+        sk, rs, perm = ann[b]
+        zp = proxy_ring(tree.rect[b], layers)
+        k = sk.size
+        if rs.size:
+            t_up = sla.lstsq(proxy_tgt(P, zp, sk), proxy_tgt(P, zp, rs))[0]
+            t_dn = sla.lstsq(proxy_src(P, sk, zp).T, proxy_src(P, rs, zp).T)[0]
+        else:
+            t_up = t_dn = np.zeros((k, 0))
+        H.Lf[b] = ColumnID(perm, k, t_dn, 0.0)
+        H.Rf[b] = ColumnID(perm, k, t_up, 0.0)
+        H.rskel[b] = H.cskel[b] = sk
+    return H, ann
+
+
+def solve_apriori(P, n_max, layers, f):
+    """Tree + a-priori compression + invert + apply; returns (x, H, inv)."""
+    tree = make_tree(P.n_side, n_max)
+    H, _ = compress_apriori(P, tree, layers)
+    inv = invert(H)
+    return apply_inverse(inv, f), H, inv

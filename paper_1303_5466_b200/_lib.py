@@ -40,7 +40,7 @@ class IdDesc(ctypes.Structure):
                 ("maxp", c_int), ("maxm", c_int), ("count", c_int), ("group", c_int),
                 ("eps", c_double), ("rank", c_vp), ("perm", c_vp),
                 ("T", c_vp), ("sT", c_ll), ("ldT", c_int), ("seed", ctypes.c_ulonglong),
-                ("force_blocked", c_int)]
+                ("force_blocked", c_int), ("kfix", c_vp)]
 
 
 # name -> argtypes (all return int unless listed in _RET)

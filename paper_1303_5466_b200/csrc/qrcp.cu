@@ -663,6 +663,25 @@ __global__ void k_group_update(HState S, int count, int group) {
   }
 }
 
+// fixed-skeleton mode (kfix != null): no pivoting, every item factors its
+// first kfix columns (in whole blocks; Householder column j only depends on
+// columns <= j, so R(0:kfix, :) is exact) and T = R11^-1 R12 is the least-
+// squares solution of A(:, :kfix) T = A(:, kfix:m).
+__global__ void k_fixed_init(HState S, const int* kfix, int count) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= count) return;
+  S.k[b] = kfix[b];
+  S.done[b] = 1;
+  S.active[b] = kfix[b] > 0;
+}
+
+__global__ void k_fixed_update(HState S, const int* kfix, const int* mv, int J, int count) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= count || !S.active[b]) return;
+  if (J + HB >= kfix[b] || J + HB >= mv[b]) S.active[b] = 0;
+  else atomicOr(S.any, 1);
+}
+
 __global__ void k_init_state(HState S, const double* colmax, const int* pv, const int* mv, int count,
                              double eps) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -871,7 +890,8 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   int Kmax = 0;
   const size_t smem_small = ((size_t)(maxp | 1) * maxm + 2 * (size_t)maxm) * sizeof(double);
   // measured: the one-CTA-per-matrix SMEM QRCP wins only while two CTAs fit an SM
-  const bool small = !d->force_blocked && smem_small <= 110 * 1024;
+  const bool fixed = d->kfix != nullptr;
+  const bool small = !fixed && !d->force_blocked && smem_small <= 110 * 1024;
   int* kdev = d->rank;
   if (small) {
     prof_push(st, "id.small_qrcp");
@@ -930,6 +950,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
                             st));
     k_colmax<<<count, 256, 0, st>>>(S.tn, maxm, d->m, count, colmax);
     k_init_state<<<cdiv(count, 128), 128, 0, st>>>(S, colmax, d->p, d->m, count, d->eps);
+    if (fixed) k_fixed_init<<<cdiv(count, 128), 128, 0, st>>>(S, d->kfix, count);
     k_gaussian<<<cdiv((long long)HS * maxp, 256), 256, 0, st>>>(Om, (long long)HS * maxp,
                                                                d->seed ^ 0x5eedULL);
     k_bcast_omega<<<dim3(std::min<unsigned>(cdiv((long long)HS * maxp, 256), 64u), count), 256, 0, st>>>(
@@ -937,7 +958,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     g_launches += 6;
     VF_LAUNCH_CHECK("id init");
     int rc;
-    {  // Y = Omega A
+    if (!fixed) {  // Y = Omega A
       vief_gemm_desc g{};
       g.A = Om; g.strideA = 0; g.lda = HS;
       g.B = d->A; g.strideB = d->sA; g.ldb = d->lda;
@@ -961,14 +982,16 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       prof_push(st, "id.setup+select");
       k_block_setup<<<cdiv(count, 128), 128, 0, st>>>(J, Jf, d->p, d->m, count, S);
       ++g_launches;
-      if ((rc = sketch_select(S.Y, HS, sY, d->m, S.active, S.bs, J, maxm, count, S.swaps, st)))
-        return rc;
-      prof_push(st, "id.swaps");
-      k_apply_perm<<<dim3(cdiv(std::max(std::max(maxp, HS), std::max(J, kp)), AP_T), count), AP_T,
-                     0, st>>>(d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S, Rm, sR,
-                              ldR, kp, ldU);
-      g_launches += 2;
-      VF_LAUNCH_CHECK("id select/swap");
+      if (!fixed) {
+        if ((rc = sketch_select(S.Y, HS, sY, d->m, S.active, S.bs, J, maxm, count, S.swaps, st)))
+          return rc;
+        prof_push(st, "id.swaps");
+        k_apply_perm<<<dim3(cdiv(std::max(std::max(maxp, HS), std::max(J, kp)), AP_T), count),
+                       AP_T, 0, st>>>(d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S,
+                                      Rm, sR, ldR, kp, ldU);
+        g_launches += 2;
+        VF_LAUNCH_CHECK("id select/swap");
+      }
       double* Vi = S.Vw + (long long)kp * maxp;
       if (pend > 0) {  // make the panel current: A(Jf:p, J:J+bs) -= V_cat U_cat(:, J:J+bs)
         prof_push(st, "id.panel_catchup");
@@ -1037,6 +1060,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         if ((rc = vief_dgemm_batched(&r, st))) return rc;
         // sketch: Omega_i = Omega_{i-1} H_i on columns J..p-1, then
         // Y_trail -= Omega_i(:, J:J+bs) R(J block, trail)
+        if (!fixed) {
         prof_push(st, "id.sketch_downdate");
         vief_gemm_desc o1{};  // OV = Omega(:, J:p) V_i
         o1.A = S.Om + (long long)J * HS; o1.strideA = sOm; o1.lda = HS;
@@ -1066,9 +1090,12 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         y.M = HS; y.N = maxm; y.K = HB; y.Mb = S.sact; y.Nb = S.nrem; y.Kb = S.bs;
         y.alpha = -1.0; y.beta = 1.0; y.batch = count;
         if ((rc = vief_dgemm_batched(&y, st))) return rc;
+        }
       }
       // norms: downdate; columns near the cut (or with lost digits) need exact values,
       // which are only formed on a current A (after a flush)
+      int need = 0;
+      if (!fixed) {
       prof_push(st, "id.norms+rank");
       VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
       VF_CUDA(cudaMemsetAsync(S.certany, 0, sizeof(int) * 2 * count, st));
@@ -1077,9 +1104,9 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
           S.certany, S.flagany);
       k_need_exact<<<cdiv(count, 128), 128, 0, st>>>(S.active, S.certany, S.flagany, count, S.any);
       g_launches += 2;
-      int need = 0;
       VF_CUDA(cudaMemcpyAsync(&need, S.any, sizeof(int), cudaMemcpyDeviceToHost, st));
       VF_CUDA(cudaStreamSynchronize(st));
+      }
       ++pend;
       if (pend == D || need) {  // flush: A(Jf:p, trail) -= V_cat U_cat(:, trail)  (K = 32 pend)
         prof_push(st, "id.gemm_update");
@@ -1101,9 +1128,14 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       }
       prof_push(st, "id.norms+rank");
       VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
-      k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J);
-      k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
-      g_launches += 2;
+      if (fixed) {
+        k_fixed_update<<<cdiv(count, 128), 128, 0, st>>>(S, d->kfix, d->m, J, count);
+        ++g_launches;
+      } else {
+        k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J);
+        k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
+        g_launches += 2;
+      }
       VF_LAUNCH_CHECK("id rank");
       prof_push(st, "id.hostsync");
       int any = 0;

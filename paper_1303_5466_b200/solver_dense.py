@@ -35,7 +35,7 @@ import torch
 
 from . import _lib
 from .config import SolverOptions
-from .errors import SingularFactorError
+from .errors import ConfigError, SingularFactorError
 from .kernels import PLAIN, get_assembler
 from .tree import proxy_count_v, near_count, proxy_count
 
@@ -434,6 +434,8 @@ def _compress_level_id(H, L, pad, seed):
     nb = L.nb
     if L.lv == 0:
         return
+    if getattr(H, "apriori", None):
+        return _compress_level_apriori(H, L, H.apriori)
     _lib.prof_mark("py.sources+idmat")
     # proxy + near sources and the ID matrices (solver_dense.py:250-263)
     p, pmax, src_xy, src_g = _level_sources(H, L, pad)
@@ -492,6 +494,88 @@ def _compress_level_id(H, L, pad, seed):
         L.cskel = L.rskel
 
 
+def _compress_level_apriori(H, L, layers):
+    """Second half of a level's compression on the compressed path
+    (solver_compressed.py:223-266, 437-483): the skeleton is the a-priori
+    boundary band (tree.annotate_skeletons), and the interpolation
+    T_up (column fields c) / T_dn (row fields b) is the least-squares solution
+    of K(Z, X_sk) T = K(Z, X_rs) against the `layers` proxy rings Z.  It runs
+    as the batched blocked Householder QR of [A_sk | A_rs] without pivoting
+    and with the rank fixed to |sk| (vief_id_batched, kfix): T = R11^-1 R12."""
+    dev = H.device
+    prob = ctypes.byref(H.problem)
+    st = _lib.stream_handle
+    nb, mm, g = L.nb, L.mmax, H.group
+    kall, pall = H.tree.ann_levels[L.lv]
+    lo, hi = L.sl
+    k = kall[lo:hi].astype(np.int32)
+    if pall.shape[1] != mm:
+        raise ConfigError(f"level {L.lv}: annotated work sets ({pall.shape[1]}) do not match "
+                          f"the children's skeletons ({mm})")
+    wperm = pall[lo:hi].astype(np.int32)
+    w = L.rects[:, 1] - L.rects[:, 0]
+    h = L.rects[:, 3] - L.rects[:, 2]
+    p = proxy_count_v(w, h, layers).astype(np.int32)
+    # zero rows pad the QR to whole 32-column blocks (least squares unchanged)
+    kup = np.minimum(L.m, -(-k // 32) * 32)
+    if (p < k).any():
+        j = int(np.argmax(k - p))
+        raise ConfigError(f"box {int(L.ids[j])}: {int(p[j])} proxy points for {int(k[j])} "
+                          "skeleton points (least-squares interpolation needs p >= k)")
+    pv = np.maximum(p, kup).astype(np.int32)
+    L.p = p
+    _, pmax, src_xy, src_g = _level_sources(H, L, layers)   # proxy rings come first
+    p_d = _dev_i32(p, dev)
+    L.perm_r = _dev_i32(wperm, dev)
+    pts = torch.zeros((nb, mm), dtype=_I32, device=dev)       # [sk, rs] order
+    _lib.gather_int(L.rows, mm, L.perm_r, mm, pts, mm, L.m_d, mm, nb)
+    ldA = _even(pv.max())
+    A = torch.zeros((nb * g, mm, ldA), dtype=_F64, device=dev)
+    # kind 0: h^2 b_i K(x_i, z) (row fields: T_dn); kind 1: h^2 K(z, x_j) c_j (T_up)
+    _lib.call("vief_gen_idmat", prob, 0, _lib.ptr(pts), mm, _lib.ptr(L.m_d), mm,
+              _lib.ptr(src_xy), _lib.ptr(src_g), pmax, _lib.ptr(p_d), pmax, _lib.ptr(A),
+              g * mm * ldA, ldA, nb, st())
+    if g == 2:
+        _lib.call("vief_gen_idmat", prob, 1, _lib.ptr(pts), mm, _lib.ptr(L.m_d), mm,
+                  _lib.ptr(src_xy), _lib.ptr(src_g), pmax, _lib.ptr(p_d), pmax,
+                  _lib.ptr(A) + 8 * mm * ldA, g * mm * ldA, ldA, nb, st())
+    del src_xy, src_g, pts
+    count = nb * g
+    pvd = _dev_i32(np.repeat(pv, g), dev)
+    mv = _dev_i32(np.repeat(L.m, g), dev)
+    kfix = _dev_i32(np.repeat(k, g), dev)
+    rank = torch.zeros(count, dtype=_I32, device=dev)
+    perm = torch.zeros((count, mm), dtype=_I32, device=dev)
+    T = torch.zeros((count, mm, mm), dtype=_F64, device=dev)
+    _id_batched(dev, A, mm * ldA, ldA, pvd, mv, int(pv.max()), mm, count, g, float(H.eps), rank,
+                perm, T, 0, 1, kfix)
+    del A, perm
+    L.k = k
+    L.kmax = max(int(k.max()), 1)
+    L.k_d = _dev_i32(k, dev)
+    nT = L.m - k
+    L.ntmax = max(int(nT.max()), 1)
+    L.nT_d = _dev_i32(nT, dev)
+    L.perm_c = L.perm_r
+    L.Tr = torch.zeros((nb, L.ntmax, L.kmax), dtype=_F64, device=dev)
+    _lib.copy2d(T, g * mm * mm, mm, L.Tr, L.ntmax * L.kmax, L.kmax, L.k_d, L.kmax, L.nT_d,
+                L.ntmax, nb)
+    if g == 2:
+        L.Tc = torch.zeros_like(L.Tr)
+        _lib.copy2d(_lib.ptr(T) + 8 * mm * mm, g * mm * mm, mm, L.Tc, L.ntmax * L.kmax, L.kmax,
+                    L.k_d, L.kmax, L.nT_d, L.ntmax, nb)
+    else:
+        L.Tc = L.Tr
+    del T
+    L.rskel = torch.zeros((nb, L.kmax), dtype=_I32, device=dev)
+    _lib.gather_int(L.rows, mm, L.perm_r, mm, L.rskel, L.kmax, L.k_d, L.kmax, nb)
+    if g == 2:
+        L.cskel = torch.zeros((nb, L.kmax), dtype=_I32, device=dev)
+        _lib.gather_int(L.cols, mm, L.perm_r, mm, L.cskel, L.kmax, L.k_d, L.kmax, nb)
+    else:
+        L.cskel = L.rskel
+
+
 # The IDs of a level run as VF_ID_SPLIT (default 2) slices of the batch on as
 # many streams, each driven by its own host thread (the blocked ID
 # synchronises its stream twice per column block; ctypes releases the GIL):
@@ -515,13 +599,16 @@ def _id_side(dev, n):
     return ent
 
 
-def _id_batched(dev, A, sA, ldA, pv, mv, maxp, mm, count, g, eps, rank, perm, T, seed, forced):
-    """vief_id_batched over `count` items (groups of g share a rank)."""
+def _id_batched(dev, A, sA, ldA, pv, mv, maxp, mm, count, g, eps, rank, perm, T, seed, forced,
+                kfix=None):
+    """vief_id_batched over `count` items (groups of g share a rank); `kfix`
+    (device int32, count) fixes the ranks and disables pivoting."""
     def desc(lo, n):
         return _lib.IdDesc(_lib.ptr(A) + 8 * lo * sA, sA, ldA, _lib.ptr(pv) + 4 * lo,
                            _lib.ptr(mv) + 4 * lo, maxp, mm, n, g, eps, _lib.ptr(rank) + 4 * lo,
                            _lib.ptr(perm) + 4 * lo * mm, _lib.ptr(T) + 8 * lo * mm * mm, mm * mm,
-                           mm, seed, forced)
+                           mm, seed, forced,
+                           None if kfix is None else _lib.ptr(kfix) + 4 * lo)
     nb = count // g
     parts = min(_ID_SPLIT, nb)
     if parts < 2:
@@ -932,13 +1019,15 @@ def factor_solve(spec, grid, tree, eps, opts, f, quad=PLAIN):
         return H, inv, _from_device(out, f, single, H.realified)
 
 
-def factorize(spec, grid, tree, eps, opts, quad=PLAIN):
+def factorize(spec, grid, tree, eps, opts, quad=PLAIN, apriori=None):
+    """`apriori` = boundary-layer width: skeletons from tree.annotate_skeletons
+    (the compressed path's a-priori choice) instead of the IDs."""
     with _host_quiet():
-        H, inv, _ = _factorize(spec, grid, tree, eps, opts, quad)
+        H, inv, _ = _factorize(spec, grid, tree, eps, opts, quad, apriori=apriori)
     return H, inv
 
 
-def _factorize(spec, grid, tree, eps, opts, quad=PLAIN, rhs=None):
+def _factorize(spec, grid, tree, eps, opts, quad=PLAIN, rhs=None, apriori=None):
     """compress_outer + invert_dense_block with the levels pipelined over two
     CUDA streams: level l is inverted (side stream) while level l-1 is being
     compressed (current stream).  Inverting level l needs only level l's
@@ -946,6 +1035,7 @@ def _factorize(spec, grid, tree, eps, opts, quad=PLAIN, rhs=None):
     a different order; the latency-bound panels of one stage overlap the
     GEMMs of the other.  Singularity checks run at the end (same exception)."""
     H = Hss2dMatrix(spec, grid, tree, eps, opts, quad)
+    H.apriori = apriori
     pad = H.opts.resolved_proxy_layers(H.spec)
     inv = DenseBlockInverse(H)
     # compression on the caller's stream, inversions on a second stream (a

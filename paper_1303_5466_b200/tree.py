@@ -6,7 +6,8 @@ Mirrors the reference's tree.py for the HSS-D path: `build_tree`
 level at a time with array operations (breadth-first ids, so children of the
 j-th box of a level are boxes 2j, 2j+1 of the next level); the per-level
 rectangle arrays are what the device planner consumes.  The a-priori
-skeleton machinery of the O(N) path (tree.py:141-269) is out of scope.
+skeleton choice of the compressed path (`annotate_skeletons`,
+tree.py:141-269) fills per-box skeleton / residual splits on the host.
 """
 
 import numpy as np
@@ -15,11 +16,14 @@ from .errors import ConfigError
 
 
 class BoxNode:
-    __slots__ = ("idx", "level", "parent", "children", "x0", "x1", "y0", "y1")
+    __slots__ = ("idx", "level", "parent", "children", "x0", "x1", "y0", "y1",
+                 "full_idx", "sk_idx", "rs_idx", "work_perm", "n_interior_sk")
 
     def __init__(self, idx, level, parent, x0, x1, y0, y1):
         self.idx, self.level, self.parent = idx, level, parent
         self.children = None
+        self.full_idx = self.sk_idx = self.rs_idx = self.work_perm = None
+        self.n_interior_sk = 0
         self.x0, self.x1, self.y0, self.y1 = x0, x1, y0, y1
 
     @property
@@ -250,3 +254,182 @@ def near_field_indices(box, grid, pad):
     yy, xx = np.mgrid[Y0:Y1, X0:X1]
     keep = ~((xx >= box.x0) & (xx < box.x1) & (yy >= box.y0) & (yy < box.y1))
     return (yy[keep] * n + xx[keep]).astype(np.int64)
+
+
+# ---------------------------------------------------------------------------
+# a-priori skeletons of the compressed path (tree.py:141-269)
+
+def ring_of(dx, dy, w, h):
+    """Distance of box-local cell (dx, dy) to the box boundary (tree.py:143-145)."""
+    return np.minimum(np.minimum(dx, w - 1 - dx), np.minimum(dy, h - 1 - dy))
+
+
+def walk_key(dx, dy, w, h):
+    """(t, ring): t = CCW position of the cell on its own ring, from that
+    ring's lower-left corner, over the ring length (tree.py:148-167)."""
+    dx = np.asarray(dx, dtype=np.int64)
+    dy = np.asarray(dy, dtype=np.int64)
+    r = ring_of(dx, dy, w, h)
+    rw, rh = w - 2 * r, h - 2 * r
+    lx, ly = dx - r, dy - r
+    pos = np.select([ly == 0, lx == rw - 1, ly == rh - 1],
+                    [lx, (rw - 1) + ly, (rw - 1) + (rh - 1) + (rw - 1 - lx)],
+                    2 * (rw - 1) + (rh - 1) + (rh - 1 - ly))
+    per = np.maximum(2 * (rw - 1) + 2 * (rh - 1), 1)
+    return pos / per, r
+
+
+def order_boundary_cyclic(indices, box, grid):
+    """Band points by (t, ring, dx, dy) (tree.py:170-180)."""
+    indices = np.asarray(indices, dtype=np.int64)
+    if indices.size == 0:
+        return indices
+    n = grid.n_side
+    dx, dy = indices % n - box.x0, indices // n - box.y0
+    t, r = walk_key(dx, dy, box.width, box.height)
+    return indices[np.lexsort((dy, dx, r, t))]
+
+
+def order_interface(indices, box, grid):
+    """Interior points along the children's interface (tree.py:183-195)."""
+    indices = np.asarray(indices, dtype=np.int64)
+    if indices.size == 0:
+        return indices
+    n = grid.n_side
+    dx, dy = indices % n - box.x0, indices // n - box.y0
+    keys = (dx, dy) if box.split_axis() == "x" else (dy, dx)
+    return indices[np.lexsort(keys)]
+
+
+def boundary_layer_split(box, layers, grid, candidates=None, support_mask=None):
+    """(sk, rs): candidates within `layers` of the box boundary vs the rest;
+    points outside `support_mask` never become skeletons (tree.py:198-218)."""
+    n = grid.n_side
+    if candidates is None:
+        candidates = (np.arange(box.y0, box.y1)[:, None] * n
+                      + np.arange(box.x0, box.x1)[None, :]).ravel()
+    candidates = np.asarray(candidates, dtype=np.int64)
+    dx, dy = candidates % n - box.x0, candidates // n - box.y0
+    band = ring_of(dx, dy, box.width, box.height) < layers
+    if support_mask is not None:
+        band &= np.asarray(support_mask)[candidates]
+    return (order_boundary_cyclic(candidates[band], box, grid),
+            order_interface(candidates[~band], box, grid))
+
+
+def interface_interior_subset(rs_idx, box, grid, k_wave, points_per_wavelength):
+    """Residual points kept as skeletons for oscillatory kernels: a sublattice
+    at the requested density per wavelength (tree.py:221-234)."""
+    if rs_idx.size == 0:
+        return np.zeros(0, dtype=bool)
+    cells = (2.0 * np.pi / k_wave) / grid.h
+    stride = max(1, int(np.floor(cells / points_per_wavelength)))
+    if stride <= 1:
+        return np.ones(rs_idx.size, dtype=bool)
+    n = grid.n_side
+    return (rs_idx % n % stride == 0) & (rs_idx // n % stride == 0)
+
+
+def annotate_skeletons(tree, layers, support_mask=None, k_wave=None, points_per_wavelength=0.0):
+    """A-priori skeleton / residual split of every box, fine to coarse
+    (tree.py:237-269): a leaf splits its owned points, a parent the
+    concatenation of its children's skeletons, against its own boundary band
+    of width `layers`.  `work_perm` maps [sk, rs] onto positions in that
+    concatenation (`full_idx`).  Levels whose boxes share one shape (every
+    level of a power-of-two grid) are split with 2-D array operations; the
+    per-level arrays are kept in `tree.ann_levels[lv]` = (k, work_perm) for
+    the device planner."""
+    tree.layers = layers
+    keep_interior = k_wave is not None and points_per_wavelength > 0
+    nodes = tree.nodes
+    tree.ann_levels = {}
+    n = tree.grid.n_side
+    for lv in range(tree.depth, -1, -1):
+        ids = tree.ids[lv]
+        rects = tree.rects[lv]
+        w, h = rects[:, 1] - rects[:, 0], rects[:, 3] - rects[:, 2]
+        uniform = (support_mask is None and not keep_interior
+                   and (w == w[0]).all() and (h == h[0]).all())
+        if lv == tree.depth:
+            full = [tree.owned_indices(nodes[i]) for i in ids.tolist()] if not uniform else \
+                tree.owned_level(lv)
+        else:
+            kid = tree.ids[lv + 1]
+            full = [np.concatenate([nodes[a].sk_idx, nodes[b].sk_idx])
+                    for a, b in zip(kid[0::2].tolist(), kid[1::2].tolist())]
+            uniform = uniform and len({f.size for f in full}) == 1
+            if uniform:
+                full = np.stack(full)
+        if uniform:
+            _annotate_level_uniform(tree, lv, np.asarray(full), layers)
+            continue
+        for j, i in enumerate(ids.tolist()):
+            box = nodes[i]
+            box.full_idx = np.asarray(full[j], dtype=np.int64)
+            sk, rs = boundary_layer_split(box, layers, tree.grid, candidates=box.full_idx,
+                                          support_mask=support_mask)
+            box.n_interior_sk = 0
+            if keep_interior and not box.is_leaf and rs.size:
+                keep = interface_interior_subset(rs, box, tree.grid, k_wave,
+                                                 points_per_wavelength)
+                extra = rs[keep]
+                rs = rs[~keep]
+                sk = np.concatenate([sk, extra])
+                box.n_interior_sk = extra.size
+            box.sk_idx, box.rs_idx = sk, rs
+            # full_idx has distinct entries: position of each [sk, rs] point in it
+            srt = np.argsort(box.full_idx, kind="stable")
+            order = np.concatenate([sk, rs])
+            box.work_perm = srt[np.searchsorted(box.full_idx, order, sorter=srt)].astype(np.int64)
+        k = np.array([nodes[i].sk_idx.size for i in ids.tolist()], np.int64)
+        m = max(nodes[i].full_idx.size for i in ids.tolist())
+        perm = np.zeros((len(ids), m), np.int64)
+        for j, i in enumerate(ids.tolist()):
+            perm[j, :nodes[i].work_perm.size] = nodes[i].work_perm
+        tree.ann_levels[lv] = (k, perm)
+    return tree
+
+
+def _annotate_level_uniform(tree, lv, full, layers):
+    """One level of annotate_skeletons for boxes of one shape: the band mask
+    has the same count in every row (translation of one box), so the splits
+    are (nb, k) / (nb, r) arrays ordered with a row-wise lexsort."""
+    n = tree.grid.n_side
+    rects = tree.rects[lv]
+    x0, y0 = rects[:, 0:1], rects[:, 2:3]
+    w, h = int(rects[0, 1] - rects[0, 0]), int(rects[0, 3] - rects[0, 2])
+    dx, dy = full % n - x0, full // n - y0
+    if (dx == dx[0]).all() and (dy == dy[0]).all():
+        # every box is a translate of the first (true by induction for trees
+        # of one box shape per level): split the first, reuse the permutation
+        dx, dy = dx[:1], dy[:1]
+    band = ring_of(dx, dy, w, h) < layers
+    m = full.shape[1]
+    nb = dx.shape[0]
+    k = int(band[0].sum())
+    pos = np.broadcast_to(np.arange(m), (nb, m))
+    bpos = pos[band].reshape(nb, k)
+    rpos = pos[~band].reshape(nb, m - k)
+    take = lambda a, p: np.take_along_axis(a, p, axis=1)  # noqa: E731
+    if k:
+        bdx, bdy = take(dx, bpos), take(dy, bpos)
+        t, r = walk_key(bdx, bdy, w, h)
+        bpos = take(bpos, np.lexsort((bdy, bdx, r, t), axis=-1))
+    if m - k:
+        rdx, rdy = take(dx, rpos), take(dy, rpos)
+        keys = (rdx, rdy) if lv % 2 == 0 else (rdy, rdx)
+        rpos = take(rpos, np.lexsort(keys, axis=-1))
+    perm = np.concatenate([bpos, rpos], axis=1)
+    if nb < full.shape[0]:
+        perm = np.broadcast_to(perm, full.shape)
+    nb = full.shape[0]
+    ordered = take(full, perm)
+    nodes = tree.nodes
+    for j, i in enumerate(tree.ids[lv].tolist()):
+        box = nodes[i]
+        box.full_idx = full[j]
+        box.sk_idx = ordered[j, :k]
+        box.rs_idx = ordered[j, k:]
+        box.work_perm = perm[j]
+        box.n_interior_sk = 0
+    tree.ann_levels[lv] = (np.full(nb, k, np.int64), perm)
