@@ -15,7 +15,8 @@ stores the blocks of boxes with more than k_cut skeleton points in 1-D HSS
 form (eps-accurate, O(N) memory); here every block stays dense in HBM, so
 results agree with the reference to its eps while the storage is the
 dense-block one.  ti_mode is validated like the reference's but factors every
-box (no per-level record sharing).  Real kernels only.
+box (no per-level record sharing).  Complex kernels run realified like the
+dense-block path (the realified least-squares fit is the realified complex one).
 """
 
 import numpy as np
@@ -65,8 +66,6 @@ def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti
         H, inv.dense_delegate = factorize(spec, grid, tree, eps, opts, quad)
         inv.dense_matvec_source = H
         return inv
-    if spec.is_complex:
-        raise NotImplementedError("finite k_cut on the B200 is built for real kernels only")
     layers = opts.resolved_layers(spec)
     if tree.nodes[0].sk_idx is None:
         kw = {}

@@ -509,13 +509,18 @@ def _compress_level_apriori(H, L, layers):
     kall, pall = H.tree.ann_levels[L.lv]
     lo, hi = L.sl
     k = kall[lo:hi].astype(np.int32)
+    pall = pall[lo:hi]
+    if H.realified:  # unknown u = 2 * point + component; T is the realified complex fit
+        k = 2 * k
+        pall = (2 * pall[:, :, None] + np.arange(2)).reshape(pall.shape[0], -1)
     if pall.shape[1] != mm:
         raise ConfigError(f"level {L.lv}: annotated work sets ({pall.shape[1]}) do not match "
                           f"the children's skeletons ({mm})")
-    wperm = pall[lo:hi].astype(np.int32)
+    wperm = pall.astype(np.int32)
     w = L.rects[:, 1] - L.rects[:, 0]
     h = L.rects[:, 3] - L.rects[:, 2]
-    p = proxy_count_v(w, h, layers).astype(np.int32)
+    pp = proxy_count_v(w, h, layers).astype(np.int32)   # proxy points
+    p = 2 * pp if H.realified else pp                  # rows of the fit
     # zero rows pad the QR to whole 32-column blocks (least squares unchanged)
     kup = np.minimum(L.m, -(-k // 32) * 32)
     if (p < k).any():
@@ -523,9 +528,9 @@ def _compress_level_apriori(H, L, layers):
         raise ConfigError(f"box {int(L.ids[j])}: {int(p[j])} proxy points for {int(k[j])} "
                           "skeleton points (least-squares interpolation needs p >= k)")
     pv = np.maximum(p, kup).astype(np.int32)
-    L.p = p
+    L.p = pp
     _, pmax, src_xy, src_g = _level_sources(H, L, layers)   # proxy rings come first
-    p_d = _dev_i32(p, dev)
+    p_d = _dev_i32(pp, dev)
     L.perm_r = _dev_i32(wperm, dev)
     pts = torch.zeros((nb, mm), dtype=_I32, device=dev)       # [sk, rs] order
     _lib.gather_int(L.rows, mm, L.perm_r, mm, pts, mm, L.m_d, mm, nb)
@@ -1006,14 +1011,15 @@ def _host_quiet():
             gc.enable()
 
 
-def factor_solve(spec, grid, tree, eps, opts, f, quad=PLAIN):
+def factor_solve(spec, grid, tree, eps, opts, f, quad=PLAIN, apriori=None):
     """factorize() and the solve of f in one pass: the up sweep of level l runs
     (third stream) as soon as level l is inverted, overlapping the
     factorization of the coarser levels; the down sweep follows.  Returns
     (H, inv, x) with x = inv.apply(f) (bitwise: same kernels, same order per
     level)."""
     with _host_quiet():
-        H, inv, (fd, single, phi, ups) = _factorize(spec, grid, tree, eps, opts, quad, rhs=f)
+        H, inv, (fd, single, phi, ups) = _factorize(spec, grid, tree, eps, opts, quad, rhs=f,
+                                                    apriori=apriori)
         out = torch.zeros_like(fd)
         _sweep_down(H, phi, ups, out)
         return H, inv, _from_device(out, f, single, H.realified)

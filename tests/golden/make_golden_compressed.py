@@ -47,6 +47,25 @@ def main():
         out[key + "_perm"] = np.concatenate([b.work_perm for b in tree.nodes])
         out[key + "_nsk"] = np.array([b.sk_idx.size for b in tree.nodes])
         out[key + "_nrs"] = np.array([b.rs_idx.size for b in tree.nodes])
+    # oscillatory retention (tree.py:221-234): kappa >= 16, stride 3 at 64^2
+    tree = build_tree(Grid(64), 64)
+    annotate_skeletons(tree, 3, k_wave=101.0, points_per_wavelength=0.5)
+    key = "ann_64_64_3_kw101"
+    out[key + "_sk"] = np.concatenate([b.sk_idx for b in tree.nodes])
+    out[key + "_rs"] = np.concatenate([b.rs_idx for b in tree.nodes])
+    out[key + "_perm"] = np.concatenate([b.work_perm for b in tree.nodes])
+    out[key + "_nsk"] = np.array([b.sk_idx.size for b in tree.nodes])
+    out[key + "_nrs"] = np.array([b.rs_idx.size for b in tree.nodes])
+    out[key + "_nint"] = np.array([b.n_interior_sk for b in tree.nodes])
+    # complex: test_solver_compressed.py:243-253 (k = 4 pi, 18^2, leaf 81, k_cut 16)
+    spec = KernelSpec("helmholtz2d", k=4 * np.pi)
+    grid = Grid(18)
+    inv = compress_inverse(spec, grid, eps=1e-10,
+                           opts=SolverOptions(eps=1e-10, leaf_size=81, k_cut=16))
+    rng = np.random.default_rng(4)
+    f = rng.standard_normal(grid.n) + 1j * rng.standard_normal(grid.n)
+    out["solve_helm18_f"] = f
+    out["solve_helm18_x"] = inv.apply(f)
     for name, (n, leaf, k_cut, b, c, ti, seed) in CASES.items():
         spec = KernelSpec("laplace2d", b_field=b, c_field=c)
         grid = Grid(n)

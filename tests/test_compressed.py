@@ -58,6 +58,22 @@ def test_oracle_annotate_matches_reference(n, leaf, layers):
         np.testing.assert_array_equal(ann[b][2], perm)
 
 
+def test_annotate_interior_retention_matches_reference():
+    """Oscillatory kernels keep an interface sublattice (tree.py:221-234)."""
+    from paper_1303_5466_b200 import Grid, build_tree
+    from paper_1303_5466_b200.tree import annotate_skeletons
+    tree = build_tree(Grid(64), 64)
+    annotate_skeletons(tree, 3, k_wave=101.0, points_per_wavelength=0.5)
+    key = "ann_64_64_3_kw101"
+    for b, sk, rs, perm in _split(key):
+        node = tree.nodes[b]
+        np.testing.assert_array_equal(node.sk_idx, sk)
+        np.testing.assert_array_equal(node.rs_idx, rs)
+        np.testing.assert_array_equal(node.work_perm, perm)
+    np.testing.assert_array_equal([nd.n_interior_sk for nd in tree.nodes], GOLD[key + "_nint"])
+    assert GOLD[key + "_nint"].max() > 0
+
+
 def test_support_mask_drops_skeletons():
     from paper_1303_5466_b200 import Grid, build_tree
     from paper_1303_5466_b200.tree import annotate_skeletons

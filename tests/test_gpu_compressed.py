@@ -110,3 +110,22 @@ def test_compressed_c1_size_residual():
     f = np.random.default_rng(0).standard_normal(grid.n)
     x = inv.apply(f)
     assert true_residual(spec, grid, P.PLAIN, f, x) <= 1e-8
+
+
+def test_helmholtz_compressed_matches_reference():
+    """Complex kernel, realified on the device (test_solver_compressed.py:243-253:
+    residual <= 1e-7), solution vs the reference's compressed one."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    gold = np.load(os.path.join(G, "compressed.npz"))
+    spec = P.KernelSpec("helmholtz2d", k=4 * np.pi)
+    grid = P.Grid(18)
+    inv = compress_inverse(spec, grid, eps=1e-10,
+                           opts=P.SolverOptions(eps=1e-10, leaf_size=81, k_cut=16))
+    f = gold["solve_helm18_f"]
+    x = inv.apply(f)
+    assert x.dtype == np.complex128
+    A = P.assemble_dense(spec, grid, P.PLAIN, np.arange(grid.n), np.arange(grid.n))
+    assert np.linalg.norm(A @ x - f) / np.linalg.norm(f) <= 1e-7
+    xr = gold["solve_helm18_x"]
+    assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 1e-7
