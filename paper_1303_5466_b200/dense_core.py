@@ -45,16 +45,24 @@ class IdFactor:
         return self.right_matrix(dtype).T
 
 
-def interp_decomp_batched(mats, eps, group=1, force_blocked=False, seed=0):
+def interp_decomp_batched(mats, eps, group=1, force_blocked=False, seed=0, kfix=None):
     """IDs of a list of real matrices in one K2 launch sequence.  Matrices in
     consecutive groups of `group` share a rank (max over the group), as the
-    row/column IDs of one box do in compress_outer.  Returns
+    row/column IDs of one box do in compress_outer.  `kfix` (one rank per
+    matrix) turns pivoting off: T is then the least-squares solution of
+    A[:, :k] T = A[:, k:] (the compressed path's interpolation).  Returns
     [(perm, k, T), ...]."""
     _lib.require_cuda()
     dev = torch.device("cuda")
     count = len(mats)
     ps = np.array([a.shape[0] for a in mats], dtype=np.int32)
     ms = np.array([a.shape[1] for a in mats], dtype=np.int32)
+    kf = None
+    if kfix is not None:
+        kf = np.asarray(kfix, dtype=np.int32)
+        if (kf < 0).any() or (kf > np.minimum(ps, ms)).any():
+            raise ValueError("kfix must lie in [0, min(p, m)]")
+        ps = np.maximum(ps, np.minimum(ms, -(-kf // 32) * 32)).astype(np.int32)  # zero rows
     maxp, maxm = max(int(ps.max()), 1), max(int(ms.max()), 1)
     ldA = maxp + (maxp & 1)
     A = torch.zeros((count, maxm, ldA), dtype=torch.float64, device=dev)
@@ -66,9 +74,10 @@ def interp_decomp_batched(mats, eps, group=1, force_blocked=False, seed=0):
     rank = torch.zeros(count, dtype=torch.int32, device=dev)
     perm = torch.zeros((count, maxm), dtype=torch.int32, device=dev)
     T = torch.zeros((count, maxm, maxm), dtype=torch.float64, device=dev)
+    kd = None if kf is None else torch.as_tensor(kf, device=dev)
     d = _lib.IdDesc(_lib.ptr(A), maxm * ldA, ldA, _lib.ptr(pv), _lib.ptr(mv), maxp, maxm, count,
                     group, float(eps), _lib.ptr(rank), _lib.ptr(perm), _lib.ptr(T), maxm * maxm,
-                    maxm, int(seed), int(force_blocked))
+                    maxm, int(seed), int(force_blocked), None if kd is None else _lib.ptr(kd))
     _lib.call("vief_id_batched", ctypes.byref(d), _lib.stream_handle())
     rank = rank.cpu().numpy()
     perm = perm.cpu().numpy()

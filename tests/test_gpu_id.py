@@ -110,3 +110,28 @@ def test_blocked_id_on_kernel_rows_vs_oracle(shape):
     assert abs(k - ref.k) <= max(3, ref.k // 20), (k, ref.k)
     assert err <= 50 * eps, err
     assert len(set(perm.tolist())) == m
+
+
+def test_fixed_rank_is_least_squares():
+    """vief_id_batched with kfix: no pivoting, rank = kfix, T = lstsq(A[:, :k],
+    A[:, k:]) (the compressed path's interpolation).  Ragged batch: k off the
+    32-column blocks, k = m, k = 0, p = k (square), several blocks."""
+    from paper_1303_5466_b200.dense_core import interp_decomp_batched
+    rng = np.random.default_rng(9)
+    shapes = [(80, 64, 48), (150, 140, 100), (40, 40, 40), (70, 50, 0), (300, 200, 130),
+              (100, 90, 100 - 10)]
+    mats, ks = [], []
+    for p, m, k in shapes:
+        A = rng.standard_normal((p, m))
+        A[:, :k] *= np.logspace(0, -2, k)  # graded skeleton columns
+        mats.append(A)
+        ks.append(k)
+    out = interp_decomp_batched(mats, 1e-10, kfix=ks)
+    for A, k, (perm, kk, T) in zip(mats, ks, out):
+        assert kk == k
+        np.testing.assert_array_equal(perm, np.arange(A.shape[1]))
+        assert T.shape == (k, A.shape[1] - k)
+        if k == 0 or k == A.shape[1]:
+            continue
+        ref = np.linalg.lstsq(A[:, :k], A[:, k:], rcond=None)[0]
+        assert np.linalg.norm(T - ref) <= 1e-9 * np.linalg.norm(ref)
