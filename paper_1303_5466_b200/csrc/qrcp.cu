@@ -977,7 +977,16 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     // The sketch is kept in original coordinates: Omega_i = Omega H_1..H_i,
     // Y_trail -= Omega_i(:, J block) R(J block, trail).
     int pend = 0, Jf = 0;
+    int kfix_max = -1;  // fixed ranks: the block count is known up front (no per-block sync)
+    if (fixed) {
+      std::vector<int> hk(count);
+      VF_CUDA(cudaMemcpyAsync(hk.data(), d->kfix, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+      VF_CUDA(cudaStreamSynchronize(st));
+      kfix_max = 0;
+      for (int b = 0; b < count; ++b) kfix_max = std::max(kfix_max, hk[b]);
+    }
     for (int J = 0; J < kcap; J += HB) {
+      if (fixed && J >= kfix_max) break;
       const int kp = pend * HB;  // pending reflector columns
       prof_push(st, "id.setup+select");
       k_block_setup<<<cdiv(count, 128), 128, 0, st>>>(J, Jf, d->p, d->m, count, S);
@@ -1131,6 +1140,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       if (fixed) {
         k_fixed_update<<<cdiv(count, 128), 128, 0, st>>>(S, d->kfix, d->m, J, count);
         ++g_launches;
+        continue;
       } else {
         k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J);
         k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
