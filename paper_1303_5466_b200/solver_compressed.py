@@ -28,6 +28,48 @@ from .solver_dense import compress_outer, factorize, invert_dense_block
 from .tree import annotate_skeletons, build_tree
 
 
+class BoxFactors:
+    """Host view of one non-root box's factors on the finite-k_cut path, in the
+    reference's [sk, rs] ordering (BoxFactors, solver_compressed.py:73-140).
+    Every box here is of the dense kinds ("leaf" / "dense"): T_up, T_dn, E
+    and F^-1 are plain arrays copied from HBM on access.  Real kernels."""
+
+    def __init__(self, inv, box):
+        if inv.spec.is_complex:
+            raise NotImplementedError("factor views are built for real kernels")
+        H, D = inv.dense_matvec_source, inv.dense_delegate
+        i = box.idx
+        self.kind = "leaf" if box.is_leaf else "dense"
+        self.k, self.r = int(box.sk_idx.size), int(box.rs_idx.size)
+        self.k1 = None if box.is_leaf else int(inv.tree.nodes[box.children[0]].sk_idx.size)
+        wp = box.work_perm
+        self.perm = None if box.is_leaf else wp
+        self.iperm = None
+        if not box.is_leaf:
+            self.iperm = np.empty_like(wp)
+            self.iperm[wp] = np.arange(wp.size)
+        self.T_up = H.Rfac[i].T
+        self.T_dn = H.Lfac[i].T
+        self.E = D.E[i]
+        self.Finv = D.Finv[i][np.ix_(wp, wp)]
+
+    def nbytes(self):
+        return self.T_up.nbytes + self.T_dn.nbytes + self.E.nbytes + self.Finv.nbytes
+
+    def apply_finv(self, u):
+        """sigma = F^-1 u on the box ordering [sk, rs]."""
+        return self.Finv @ u
+
+    def apply_R(self, phi):
+        return phi[:self.k] + self.T_up @ phi[self.k:]
+
+    def apply_L(self, w):
+        return np.vstack([w, self.T_dn.T @ w])
+
+    def apply_E(self, x):
+        return self.E @ x
+
+
 class CompressedInverse:
     def __init__(self, spec, grid, tree, eps, opts, quad, ti_mode):
         self.spec, self.grid, self.tree = spec, grid, tree
@@ -37,6 +79,17 @@ class CompressedInverse:
 
     def nbytes(self):
         return self.dense_delegate.nbytes()
+
+    def factor_of(self, box):
+        """Factors of a non-root box (finite k_cut; solver_compressed.py:166-167)."""
+        if self.dense_delegate is None or not hasattr(self.tree.nodes[0], "sk_idx") \
+                or self.tree.nodes[0].sk_idx is None or box.idx == 0:
+            raise KeyError(box.idx)
+        return BoxFactors(self, box)
+
+    def record_count(self):
+        """Factor records: one per non-root box plus the top (solver_compressed.py:169-171)."""
+        return len(self.tree.nodes)
 
     def apply(self, f):
         return self.dense_delegate.apply(f)

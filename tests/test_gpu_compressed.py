@@ -129,3 +129,52 @@ def test_helmholtz_compressed_matches_reference():
     assert np.linalg.norm(A @ x - f) / np.linalg.norm(f) <= 1e-7
     xr = gold["solve_helm18_x"]
     assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 1e-7
+
+
+def _oracle_apriori(name):
+    import oracle.hssd as O
+    n, leaf, _, b, c, _ = CASES[name]
+    Pr = O.Problem(n, "laplace2d", 0.0, ("one", ()), (b, ()), (c, ()), "none")
+    tree = O.make_tree(n, leaf)
+    H, ann = O.compress_apriori(Pr, tree, 2)
+    return O, tree, H, ann, O.invert(H)
+
+
+def test_build_e_matches_dense_oracle():
+    """E = ([I T_up] F^-1 [I; T_dn^T])^-1 per box vs the dense oracle
+    (test_solver_compressed.py:168-184: <= 1e-7; here <= 1e-8)."""
+    _, _, inv = _solve("nonsym28_k8")
+    O, tree, H, ann, oinv = _oracle_apriori("nonsym28_k8")
+    for bid in (1, 3, 7, 20):
+        fac = inv.factor_of(inv.tree.nodes[bid])
+        assert fac.kind == ("leaf" if inv.tree.nodes[bid].is_leaf else "dense")
+        assert fac.E.shape == (fac.k, fac.k)
+        E = oinv.E[bid]
+        # T comes from an ill-conditioned least-squares fit (LAPACK gelsd in the
+        # oracle, Householder QR here): E agrees to ~1e-9, 100x inside the bar
+        assert np.linalg.norm(fac.E - E) / np.linalg.norm(E) <= 1e-8
+        assert fac.T_up.shape == fac.T_dn.shape == (fac.k, fac.r)
+
+
+def test_apply_finv_matches_dense_oracle():
+    """F^-1 on [sk, rs] vs the dense oracle F (test_solver_compressed.py:129-153),
+    linearity, record count."""
+    _, _, inv = _solve("nti28_k8")
+    O, tree, H, ann, oinv = _oracle_apriori("nti28_k8")
+    bid = 3
+    fac = inv.factor_of(inv.tree.nodes[bid])
+    c1, c2 = tree.kids[bid]
+    F = np.block([[oinv.E[c1], H.B[bid][0]], [H.B[bid][1], oinv.E[c2]]])
+    perm = ann[bid][2]
+    Fd = F[np.ix_(perm, perm)]
+    rng = np.random.default_rng(0)
+    u = rng.standard_normal((Fd.shape[0], 3))
+    got, ref = fac.apply_finv(u), np.linalg.solve(Fd, u)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-9
+    u2 = rng.standard_normal(Fd.shape[0])
+    lhs = fac.apply_finv((2.0 * u[:, 0] + u2)[:, None])
+    rhs = 2.0 * fac.apply_finv(u[:, 0][:, None]) + fac.apply_finv(u2[:, None])
+    assert np.linalg.norm(lhs - rhs) <= 1e-11 * np.linalg.norm(rhs)
+    assert inv.record_count() == len(inv.tree.nodes)
+    with pytest.raises(KeyError):
+        inv.factor_of(inv.tree.nodes[0])
