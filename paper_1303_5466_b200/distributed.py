@@ -23,6 +23,7 @@ import torch
 
 from . import _lib
 from . import solver_dense as sd
+from .tree import annotate_skeletons
 
 _F64, _I32 = torch.float64, torch.int32
 
@@ -155,10 +156,18 @@ class ShardedInverse:
         self.emulate = emulate
         self.ranks = list(range(world)) if emulate else [comm.rank]
         self.local = {}
+        # finite k_cut: the compressed path's a-priori skeletons (host annotation
+        # is deterministic, so every rank derives the same splits)
+        apriori = None
+        if not (opts.k_cut is None or opts.k_cut == np.inf):
+            apriori = opts.resolved_layers(spec)
+            if tree.nodes[0].sk_idx is None:
+                annotate_skeletons(tree, apriori)
         s = self.plan.split
         payloads = {}
         for g in self.ranks:
             Hl = sd.Hss2dMatrix(spec, grid, tree, eps, opts, quad, level_slices=self.plan.slices[g])
+            Hl.apriori = apriori
             sd.compress_levels(Hl)
             invl = sd.invert_dense_block(Hl)
             self.local[g] = (Hl, invl)
@@ -186,6 +195,7 @@ class ShardedInverse:
             top_slices[s] = (0, world)
             Ht = sd.Hss2dMatrix(spec, grid, tree, eps, opts, quad, level_slices=top_slices)
             _virtual_level(Ht, s, ks, rsk, csk, Es, self.dev)
+            Ht.apriori = apriori
             sd.compress_levels(Ht)
             self.top = (Ht, sd.invert_dense_block(Ht))
 

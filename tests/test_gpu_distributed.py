@@ -33,7 +33,7 @@ def test_emulated_shards_equal_single_gpu():
     spec = P.KernelSpec("laplace2d", b_field=P.make_field("gaussian_bump"), c_field=P.make_field("one"))
     grid = P.Grid(64)
     tree = P.build_tree(grid, 64)
-    opts = P.SolverOptions(eps=1e-10, leaf_size=64)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=None)  # ID skeletons (HSS-D)
     ref = sd.invert_dense_block(sd.compress_outer(spec, grid, tree, 1e-10, opts))
     f = np.random.default_rng(3).standard_normal((grid.n, 3))
     xr = ref.apply(f)
@@ -41,3 +41,24 @@ def test_emulated_shards_equal_single_gpu():
         x = ShardedInverse(spec, grid, tree, 1e-10, opts, P.PLAIN, world, emulate=True).apply(f)
         # same per-box arithmetic; the sketch seeds are per level, so skeletons agree
         assert np.linalg.norm(x - xr) <= 1e-12 * np.linalg.norm(xr)
+
+
+def test_emulated_shards_compressed_path():
+    """Finite k_cut (a-priori skeletons) through the sharded phases: same
+    arithmetic per box as the single-GPU compressed path, and the reference's
+    compressed solution (tests/golden/compressed.npz)."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200.distributed import ShardedInverse
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    gold = np.load(os.path.join(G, "compressed.npz"))
+    spec = P.KernelSpec("laplace2d", b_field=P.make_field("gaussian_bump"), c_field=P.make_field("one"))
+    grid = P.Grid(64)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=64)
+    f = gold["solve_nonsym64_leaf64_f"]
+    xr = compress_inverse(spec, grid, eps=1e-10, opts=opts).apply(f)
+    for world in (2, 4):
+        tree = P.build_tree(grid, 64)
+        x = ShardedInverse(spec, grid, tree, 1e-10, opts, P.PLAIN, world, emulate=True).apply(f)
+        assert np.linalg.norm(x - xr) <= 1e-12 * np.linalg.norm(xr)
+        xg = gold["solve_nonsym64_leaf64_x"]
+        assert np.linalg.norm(x - xg) / np.linalg.norm(xg) <= 1e-8
