@@ -276,6 +276,9 @@ def save(obj, path):
     from .solver_compressed import CompressedInverse
     from .solver_dense import DenseBlockInverse, Hss2dMatrix
     if isinstance(obj, CompressedInverse):
+        if obj.ti_mode and any(getattr(L, "ti", False) for L in obj.dense_matvec_source.levels
+                               if L is not None):
+            raise NotImplementedError("saving TI-mode (shared-record) factors is not supported")
         kind, H = "CompressedInverse", obj.dense_matvec_source
     elif isinstance(obj, DenseBlockInverse):
         kind, H = "DenseBlockInverse", obj.H

@@ -14,8 +14,10 @@ root F = cross + diag(E1, E2) (solver_compressed.py:560-577).  The reference
 stores the blocks of boxes with more than k_cut skeleton points in 1-D HSS
 form (eps-accurate, O(N) memory); here every block stays dense in HBM, so
 results agree with the reference to its eps while the storage is the
-dense-block one.  ti_mode is validated like the reference's but factors every
-box (no per-level record sharing).  Complex kernels run realified like the
+dense-block one.  ti_mode (translation-invariant kernels) keeps one factor
+record per level after the factorization (share_level_records: the sweeps read
+it with batch stride 0), as the reference's TI mode does; every box is still
+factored.  Complex kernels run realified like the
 dense-block path (the realified least-squares fit is the realified complex one).
 """
 
@@ -24,7 +26,7 @@ import numpy as np
 from .config import SolverOptions
 from .errors import ConfigError
 from .kernels import PLAIN
-from .solver_dense import compress_outer, factorize, invert_dense_block
+from .solver_dense import compress_outer, factorize, invert_dense_block, share_level_records
 from .tree import annotate_skeletons, build_tree
 
 
@@ -88,7 +90,10 @@ class CompressedInverse:
         return BoxFactors(self, box)
 
     def record_count(self):
-        """Factor records: one per non-root box plus the top (solver_compressed.py:169-171)."""
+        """Factor records: one per non-root box plus the top, or one per level
+        in TI mode (solver_compressed.py:169-171)."""
+        if self.ti_mode and self.dense_delegate is not None and self.tree.nodes[0].sk_idx is not None:
+            return self.tree.depth + 1
         return len(self.tree.nodes)
 
     def apply(self, f):
@@ -126,6 +131,8 @@ def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti
             kw = dict(k_wave=spec.k, points_per_wavelength=opts.points_per_wavelength)
         annotate_skeletons(tree, layers, support_mask=support_mask, **kw)
     H, inv.factors = factorize(spec, grid, tree, eps, opts, quad, apriori=layers)
+    if ti_mode:
+        share_level_records(inv.factors)
     inv.dense_delegate = inv.factors
     inv.dense_matvec_source = H
     return inv

@@ -891,10 +891,11 @@ class DenseBlockInverse:
 
     def _get(self, i, which):
         L, j = self.H._lvl_of[i]
+        k, m = int(L.k[j]), int(L.m[j])
+        if getattr(L, "ti", False):
+            j = 0
         if which == "E":
-            k = int(L.k[j])
             return L.E[j, :k, :k].t().cpu().numpy()
-        m = int(L.m[j])
         if getattr(L, "rb", None) is not None:  # root in block form: F^{-1} = solve(I)
             eye = torch.eye(m, dtype=_F64, device=self.H.device)
             X = torch.zeros_like(eye)
@@ -908,9 +909,12 @@ class DenseBlockInverse:
         H = self.H
         for L in _real_levels(H):
             m = L.m.astype(np.int64)
+            k = L.k.astype(np.int64) if L.lv > 0 else None
+            if getattr(L, "ti", False):  # one shared record per level
+                m = m[:1]
+                k = k[:1]
             tot += int((m * m).sum()) * 8
             if L.lv > 0:
-                k = L.k.astype(np.int64)
                 tot += int((k * k + 2 * k * m).sum()) * 8
                 tot += int((k * (m - k)).sum()) * 8 * H.group
         return tot
@@ -1230,6 +1234,29 @@ def _level_dn_idx(H, L):
     return L.dn_idx
 
 
+def _fs(L, stride):
+    """Batch stride of a level's factor arrays: 0 once the level shares one
+    record (TI mode, share_level_records)."""
+    return 0 if getattr(L, "ti", False) else stride
+
+
+def share_level_records(inv):
+    """TI mode (solver_compressed.py:33-37,548-552): with a-priori skeletons and
+    a translation-invariant kernel every box of a level is a translate of the
+    first, so its factors are the first box's; keep that record (F^-1, C, E, W)
+    per level and let the sweeps read it with batch stride 0.  Factor memory
+    drops from O(N log N) to one record per level."""
+    for L in _real_levels(inv.H):
+        if L.nb < 2:
+            continue
+        for name in ("Finv", "C", "E", "W"):
+            t = getattr(L, name, None)
+            if t is not None:
+                setattr(L, name, t[:1].clone())
+        L.ti = True
+    torch.cuda.empty_cache()
+
+
 def _mv(A, sA, lda, X, sx, ldx, Y, sy, ldy, M, K, Mb, Kb, nb, r, alpha, beta):
     """Y_b = alpha * A_b X_b + beta * Y_b for r right-hand sides."""
     if r == 1:
@@ -1263,7 +1290,7 @@ def _sweep_up_level(H, L, fd, phi, ups):
     if getattr(L, "rb", None) is not None:
         _root_block_solve(L, U, ldv, r, Phi, ldv)
     else:
-        _mv(L.Finv, mm * mm, mm, U, mm, ldv, Phi, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r,
+        _mv(L.Finv, _fs(L, mm * mm), mm, U, mm, ldv, Phi, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r,
             1.0, 0.0)
     del U
     phi[L.lv] = Phi
@@ -1271,7 +1298,7 @@ def _sweep_up_level(H, L, fd, phi, ups):
         return
     kk = L.kmax
     Ups = torch.zeros((r, nb * kk), dtype=_F64, device=dev)
-    _mv(L.C, mm * kk, kk, Phi, mm, ldv, Ups, kk, nb * kk, kk, mm, L.k_d, L.m_d, nb, r,
+    _mv(L.C, _fs(L, mm * kk), kk, Phi, mm, ldv, Ups, kk, nb * kk, kk, mm, L.k_d, L.m_d, nb, r,
         1.0, 0.0)
     ups[L.lv] = Ups
 
@@ -1309,9 +1336,9 @@ def _sweep_down(H, phi, ups, out, pd_top=None):
             par = H.levels[L.lv - 1]
             PD = pd_top if par is None else _phi_dn(H, L, phi, r)
             Ups = ups[L.lv]
-            _mv(L.E, kk * kk, kk, PD, kk, nb * kk, Ups, kk, nb * kk, kk, kk, L.k_d, L.k_d, nb, r,
+            _mv(L.E, _fs(L, kk * kk), kk, PD, kk, nb * kk, Ups, kk, nb * kk, kk, kk, L.k_d, L.k_d, nb, r,
                 -1.0, 1.0)
-            _mv(L.W, kk * mm, mm, Ups, kk, nb * kk, Phi, mm, ldv, mm, kk, L.m_d, L.k_d, nb, r,
+            _mv(L.W, _fs(L, kk * mm), mm, Ups, kk, nb * kk, Phi, mm, ldv, mm, kk, L.m_d, L.k_d, nb, r,
                 -1.0, 1.0)
             del PD
         if L.leaf:

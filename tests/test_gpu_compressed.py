@@ -178,3 +178,43 @@ def test_apply_finv_matches_dense_oracle():
     assert inv.record_count() == len(inv.tree.nodes)
     with pytest.raises(KeyError):
         inv.factor_of(inv.tree.nodes[0])
+
+
+def test_ti_record_sharing_and_accuracy():
+    """TI mode keeps one record per level (test_solver_compressed.py:216-234):
+    same solution as per-box factors, factor memory one record per level."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    spec = P.KernelSpec("laplace2d")
+    grid = P.Grid(28)
+    opts = P.SolverOptions(eps=1e-10, k_cut=8)
+    inv_ti = compress_inverse(spec, grid, eps=1e-10, opts=opts, ti_mode=True)
+    inv_nti = compress_inverse(spec, grid, eps=1e-10, opts=opts, ti_mode=False)
+    assert inv_ti.record_count() == inv_ti.tree.depth + 1
+    assert inv_ti.nbytes() < inv_nti.nbytes() / 2   # reference: 2.6 MB vs 6.3 MB
+    A = P.assemble_dense(spec, grid, P.PLAIN, np.arange(grid.n), np.arange(grid.n))
+    v = np.random.default_rng(3).standard_normal((grid.n, 2))
+    x_ti, x_nti = inv_ti.apply(v), inv_nti.apply(v)
+    assert np.linalg.norm(x_ti - x_nti) <= 1e-12 * np.linalg.norm(x_nti)
+    r = np.linalg.norm(A @ x_ti - v) / np.linalg.norm(v)
+    assert r <= 1e-8
+    x1 = inv_ti.apply(v[:, 0])   # single RHS: the GEMV path with stride-0 factors
+    assert np.linalg.norm(x1 - x_ti[:, 0]) <= 1e-13 * np.linalg.norm(x1)
+    gold = np.load(os.path.join(G, "compressed.npz"))
+    f = gold["solve_ti28_k8_f"]
+    xg = gold["solve_ti28_k8_x"]
+    assert np.linalg.norm(inv_ti.apply(f) - xg) / np.linalg.norm(xg) <= 1e-8
+
+
+def test_ti_mode_512_memory():
+    """512^2 TI problem: shared records make the factors small; true residual."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    from paper_1303_5466_b200.verify import true_residual
+    spec = P.KernelSpec("laplace2d")
+    grid = P.Grid(512)
+    inv = compress_inverse(spec, grid, eps=1e-10,
+                           opts=P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=64), ti_mode=True)
+    assert inv.nbytes() < 2e9
+    f = np.random.default_rng(0).standard_normal(grid.n)
+    assert true_residual(spec, grid, P.PLAIN, f, inv.apply(f)) <= 1e-8
