@@ -6,10 +6,11 @@ conventions.  (The preconditioned iterative solve and the convergence study
 are not part of this build.)
 
 Differences, all confined to what this build covers:
-  * mode="compressed" (the reference default) runs compress_inverse with
-    k_cut=None, i.e. the dense-block path: the O(N) finite-k_cut solver is
-    out of scope (solver_compressed.py).  When the caller passes options
-    with a finite k_cut they are copied with k_cut=None.
+  * mode="compressed" (the reference default, k_cut = 64) runs the
+    compressed path's a-priori skeletons with the scatterer support mask
+    (solver_compressed.compress_inverse, dense blocks) and refines against
+    the ID-compressed operator H, as the reference does; k_cut=None runs the
+    dense-block inverse of H itself.
   * info additionally carries "true_residual": ||rhs - A tau|| / ||rhs|| with
     A applied exactly by FFT (verify.py), not just the compressed matvec.
 Reference: scattering.py:22-128 (problem, setup_ls, outgoing_field,
@@ -99,11 +100,11 @@ def outgoing_field(problem, tau, targets, chunk=1 << 22):
     return np.concatenate(parts).astype(np.complex128) if parts else np.zeros(0, np.complex128)
 
 
-def _dense_opts(opts, eps):
-    opts = opts or SolverOptions(eps=eps, k_cut=None)
-    if not (opts.k_cut is None or opts.k_cut == np.inf):
-        opts = replace(opts, k_cut=None)
-    return opts
+def _support_mask(spec, grid):
+    """Points with nonzero contrast; None when the support is everything
+    (scattering.py:87-89)."""
+    vals = np.abs(spec.b_field(grid.points()))
+    return vals > 0.0 if np.any(vals == 0.0) else None
 
 
 def approx_residual(H, inv, grid, n_rhs=3, rng=None):
@@ -128,7 +129,7 @@ def solve_direct(problem, eps=1e-10, refine=True, mode="compressed", opts=None,
     from .verify import FFTOperator
     spec, rhs = setup_ls(problem)
     grid = problem.grid
-    opts = _dense_opts(opts, eps)
+    opts = opts or SolverOptions(eps=eps)
     info = {}
     if np.linalg.norm(rhs) == 0.0:
         tau = np.zeros(grid.n, dtype=np.complex128)
@@ -136,9 +137,15 @@ def solve_direct(problem, eps=1e-10, refine=True, mode="compressed", opts=None,
                     u_out=lambda t: np.zeros(len(np.atleast_2d(t)), dtype=np.complex128))
         return tau, info
     tree = build_tree(grid, opts.leaf_size)
+    finite = not (opts.k_cut is None or opts.k_cut == np.inf)
     if mode == "dense":
         H = compress_outer(spec, grid, tree, eps, opts, quad=problem.quad)
         inv = invert_dense_block(H)
+    elif finite:
+        H = compress_outer(spec, grid, tree, eps, opts, quad=problem.quad)
+        inv = compress_inverse(spec, grid, tree=build_tree(grid, opts.leaf_size), eps=eps,
+                               opts=opts, quad=problem.quad,
+                               support_mask=_support_mask(spec, grid))
     else:
         inv = compress_inverse(spec, grid, tree=tree, eps=eps, opts=opts, quad=problem.quad)
         H = inv.dense_matvec_source
