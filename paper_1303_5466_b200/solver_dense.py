@@ -891,11 +891,12 @@ class DenseBlockInverse:
 
     def _get(self, i, which):
         L, j = self.H._lvl_of[i]
-        k, m = int(L.k[j]), int(L.m[j])
-        if getattr(L, "ti", False):
-            j = 0
+        m = int(L.m[j])
+        jr = 0 if getattr(L, "ti", False) else j   # TI: the level's shared record
         if which == "E":
-            return L.E[j, :k, :k].t().cpu().numpy()
+            k = int(L.k[j])
+            return L.E[jr, :k, :k].t().cpu().numpy()
+        j = jr
         if getattr(L, "rb", None) is not None:  # root in block form: F^{-1} = solve(I)
             eye = torch.eye(m, dtype=_F64, device=self.H.device)
             X = torch.zeros_like(eye)
