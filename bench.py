@@ -91,6 +91,23 @@ def _cpu_threads():
         return os.cpu_count() or 1
 
 
+def _reference_headline():
+    """The reference package itself (vief, /root/reference) at the headline
+    size, measured once in the build container by tests/golden/make_golden_c3c4.py
+    (stored with its solution in tests/golden/solve_c4_1024.npz): a stated
+    baseline, not a same-run measurement."""
+    path = os.path.join(ROOT, "tests", "golden", "solve_c4_1024.npz")
+    if not os.path.exists(path):
+        return None
+    g = np.load(path)
+    tb, tf, ts = (float(x) for x in g["times"])
+    n = 1024 * 1024
+    return {"n_side": 1024, "build_s": tb, "factor_s": tf, "solve_1rhs_s": ts,
+            "factor_unknowns_per_s": n / (tb + tf), "threads": int(g["threads"]),
+            "host": "build container (8-core Xeon, OpenBLAS), not the GPU box",
+            "source": "tests/golden/solve_c4_1024.npz (make_golden_c3c4.py)"}
+
+
 def run_reference(a):
     rank, world, _ = _dist()
     if rank != 0:
@@ -105,7 +122,14 @@ def run_reference(a):
             "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": _config(a.n, a.nrhs, world),
+            "config": dict(_config(a.cpu_n, a.nrhs, world),
+                           workload=f"c4 family, bounded CPU sample: Laplace log-kernel VIE "
+                                    f"{a.cpu_n}x{a.cpu_n} (N={a.cpu_n ** 2}), float64, leaf 64, "
+                                    f"eps 1e-10, factor + {a.nrhs}-RHS solve (the {a.n}^2 "
+                                    f"headline size takes ~1 h of reference CPU per step; its "
+                                    f"measured time is in reference_at_headline)",
+                           sample_of=_config(a.n, a.nrhs, world)["workload"]),
+            "reference_at_headline": _reference_headline(),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"oracle/hssd.py (reference algorithm on scipy "
                                        f"{__import__('scipy').__version__}/OpenBLAS, "

@@ -23,7 +23,6 @@ import torch
 
 from . import _lib
 from . import solver_dense as sd
-from .tree import annotate_skeletons
 
 _F64, _I32 = torch.float64, torch.int32
 
@@ -149,7 +148,8 @@ class ShardedInverse:
     (TorchComm) for one-process-per-GPU runs, or with `emulate=True` to run
     all shards in this process (single-GPU validation of the sharded path)."""
 
-    def __init__(self, spec, grid, tree, eps, opts, quad, world, comm=None, emulate=False):
+    def __init__(self, spec, grid, tree, eps, opts, quad, world, comm=None, emulate=False,
+                 support_mask=None):
         self.spec, self.grid, self.tree, self.eps, self.opts, self.quad = spec, grid, tree, eps, opts, quad
         self.plan = subtree_plan(tree, world)
         self.comm = comm
@@ -160,9 +160,8 @@ class ShardedInverse:
         # is deterministic, so every rank derives the same splits)
         apriori = None
         if not (opts.k_cut is None or opts.k_cut == np.inf):
-            apriori = opts.resolved_layers(spec)
-            if tree.nodes[0].sk_idx is None:
-                annotate_skeletons(tree, apriori)
+            from .solver_compressed import ensure_apriori_skeletons
+            apriori = ensure_apriori_skeletons(spec, tree, opts, support_mask)
         s = self.plan.split
         payloads = {}
         for g in self.ranks:

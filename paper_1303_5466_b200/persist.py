@@ -13,7 +13,7 @@ batches, so the file is a dump of those batches, not of per-box blocks:
     ...      storages, each starting on a 4096-byte boundary
 
 The header records the problem (spec, quadrature rule, options, eps, grid side,
-leaf size, level slices -- pickled, base64), every storage (file offset, byte
+leaf size, level slices -- as plain JSON values, see `_problem_json`), every storage (file offset, byte
 count, whether it lives on the device) and, per tree level, every attribute
 of the level's state: tensors and numpy arrays as (storage, offset, shape,
 stride, dtype) views -- aliasing between tensors (the root's block-form factors
@@ -25,14 +25,15 @@ whole thing.
 
 Loading rebuilds the host objects (grid, tree, assembler) from the problem
 description and uploads the storages; `load(...).apply(f)` is bitwise
-identical to the saved object's `apply(f)` (tests).  The header's pickle is
-trusted input: load only files you wrote.
+identical to the saved object's `apply(f)` (tests).  Nothing in the file is
+executed: the header is JSON decoded into the package's own frozen dataclasses
+(field presets and kernel families are validated by their constructors), and
+every storage is a raw byte range.
 """
 
-import base64
+import dataclasses
 import json
 import os
-import pickle
 import struct
 
 import numpy as np
@@ -41,7 +42,7 @@ import torch
 from . import _lib
 
 MAGIC = b"VIEFB200"
-VERSION = 1
+VERSION = 2
 _ALIGN = 4096
 _CHUNK = 256 << 20
 
@@ -160,15 +161,60 @@ def _write_storage(f, kind, obj, stage):
     stage.write(f, src)
 
 
+def _field_json(f):
+    return {"name": f.name, "params": [[k, v] for k, v in f.params]}
+
+
+def _problem_json(pb):
+    """problem dict (spec, quad, opts, ...) -> JSON-safe dict."""
+    sp = pb["spec"]
+    out = {"spec": {"family": sp.family, "k": float(sp.k),
+                    "a_field": _field_json(sp.a_field), "b_field": _field_json(sp.b_field),
+                    "c_field": _field_json(sp.c_field)},
+           "quad": pb["quad"].order,
+           "opts": dataclasses.asdict(pb["opts"])}
+    for k in ("eps", "n_side", "n_max", "ti_mode"):
+        if k in pb:
+            out[k] = pb[k]
+    sl = pb.get("level_slices")
+    out["level_slices"] = None if sl is None else [[int(lv), list(v)] for lv, v in sl.items()]
+    return out
+
+
+def _problem_from_json(d):
+    from .config import SolverOptions
+    from .kernels import Field, KernelSpec, QuadratureCorrection, make_field
+
+    def field(e):
+        f = make_field(e["name"], **{k: v for k, v in e["params"]})  # validates the preset
+        assert isinstance(f, Field)
+        return f
+
+    sp = d["spec"]
+    spec = KernelSpec(str(sp["family"]), k=float(sp["k"]), a_field=field(sp["a_field"]),
+                      b_field=field(sp["b_field"]), c_field=field(sp["c_field"]))
+    fields = {f.name for f in dataclasses.fields(SolverOptions)}
+    opts = SolverOptions(**{k: v for k, v in d["opts"].items() if k in fields})
+    out = {"spec": spec, "quad": QuadratureCorrection(str(d["quad"])), "opts": opts,
+           "eps": float(d["eps"]), "n_side": int(d["n_side"]), "n_max": int(d["n_max"])}
+    if "ti_mode" in d:
+        out["ti_mode"] = bool(d["ti_mode"])
+    sl = d.get("level_slices")
+    out["level_slices"] = None if sl is None else {int(lv): tuple(int(x) for x in v)
+                                                   for lv, v in sl}
+    return out
+
+
 def write_state(path, problem, kind, levels):
     """Write `levels` (list of per-level attribute dicts or None) and the
-    picklable `problem` description to `path`."""
+    `problem` description (spec, quad, opts, eps, n_side, n_max, level_slices)
+    to `path`."""
     w = _Writer()
     enc_levels = [None if st is None else {k: w.encode(v) for k, v in st.items()}
                   for st in levels]
     sizes = [_nbytes(k, o) for k, o in w.storages]
     header = {"version": VERSION, "kind": kind,
-              "problem": base64.b64encode(pickle.dumps(problem)).decode(),
+              "problem": _problem_json(problem) if "spec" in problem else problem,
               "levels": enc_levels, "storages": []}
     # offsets depend on the header length; iterate until it is stable
     hlen = 0
@@ -256,7 +302,8 @@ def read_state(path, device):
 
     levels = [None if st is None else {k: decode(v) for k, v in st.items()}
               for st in header["levels"]]
-    return header["kind"], pickle.loads(base64.b64decode(header["problem"])), levels
+    pb = header["problem"]
+    return header["kind"], (_problem_from_json(pb) if "spec" in pb else pb), levels
 
 
 # ---------------------------------------------------------------------------

@@ -111,6 +111,23 @@ class CompressedInverse:
         return persist.load(path, device)
 
 
+def ensure_apriori_skeletons(spec, tree, opts, support_mask=None):
+    """Annotate `tree` with the compressed path's a-priori skeletons exactly as
+    the reference's compress_inverse does (solver_compressed.py:536-542): the
+    boundary band of `resolved_layers`, plus the oscillatory interior
+    retention for Helmholtz above the kappa threshold, restricted to an
+    optional support mask.  Every caller that factors on the finite-k_cut path
+    (compress_inverse, distributed.ShardedInverse) goes through here, so all of
+    them choose the same skeletons.  Returns the layer width."""
+    layers = opts.resolved_layers(spec)
+    if tree.nodes[0].sk_idx is None:
+        kw = {}
+        if opts.keep_interface_interior(spec):
+            kw = dict(k_wave=spec.k, points_per_wavelength=opts.points_per_wavelength)
+        annotate_skeletons(tree, layers, support_mask=support_mask, **kw)
+    return layers
+
+
 def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti_mode=False,
                      support_mask=None):
     opts = opts or SolverOptions(eps=eps)
@@ -124,12 +141,7 @@ def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti
         H, inv.dense_delegate = factorize(spec, grid, tree, eps, opts, quad)
         inv.dense_matvec_source = H
         return inv
-    layers = opts.resolved_layers(spec)
-    if tree.nodes[0].sk_idx is None:
-        kw = {}
-        if opts.keep_interface_interior(spec):
-            kw = dict(k_wave=spec.k, points_per_wavelength=opts.points_per_wavelength)
-        annotate_skeletons(tree, layers, support_mask=support_mask, **kw)
+    layers = ensure_apriori_skeletons(spec, tree, opts, support_mask)
     H, inv.factors = factorize(spec, grid, tree, eps, opts, quad, apriori=layers)
     if ti_mode:
         share_level_records(inv.factors)

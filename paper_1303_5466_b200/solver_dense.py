@@ -706,6 +706,7 @@ def _invert_root_block(inv, L, checks=None):
     else:
         checks.append((L, pmin, pmax, "F"))
     L.rb = (G1, L.B12[0], L.B21[0], S[0], k1, k2, kc)
+    C.Gkeep = None  # the root's block factors hold the one G1 the solve needs
     L.Finv = None
 
 
@@ -775,6 +776,7 @@ def _invert_level_F_block(inv, L, checks=None):
               alpha=-1.0, beta=0.0, batch=nb, Mb=k1d, Nb=k2d, Kb=k2d, Cptr=p12)   # X12
     _lib.copy2d(S, s2, kc, None, 0, mm, k2d, kc, k2d, kc, nb, dstp=p22)            # X22
     del T1, S
+    C.Gkeep = None  # consumed: only this block elimination reads the children's G1
     _lib.pad_identity(F, mm * mm, mm, L.m_d, mm, nb)
     L.Finv = F
 
@@ -1246,9 +1248,15 @@ def share_level_records(inv):
     a translation-invariant kernel every box of a level is a translate of the
     first, so its factors are the first box's; keep that record (F^-1, C, E, W)
     per level and let the sweeps read it with batch stride 0.  Factor memory
-    drops from O(N log N) to one record per level."""
+    drops from O(N log N) to one record per level.
+
+    A level is shared only when its boxes really are translates: same
+    rectangle size, same m and k (a ragged grid -- e.g. 49/56/64-point leaves
+    -- or a support mask can make them differ).  Such a level keeps its
+    per-box records, so the sweeps stay correct (the reference's shared
+    record would fail with a shape mismatch there)."""
     for L in _real_levels(inv.H):
-        if L.nb < 2:
+        if L.nb < 2 or not _level_is_uniform(L):
             continue
         for name in ("Finv", "C", "E", "W"):
             t = getattr(L, name, None)
@@ -1256,6 +1264,16 @@ def share_level_records(inv):
                 setattr(L, name, t[:1].clone())
         L.ti = True
     torch.cuda.empty_cache()
+
+
+def _level_is_uniform(L):
+    """Every box of the level has the first box's width/height, m and k."""
+    r = np.asarray(L.rects)
+    wh = np.stack([r[:, 1] - r[:, 0], r[:, 3] - r[:, 2]], 1)
+    if not (wh == wh[0]).all() or not (np.asarray(L.m) == L.m[0]).all():
+        return False
+    k = getattr(L, "k", None)
+    return k is None or bool((np.asarray(k) == k[0]).all())
 
 
 def _mv(A, sA, lda, X, sx, ldx, Y, sy, ldy, M, K, Mb, Kb, nb, r, alpha, beta):

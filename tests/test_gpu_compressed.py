@@ -218,3 +218,26 @@ def test_ti_mode_512_memory():
     assert inv.nbytes() < 2e9
     f = np.random.default_rng(0).standard_normal(grid.n)
     assert true_residual(spec, grid, P.PLAIN, f, inv.apply(f)) <= 1e-8
+
+
+def test_ti_mode_ragged_grid_keeps_per_box_records():
+    """Ragged boxes (Grid(30), leaf 64: 49/56/64-point leaves) are not
+    translates of each other; TI mode must keep their per-box records instead
+    of reading box 0's factors for every box."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    from paper_1303_5466_b200.solver_dense import _level_is_uniform
+    spec = P.KernelSpec("laplace2d")
+    grid = P.Grid(30)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=8)
+    inv_ti = compress_inverse(spec, grid, eps=1e-10, opts=opts, ti_mode=True)
+    inv_nti = compress_inverse(spec, grid, eps=1e-10, opts=opts, ti_mode=False)
+    levels = [L for L in inv_ti.dense_matvec_source.levels if L is not None]
+    assert any(not _level_is_uniform(L) for L in levels)
+    for L in levels:
+        assert getattr(L, "ti", False) == (L.nb >= 2 and _level_is_uniform(L))
+    v = np.random.default_rng(4).standard_normal((grid.n, 2))
+    x_ti, x_nti = inv_ti.apply(v), inv_nti.apply(v)
+    assert np.linalg.norm(x_ti - x_nti) <= 1e-12 * np.linalg.norm(x_nti)
+    A = P.assemble_dense(spec, grid, P.PLAIN, np.arange(grid.n), np.arange(grid.n))
+    assert np.linalg.norm(A @ x_ti - v) / np.linalg.norm(v) <= 1e-8

@@ -62,3 +62,28 @@ def test_emulated_shards_compressed_path():
         assert np.linalg.norm(x - xr) <= 1e-12 * np.linalg.norm(xr)
         xg = gold["solve_nonsym64_leaf64_x"]
         assert np.linalg.norm(x - xg) / np.linalg.norm(xg) <= 1e-8
+
+
+def test_emulated_shards_helmholtz_interior_retention():
+    """Helmholtz above the oscillatory threshold (kappa = k / 2pi >= 16): the
+    sharded path annotates the same a-priori skeletons as compress_inverse
+    (interface-interior retention included, solver_compressed.py:536-542), so
+    it reproduces the single-GPU compressed solve."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200.distributed import ShardedInverse
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    k = 2 * np.pi * 17.0
+    spec = P.KernelSpec("helmholtz2d", k=k, b_field=P.make_field("gaussian_bump"),
+                        c_field=P.make_field("one"))
+    grid = P.Grid(64)
+    opts = P.SolverOptions(eps=1e-8, leaf_size=64, k_cut=64)
+    assert opts.keep_interface_interior(spec)
+    tree1 = P.build_tree(grid, 64)
+    inv1 = compress_inverse(spec, grid, tree=tree1, eps=1e-8, opts=opts)
+    f = np.exp(1j * k * (grid.points()[:, 0] + 1.0))
+    xr = inv1.apply(f)
+    tree2 = P.build_tree(grid, 64)
+    x = ShardedInverse(spec, grid, tree2, 1e-8, opts, P.PLAIN, 2, emulate=True).apply(f)
+    for a, b in zip(tree1.nodes, tree2.nodes):
+        assert np.array_equal(a.sk_idx, b.sk_idx)
+    assert np.linalg.norm(x - xr) <= 1e-11 * np.linalg.norm(xr)

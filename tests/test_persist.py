@@ -43,6 +43,24 @@ def test_format_roundtrip_cpu(tmp_path):
     assert out[2] == {"lst": [1, 2, "a"], "f": 0.25}
 
 
+def test_problem_header_is_plain_json(tmp_path):
+    """The problem description is JSON (no pickle): spec, fields, quadrature,
+    options and level slices round-trip through their own constructors."""
+    import json
+    from paper_1303_5466_b200 import CELL, KernelSpec, SolverOptions, make_field
+    spec = KernelSpec("helmholtz2d", k=20.0, b_field=make_field("centre_bump", scale=-400.0,
+                                                                 base=0.0, amp=1.0, width=0.09))
+    pb = {"spec": spec, "quad": CELL, "opts": SolverOptions(eps=1e-8, leaf_size=64, k_cut=None),
+          "eps": 1e-8, "n_side": 16, "n_max": 64, "level_slices": {2: (0, 2), 3: (0, 4)},
+          "ti_mode": False}
+    kind, back, _ = _roundtrip(tmp_path, [None], pb)
+    assert back == pb
+    path = str(tmp_path / "f.vief")
+    hdr = persist.read_header(path)
+    assert json.loads(json.dumps(hdr)) == hdr
+    assert "pickle" not in open(persist.__file__).read().replace("no pickle", "")
+
+
 def test_format_alignment_and_magic(tmp_path):
     path = str(tmp_path / "f.vief")
     persist.write_state(path, {}, "test", [{"a": torch.ones(3, dtype=torch.float64),
