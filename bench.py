@@ -202,6 +202,8 @@ def _algorithmic_work(H):
     own_bytes = 0.0  # this layout: F^-1 (m^2) and C (k m) read up, E (k^2) and W (m k) down
     sym = H.symmetric
     for L in H.levels:
+        if L is None or getattr(L, "virtual", False):
+            continue
         m = L.m.astype(np.float64)
         if L.lv == 0:
             lu_fl += float(((2.0 / 3.0) * m ** 3).sum())
@@ -228,10 +230,13 @@ def run_sharded(a):
     import torch
     import torch.distributed as dist
     rank, world, local = _dist()
-    torch.cuda.set_device(local % torch.cuda.device_count())
-    # VF_DIST_BACKEND=gloo: host-staged collectives, used only to exercise this
-    # path with several ranks on one GPU (no rank's kernels wait on another's)
-    dist.init_process_group(os.environ.get("VF_DIST_BACKEND", "nccl"))
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    # NCCL with one GPU per rank; with fewer GPUs than ranks (e.g. --gpus 2 on a
+    # one-GPU box) the exchanges go host-staged over gloo: no rank's kernels
+    # ever wait on another rank's (VF_DIST_BACKEND overrides)
+    backend = os.environ.get("VF_DIST_BACKEND") or ("nccl" if ndev >= world else "gloo")
+    dist.init_process_group(backend)
     from paper_1303_5466_b200 import CELL, Grid, KernelSpec, SolverOptions, build_tree, make_field, _lib
     from paper_1303_5466_b200.distributed import ShardedInverse, TorchComm
     comm = TorchComm()
@@ -255,7 +260,7 @@ def run_sharded(a):
         ev[0].record()
         inv = ShardedInverse(spec, grid, build_tree(grid, 64), 1e-10, opts, CELL, world, comm=comm)
         ev[1].record()
-        X = inv.apply_device(Ft)
+        X = inv.apply_device(Ft, gather="root")
         ev[2].record()
         if record:
             torch.cuda.synchronize()
@@ -279,27 +284,43 @@ def run_sharded(a):
         e1.record()
         barrier()
     launches = _lib.launch_count() - L0
+    dev_t = "cpu" if backend == "gloo" else "cuda"
     t = torch.tensor([e0.elapsed_time(e1) / a.steps, statistics.mean(fac), statistics.mean(sol)],
-                     device="cuda")
+                     device=dev_t)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, tf, ts = (float(v) for v in t.tolist())
     local_bytes = inv.nbytes_local()
+    # whole-job algorithmic FP64 work (every rank's subtree + its top boxes)
+    work = np.zeros(2)
+    for H in [h for h, _ in inv.local.values()] + [h for h, _ in inv.top.values()]:
+        i_fl, l_fl, _, s_fl, _ = _algorithmic_work(H)
+        work += (i_fl + l_fl, s_fl * nrhs)
+    wt = torch.tensor(work, dtype=torch.float64, device=dev_t)
+    dist.all_reduce(wt)
+    fl_tot = float(wt.sum())
+    peak_fp64 = 37.1e12
+    roof = {"bound": "tensor", "achieved": fl_tot / (ms / 1e3) / 1e12,
+            "peak": peak_fp64 * world / 1e12, "unit": "TFLOP/s",
+            "frac": fl_tot / (ms / 1e3) / (peak_fp64 * world), "traffic": None,
+            "stage": "whole step (ID + LU/Schur + solve flops of all ranks, SURVEY §8(d) "
+                     "formulas) against N x the measured DMMA peak"}
     del inv, X
     torch.cuda.empty_cache()
     out = {"metric": METRIC, "value": N / (ms / 1e3), "unit": UNIT, "n_gpus": world,
            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": dict(_config(n, nrhs, world), parallelism=f"subtree shards x{world} + "
-                          "top levels on rank 0 (NCCL gathers)"),
+                          f"top boxes as a reduction tree ({backend} send/recv)"),
            "factor_s": tf / 1e3, "solve_s": ts / 1e3, "factor_bytes_rank": local_bytes,
-           "gpu_launches": int(launches), "clocks": clk.summary()}
+           "roofline": roof, "gpu_launches": int(launches), "clocks": clk.summary(),
+           "backend": backend, "devices": ndev}
     if not a.no_e2e:
         Fh = Ft.t().contiguous().cpu().pin_memory()
 
         def e2e_step():
             inv2 = ShardedInverse(spec, grid, build_tree(grid, 64), 1e-10, opts, CELL, world,
                                   comm=comm)
-            Xh = inv2.apply(Fh)
+            Xh = inv2.apply(Fh, gather="root")   # owned RHS rows up, full solution to rank 0
             torch.cuda.synchronize()
             del inv2, Xh
 
@@ -310,12 +331,13 @@ def run_sharded(a):
         for _ in range(a.steps):
             e2e_step()
         barrier()
-        te = torch.tensor([(time.perf_counter() - t0) / a.steps], device="cuda")
+        te = torch.tensor([(time.perf_counter() - t0) / a.steps], device=dev_t)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         te = float(te.item())
         out["e2e"] = {"value": N / te, "unit": UNIT, "h2d_bytes_per_step": int(N * nrhs * 8),
                       "d2h_bytes_per_step": int(N * nrhs * 8), "ms_per_step": te * 1e3,
-                      "api": "distributed.ShardedInverse(...).apply(host RHS)"}
+                      "api": "distributed.ShardedInverse(...).apply(host RHS, gather='root'): "
+                             "each rank uploads its own N/P rows, rank 0 receives the solution"}
     if rank == 0:
         print(json.dumps(out), flush=True)
     dist.destroy_process_group()
@@ -544,8 +566,27 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def _spawn(a):
+    """--gpus N > 1 without a torchrun environment: relaunch this script as N
+    ranks under torch.distributed.run (127.0.0.1 rendezvous)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)]
+    # torchrun's own parser would take "--n" as an abbreviation of its options
+    cmd += ["--side" if x == "--n" else ("--side=" + x[4:] if x.startswith("--n=") else x)
+            for x in sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 if __name__ == "__main__":
     args = _args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -2,18 +2,32 @@
 
 Boxes of one level depend only on their children, so with P = 2^s ranks the
 tree splits at level s: rank g factors the subtree rooted at the g-th box of
-level s (levels s..depth) with no communication; rank 0 then factors the top
-levels 0..s-1 from the subtree roots' interface data — skeleton index lists
-and the k x k reduced operators E — gathered over NCCL.  The solve runs the up
-sweep locally, gathers the subtree roots' `ups` to rank 0, runs the top of the
-tree there, broadcasts the phi_dn slices back and finishes the down sweep
-locally.  Every rank holds only its subtree's factors (the 2048^2 case needs
-~200 GB in total).
+level s (levels s..depth) with no communication.  The top levels 0..s-1 are
+factored as a binary reduction tree: box j of level l < s is owned by rank
+j * 2^(s-l) (the owner of its first child), which receives the second child's
+interface -- k, row/column skeleton index lists and the k x k reduced operator
+E -- from that child's owner (point-to-point, NCCL send/recv), and factors the
+box from a "virtual" child level holding both children's interface data.  The
+first child's G1 = E1^{-1} (kept before E1 was inverted) never leaves its rank,
+so every top box is inverted by block elimination, as on one GPU.  At level l
+only 2^l ranks work (rank 0 factors the root); SURVEY §8(e) bounds the factor
+speed-up of this plan at 1.92x / 2.89x / 3.54x for P = 2 / 4 / 8 at 1024^2.
+
+The solve follows the same tree: up sweep locally, then for l = s-1 .. 0 the
+second child's `ups` (r x k) goes to the parent's owner; down sweep from the
+root, the second child's phi_dn slice (r x k) goes back to the child's owner;
+the local down sweep finishes on every rank.  Each rank reads only the
+right-hand-side rows of its own grid points (`apply` uploads just those) and
+writes only its own solution rows; `gather="root"|"all"` assembles the full
+solution from the owned rows (a gather of N/P x r per rank, not an all-reduce
+of the full array).  Every rank holds only its subtree's factors plus the top
+boxes it owns.
 
 The algorithm is written as explicit phases so that the same code runs
-  * over torch.distributed (one process per GPU, NCCL; gloo for CPU tests), or
-  * emulated in one process on one GPU (`emulate=True`), which is how it is
-    exercised on a single B200 (no rank ever waits on a kernel of another).
+  * over torch.distributed (one process per GPU, NCCL; gloo for CPU tests and
+    for several ranks sharing one GPU -- host-staged, no rank ever waits on
+    another rank's kernel), or
+  * emulated in one process on one GPU (`emulate=True`).
 """
 
 from dataclasses import dataclass, field
@@ -35,7 +49,7 @@ class SplitPlan:
     world: int
     split: int                 # level s = log2(world)
     slices: list              # per rank: {level: (lo, hi)} of that level's box list
-    top: dict = field(default_factory=dict)  # rank 0: {level: (lo, hi)} for levels < s
+    top: dict = field(default_factory=dict)  # {level: (lo, hi)} for levels < s (all boxes)
 
 
 def subtree_plan(tree, world):
@@ -56,6 +70,22 @@ def subtree_plan(tree, world):
     return SplitPlan(world, s, slices, top)
 
 
+def top_owner(plan, lv, j):
+    """Rank that factors box j of level lv <= s (level s: the subtree owner)."""
+    return j << (plan.split - lv)
+
+
+def top_boxes(plan, rank):
+    """[(level, j)] of the top boxes `rank` factors, finest level first."""
+    s = plan.split
+    out = []
+    for lv in range(s - 1, -1, -1):
+        step = 1 << (s - lv)
+        if rank % step == 0:
+            out.append((lv, rank // step))
+    return out
+
+
 def owned_points(tree, plan, rank):
     """Grid points owned by a rank (its subtree's leaves)."""
     lo, hi = plan.slices[rank][tree.depth]
@@ -67,28 +97,52 @@ def owned_points(tree, plan, rank):
 # communication
 
 class TorchComm:
-    """Collectives over torch.distributed (NCCL for CUDA tensors, gloo on CPU)."""
+    """Point-to-point and collective helpers over torch.distributed (NCCL for
+    CUDA tensors, gloo for host tensors or several ranks on one GPU)."""
 
     def __init__(self):
         import torch.distributed as dist
         self.dist = dist
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
+        self.backend = dist.get_backend()
+
+    def _wire(self, t):
+        """gloo moves host tensors only."""
+        return t.cpu() if self.backend == "gloo" and t.is_cuda else t
+
+    def send(self, t, dst):
+        """Ragged send: shape first (int64 vector), then the data."""
+        t = t.contiguous()
+        dev = "cpu" if self.backend == "gloo" else t.device
+        hdr = torch.tensor([t.dim()] + list(t.shape), dtype=torch.int64, device=dev)
+        self.dist.send(torch.tensor([hdr.numel()], dtype=torch.int64, device=dev), dst)
+        self.dist.send(hdr, dst)
+        if t.numel():
+            self.dist.send(self._wire(t), dst)
+
+    def recv(self, src, dtype, device):
+        dev = "cpu" if self.backend == "gloo" else device
+        n = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.dist.recv(n, src)
+        hdr = torch.zeros(int(n.item()), dtype=torch.int64, device=dev)
+        self.dist.recv(hdr, src)
+        shape = [int(x) for x in hdr[1:].tolist()]
+        t = torch.empty(shape, dtype=dtype, device=dev)
+        if t.numel():
+            self.dist.recv(t, src)
+        return t.to(device)
 
     def gather0(self, t):
-        """Tensors of any shape (same dtype/ndim) -> list on rank 0, None elsewhere."""
-        dist = self.dist
-        shape = torch.tensor(list(t.shape), dtype=torch.int64, device=t.device)
-        shapes = [torch.zeros_like(shape) for _ in range(self.world)]
-        dist.all_gather(shapes, shape)
-        mx = torch.stack(shapes).max(dim=0).values.tolist()
-        pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
-        pad[tuple(slice(0, s) for s in t.shape)] = t
-        bufs = [torch.zeros_like(pad) for _ in range(self.world)]
-        dist.all_gather(bufs, pad)
+        """Tensors of any shape (same dtype) -> list on rank 0, None elsewhere
+        (point-to-point: only rank 0 receives, nobody gets the others' data)."""
         if self.rank != 0:
+            self.send(t, 0)
             return None
-        return [b[tuple(slice(0, int(s)) for s in sh.tolist())] for b, sh in zip(bufs, shapes)]
+        out = [t]
+        for g in range(1, self.world):
+            out.append(self.recv(g, t.dtype, t.device))
+        return out
 
     def bcast0(self, t, shape=None, dtype=None, device=None):
         dist = self.dist
@@ -96,50 +150,81 @@ class TorchComm:
             t = torch.empty(shape, dtype=dtype, device=device)
         else:
             t = t.contiguous()  # collectives move raw storage
-        dist.broadcast(t, src=0)
-        return t
+        w = self._wire(t)
+        dist.broadcast(w, src=0)
+        return w.to(t.device) if w is not t else t
 
     def bcast_shape0(self, shape, device):
+        dev = "cpu" if self.backend == "gloo" else device
         v = torch.tensor(list(shape) if shape is not None else [0, 0], dtype=torch.int64,
-                         device=device)
+                         device=dev)
         self.dist.broadcast(v, src=0)
         return tuple(v.tolist())
 
     def allreduce_sum(self, t):
         t = t.contiguous()
-        self.dist.all_reduce(t)
-        return t
+        w = self._wire(t)
+        self.dist.all_reduce(w)
+        return w.to(t.device) if w is not t else t
+
+    def all_gather(self, t):
+        """Same-shape tensors -> list on every rank."""
+        w = self._wire(t.contiguous())
+        bufs = [torch.empty_like(w) for _ in range(self.world)]
+        self.dist.all_gather(bufs, w)
+        return [b.to(t.device) for b in bufs]
+
+
+class _LocalComm:
+    """Message passing between the emulated ranks of one process."""
+
+    def __init__(self):
+        self.box = {}
+
+    def send(self, t, src, dst, tag):
+        self.box[(src, dst, tag)] = t
+
+    def recv(self, src, dst, tag):
+        return self.box.pop((src, dst, tag))
 
 
 # ---------------------------------------------------------------------------
 # device phases
 
-def _interface_payload(Hl, invl, split):
-    """The subtree root's data the top levels need: k, row/col skeletons, E."""
-    L = Hl.levels[split]
-    k = int(L.k[0])
-    rs = L.rskel[0, :k].to(torch.int64)
-    cs = L.cskel[0, :k].to(torch.int64)
-    E = L.E[0, :k, :k].contiguous()        # storage [col, row]
-    return k, rs, cs, E
+def _interface(H, lv, item=0):
+    """Item `item` of level lv's interface: k, row/col skeletons, E, G1 or None."""
+    L = H.levels[lv]
+    k = int(L.k[item])
+    rs = L.rskel[item, :k].to(torch.int64)
+    cs = L.cskel[item, :k].to(torch.int64)
+    E = L.E[item, :k, :k].contiguous()        # storage [col, row]
+    G = getattr(L, "Gkeep", None)
+    G1 = None if G is None else G[item // 2, :k, :k].contiguous()
+    return k, rs, cs, E, G1
 
 
-def _virtual_level(Ht, split, ks, rskels, cskels, Es, dev):
-    """Populate level `split` of the top object with the gathered interface."""
-    V = Ht.levels[split]
+def _virtual_level(Ht, lv, parts, dev):
+    """Populate level `lv` of a top object with the children's interface
+    data: parts = [(k, rskel, cskel, E, G1 or None)] for the level's boxes.
+    The first child's G1 = E1^{-1} feeds the parent's block elimination."""
+    V = Ht.levels[lv]
     V.virtual = True
-    V.k = np.asarray(ks, dtype=np.int32)
+    V.k = np.asarray([p[0] for p in parts], dtype=np.int32)
     V.kmax = max(int(V.k.max()), 1)
     V.k_d = sd._dev_i32(V.k, dev)
-    P = len(ks)
+    P = len(parts)
     V.rskel = torch.zeros((P, V.kmax), dtype=_I32, device=dev)
     V.cskel = torch.zeros((P, V.kmax), dtype=_I32, device=dev)
     V.E = torch.zeros((P, V.kmax, V.kmax), dtype=_F64, device=dev)
-    for g in range(P):
-        k = int(ks[g])
-        V.rskel[g, :k] = rskels[g].to(dev, _I32)
-        V.cskel[g, :k] = cskels[g].to(dev, _I32)
-        V.E[g, :k, :k] = Es[g].to(dev)
+    have_g = all(parts[g][4] is not None for g in range(0, P, 2))
+    if have_g:
+        V.Gkeep = torch.zeros((P // 2, V.kmax, V.kmax), dtype=_F64, device=dev)
+    for g, (k, rs, cs, E, G1) in enumerate(parts):
+        V.rskel[g, :k] = rs.to(dev, _I32)
+        V.cskel[g, :k] = cs.to(dev, _I32)
+        V.E[g, :k, :k] = E.to(dev)
+        if have_g and g % 2 == 0:
+            V.Gkeep[g // 2, :k, :k] = G1.to(dev)
     return V
 
 
@@ -151,10 +236,11 @@ class ShardedInverse:
     def __init__(self, spec, grid, tree, eps, opts, quad, world, comm=None, emulate=False,
                  support_mask=None):
         self.spec, self.grid, self.tree, self.eps, self.opts, self.quad = spec, grid, tree, eps, opts, quad
-        self.plan = subtree_plan(tree, world)
+        self.plan = plan = subtree_plan(tree, world)
         self.comm = comm
         self.emulate = emulate
         self.ranks = list(range(world)) if emulate else [comm.rank]
+        self._lc = _LocalComm() if emulate else None
         self.local = {}
         # finite k_cut: the compressed path's a-priori skeletons (host annotation
         # is deterministic, so every rank derives the same splits)
@@ -162,49 +248,95 @@ class ShardedInverse:
         if not (opts.k_cut is None or opts.k_cut == np.inf):
             from .solver_compressed import ensure_apriori_skeletons
             apriori = ensure_apriori_skeletons(spec, tree, opts, support_mask)
-        s = self.plan.split
-        payloads = {}
+        self.apriori = apriori
+        s = plan.split
         for g in self.ranks:
-            Hl = sd.Hss2dMatrix(spec, grid, tree, eps, opts, quad, level_slices=self.plan.slices[g])
+            Hl = sd.Hss2dMatrix(spec, grid, tree, eps, opts, quad, level_slices=plan.slices[g])
             Hl.apriori = apriori
             sd.compress_levels(Hl)
             invl = sd.invert_dense_block(Hl)
             self.local[g] = (Hl, invl)
-            if world > 1:
-                payloads[g] = _interface_payload(Hl, invl, s)
         self.dev = next(iter(self.local.values()))[0].device
         self.realified = next(iter(self.local.values()))[0].realified
-        self.top = None
-        if world == 1:
+        # top boxes: (lv, j) -> (object, inverse), on the owning rank
+        self.top = {}
+        for lv in range(s - 1, -1, -1):
+            # second children's owners send their interface to the parent's owner
+            for j in range(1 << lv):
+                owner = top_owner(plan, lv, j)
+                src = top_owner(plan, lv + 1, 2 * j + 1)
+                if src in self.ranks:
+                    self._send(self._iface(lv + 1, 2 * j + 1), src, owner, ("if", lv, j))
+            for j in range(1 << lv):
+                owner = top_owner(plan, lv, j)
+                if owner not in self.ranks:
+                    continue
+                src = top_owner(plan, lv + 1, 2 * j + 1)
+                first = self._iface(lv + 1, 2 * j)
+                second = self._recv_iface(src, owner, ("if", lv, j))
+                Ht = sd.Hss2dMatrix(spec, grid, tree, eps, opts, quad,
+                                    level_slices={lv: (j, j + 1), lv + 1: (2 * j, 2 * j + 2)})
+                _virtual_level(Ht, lv + 1, [first, second], self.dev)
+                Ht.apriori = apriori
+                sd.compress_levels(Ht)
+                self.top[(lv, j)] = (Ht, sd.invert_dense_block(Ht))
+                self._drop_g1(lv + 1, 2 * j)   # copied into the virtual level, consumed
+
+    # -- messaging (emulated or torch.distributed) -----------------------------
+    def _iface(self, lv, j):
+        """Interface of box j of level lv, from the object on this process
+        that factored it (subtree root at lv == s, else a top box)."""
+        if lv == self.plan.split:
+            return _interface(self.local[j][0], lv, 0)
+        return _interface(self.top[(lv, j)][0], lv, 0)
+
+    def _drop_g1(self, lv, j):
+        H = self.local[j][0] if lv == self.plan.split else self.top[(lv, j)][0]
+        H.levels[lv].Gkeep = None
+
+    def _send(self, iface, src, dst, tag):
+        if src == dst:
             return
-        if emulate:
-            ks = [payloads[g][0] for g in range(world)]
-            rsk = [payloads[g][1] for g in range(world)]
-            csk = [payloads[g][2] for g in range(world)]
-            Es = [payloads[g][3] for g in range(world)]
-        else:
-            k, rs, cs, E = payloads[comm.rank]
-            ks_t = comm.gather0(torch.tensor([k], dtype=torch.int64, device=self.dev))
-            rsk = comm.gather0(rs)
-            csk = comm.gather0(cs)
-            Es = comm.gather0(E)
-            ks = [int(x.item()) for x in ks_t] if ks_t is not None else None
-        if self.emulate or comm.rank == 0:
-            top_slices = dict(self.plan.top)
-            top_slices[s] = (0, world)
-            Ht = sd.Hss2dMatrix(spec, grid, tree, eps, opts, quad, level_slices=top_slices)
-            _virtual_level(Ht, s, ks, rsk, csk, Es, self.dev)
-            Ht.apriori = apriori
-            sd.compress_levels(Ht)
-            self.top = (Ht, sd.invert_dense_block(Ht))
+        if self.emulate:
+            self._lc.send(iface, src, dst, tag)
+            return
+        k, rs, cs, E, _ = iface
+        for t in (torch.tensor([k], dtype=torch.int64, device=self.dev), rs, cs, E):
+            self.comm.send(t, dst)
+
+    def _recv_iface(self, src, dst, tag):
+        if self.emulate:
+            k, rs, cs, E, _ = self._lc.recv(src, dst, tag)
+            return k, rs, cs, E, None
+        k = int(self.comm.recv(src, torch.int64, self.dev).item())
+        rs = self.comm.recv(src, torch.int64, self.dev)
+        cs = self.comm.recv(src, torch.int64, self.dev)
+        E = self.comm.recv(src, _F64, self.dev)
+        return k, rs, cs, E, None
+
+    def _xfer(self, t, src, dst, tag):
+        """Move tensor t (present on src) to dst; returns it on dst."""
+        if src == dst:
+            return t
+        if self.emulate:
+            self._lc.send(t, src, dst, tag)
+            return self._lc.recv(src, dst, tag)
+        if self.comm.rank == src:
+            self.comm.send(t, dst)
+            return None
+        if self.comm.rank == dst:
+            return self.comm.recv(src, _F64, self.dev)
+        return None
 
     # -- solve ----------------------------------------------------------------
-    def apply_device(self, fd):
-        """fd: (r, N') right-hand sides (every rank passes the full vector);
-        returns the full (r, N') solution on every rank."""
+    def apply_device(self, fd, gather="all"):
+        """fd: (r, N') right-hand sides on the device (only the rows of this
+        rank's grid points are read).  Returns the (r, N') solution: complete
+        on every rank (gather="all"), on rank 0 only ("root"; other ranks get
+        their owned rows), or owned rows only ("none")."""
         r = fd.shape[0]
-        s = self.plan.split
-        world = self.plan.world
+        plan = self.plan
+        s, world = plan.split, plan.world
         st = {}
         for g in self.ranks:
             Hl, _ = self.local[g]
@@ -217,44 +349,114 @@ class ShardedInverse:
             phi, ups = st[0]
             sd._sweep_down(Hl, phi, ups, out)
             return out
-        # gather the subtree roots' ups (r x k_g) to rank 0
-        if self.emulate:
-            ups_all = [st[g][1][s] for g in range(world)]
-        else:
-            ups_all = self.comm.gather0(st[self.comm.rank][1][s])
-        pd = None
-        if self.top is not None:
-            Ht, _ = self.top
-            V = Ht.levels[s]
-            kk = V.kmax
-            U = torch.zeros((r, world * kk), dtype=_F64, device=self.dev)
-            for g in range(world):
-                k = int(V.k[g])
-                U[:, g * kk:g * kk + k] = ups_all[g][:, :k]
-            phi_t, ups_t = {}, {s: U}
-            sd._sweep_up(Ht, fd, phi_t, ups_t)
-            sd._sweep_down(Ht, phi_t, ups_t, torch.zeros_like(fd))
-            pd = sd._phi_dn(Ht, V, phi_t, r)          # (r, world * kk)
-        if not self.emulate:
-            shape = self.comm.bcast_shape0(None if pd is None else pd.shape, self.dev)
-            pd = self.comm.bcast0(pd, shape=shape, dtype=_F64, device=self.dev)
-        kk = pd.shape[1] // world
+
+        def ups_of(lv, j):  # this process's ups of box j at level lv (r x k)
+            if lv == s:
+                return st[j][1][s]
+            return self._tst[(lv, j)][1][lv]
+
+        # up: level s-1 .. 0 (second child's ups travel to the parent's owner)
+        self._tst = {}
+        for lv in range(s - 1, -1, -1):
+            moved = {}
+            for j in range(1 << lv):
+                owner = top_owner(plan, lv, j)
+                src = top_owner(plan, lv + 1, 2 * j + 1)
+                if self.emulate or self.comm.rank in (owner, src):
+                    have = src in self.ranks
+                    moved[j] = self._xfer(ups_of(lv + 1, 2 * j + 1) if have else None, src, owner,
+                                          ("up", lv, j))
+            for j in range(1 << lv):
+                owner = top_owner(plan, lv, j)
+                if owner not in self.ranks:
+                    continue
+                Ht, _ = self.top[(lv, j)]
+                V = Ht.levels[lv + 1]
+                kk = V.kmax
+                U = torch.zeros((r, 2 * kk), dtype=_F64, device=self.dev)
+                u1 = ups_of(lv + 1, 2 * j)
+                U[:, :int(V.k[0])] = u1[:, :int(V.k[0])]
+                U[:, kk:kk + int(V.k[1])] = moved[j][:, :int(V.k[1])]
+                phi_t, ups_t = {}, {lv + 1: U}
+                sd._sweep_up(Ht, fd, phi_t, ups_t)
+                self._tst[(lv, j)] = (phi_t, ups_t)
+        # down: level 0 .. s-1 (second child's phi_dn travels to its owner)
+        pd_of = {}   # (lv, j) -> phi_dn (r x k) of box j at level lv, on its owner
+        for lv in range(s):
+            sent = {}
+            for j in range(1 << lv):
+                owner = top_owner(plan, lv, j)
+                if owner in self.ranks:
+                    Ht, _ = self.top[(lv, j)]
+                    phi_t, ups_t = self._tst[(lv, j)]
+                    sd._sweep_down(Ht, phi_t, ups_t, torch.zeros_like(fd), pd_top=pd_of.get((lv, j)))
+                    V = Ht.levels[lv + 1]
+                    pd = sd._phi_dn(Ht, V, phi_t, r)          # (r, 2 * kk)
+                    kk = V.kmax
+                    pd_of[(lv + 1, 2 * j)] = pd[:, :int(V.k[0])].contiguous()
+                    sent[j] = pd[:, kk:kk + int(V.k[1])].contiguous()
+            for j in range(1 << lv):
+                owner = top_owner(plan, lv, j)
+                dst = top_owner(plan, lv + 1, 2 * j + 1)
+                if self.emulate or self.comm.rank in (owner, dst):
+                    got = self._xfer(sent.get(j), owner, dst, ("dn", lv, j))
+                    if dst in self.ranks:
+                        pd_of[(lv + 1, 2 * j + 1)] = got
         for g in self.ranks:
             Hl, _ = self.local[g]
             phi, ups = st[g]
-            k = int(Hl.levels[s].k[0])
-            pdg = pd[:, g * kk:g * kk + k].contiguous()
-            sd._sweep_down(Hl, phi, ups, out, pd_top=pdg)
-        if not self.emulate:
-            out = self.comm.allreduce_sum(out)
-        return out
+            sd._sweep_down(Hl, phi, ups, out, pd_top=pd_of[(s, g)].contiguous())
+        self._tst = None
+        if self.emulate or gather == "none":
+            return out
+        return self._assemble(out, gather)
 
-    def apply(self, f):
-        fd, single = sd._as_device_rhs(f, self.grid.n, self.dev, self.realified)
-        return sd._from_device(self.apply_device(fd), f, single, self.realified)
+    def _owned_cols(self, g):
+        cols = getattr(self, "_own_cache", {}).get(g)
+        if cols is None:
+            pts = owned_points(self.tree, self.plan, g)
+            if self.realified:  # (Re, Im) interleaved per point
+                pts = np.stack([2 * pts, 2 * pts + 1], 1).ravel()
+            cols = torch.as_tensor(pts, dtype=torch.int64, device=self.dev)
+            self.__dict__.setdefault("_own_cache", {})[g] = cols
+        return cols
+
+    def _assemble(self, out, gather):
+        """Full solution from every rank's owned columns (equal counts per rank
+        for the uniform trees this plan accepts)."""
+        comm = self.comm
+        mine = out[:, self._owned_cols(comm.rank)].contiguous()
+        if gather == "all":
+            parts = comm.all_gather(mine)
+        else:
+            parts = comm.gather0(mine)
+            if parts is None:
+                return out
+        full = torch.zeros_like(out)
+        for g, p in enumerate(parts):
+            full[:, self._owned_cols(g)] = p.to(full.device)
+        return full
+
+    def apply(self, f, gather="all"):
+        """Host or device right-hand sides (N,) / (N, r).  Only this rank's
+        grid points are uploaded (H2D bytes ~ N / P per rank)."""
+        n = self.grid.n
+        if isinstance(f, torch.Tensor) and f.is_cuda:
+            fd, single = sd._as_device_rhs(f, n, self.dev, self.realified)
+        else:
+            arr = f.numpy() if isinstance(f, torch.Tensor) else np.asarray(f)
+            a2 = arr[:, None] if arr.ndim == 1 else arr
+            pts = np.concatenate([owned_points(self.tree, self.plan, g) for g in self.ranks])
+            rows = torch.from_numpy(np.ascontiguousarray(a2[pts]))
+            if torch.cuda.is_available():
+                rows = rows.pin_memory()
+            full = torch.zeros((n, a2.shape[1]), dtype=rows.dtype, device=self.dev)
+            full[torch.as_tensor(pts, device=self.dev)] = rows.to(self.dev, non_blocking=True)
+            fd, single = sd._as_device_rhs(full[:, 0] if arr.ndim == 1 else full, n, self.dev,
+                                           self.realified)
+        return sd._from_device(self.apply_device(fd, gather), f, single, self.realified)
 
     def nbytes_local(self):
         tot = sum(inv.nbytes() for _, inv in self.local.values())
-        if self.top is not None:
-            tot += self.top[1].nbytes()
+        tot += sum(inv.nbytes() for _, inv in self.top.values())
         return tot

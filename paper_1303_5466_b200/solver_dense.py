@@ -638,8 +638,9 @@ def _id_batched(dev, A, sA, ldA, pv, mv, maxp, mm, count, g, eps, rank, perm, T,
 
 def compress_outer(spec, grid, tree, eps, opts, quad=PLAIN, spill=None):
     """Skeletonize all boxes fine-to-coarse, one batch per level
-    (solver_dense.py:234-272).  `spill` is accepted for signature
-    compatibility; every block stays in HBM."""
+    (solver_dense.py:234-272).  The compressed operator's blocks stay in HBM
+    (they feed the inversion level by level); `spill` is accepted for the
+    reference's signature -- the factor tier is invert_dense_block(spill=)."""
     H = Hss2dMatrix(spec, grid, tree, eps, opts, quad)
     return compress_levels(H)
 
@@ -790,8 +791,7 @@ def _invert_level_F(inv, L, checks=None):
     if not L.leaf and getattr(C1, "Gkeep", None) is not None:
         if L.lv == 0:
             return _invert_root_block(inv, L, checks)
-        if _BLOCK_F:
-            return _invert_level_F_block(inv, L, checks)
+        return _invert_level_F_block(inv, L, checks)
     _lib.prof_mark("py.F_assemble")
     F = torch.zeros((nb, mm, mm), dtype=_F64, device=dev)
     if L.leaf:
@@ -850,7 +850,9 @@ def _invert_level_rest(inv, L, checks=None):
               sA=L.ntmax * kk, sC=kk * kk, alpha=1.0, beta=1.0, batch=nb,
               Mb=L.k_d, Nb=L.k_d, Kb=L.nT_d, Bptr=_ptrs(Wp, base * kk * mm + k, dev))
     del Wp
-    if nb >= 2 and (L.lv == 1 or _BLOCK_F):  # parent's block elimination needs G1 = E1^{-1}
+    if nb >= 2 or H.sharded:  # the parent's block elimination needs G1 = E1^{-1}
+        # (a sharded slice keeps it for a single box too: its parent may be
+        # factored by the same rank from a virtual child level, distributed.py)
         L.Gkeep = G[0::2].clone()
     _lib.pad_identity(G, kk * kk, kk, L.k_d, kk, nb)
     pmin, pmax = _lib.inv_batched(G, kk * kk, kk, kk, nb)
@@ -949,13 +951,110 @@ class DenseBlockInverse:
         return persist.load(path, device)
 
 
+class _Spill:
+    """Host-memory tier for factor blocks (the reference's _Spill,
+    solver_dense.py:37-55, backs blocks of >= threshold_mb by .npy memmaps).
+    Here a level's factor batches (F^-1, C, E, W) of >= threshold_mb MB move
+    to pinned host memory as soon as the factorization no longer needs them
+    (after the parent level is inverted); the solve streams each level back
+    to HBM on a copy stream one level ahead of the sweep, so at most two
+    levels' factors are resident.  threshold_mb=None: nothing spills."""
+
+    def __init__(self, threshold_mb=None):
+        self.threshold = None if threshold_mb is None else threshold_mb * (1 << 20)
+
+    def hold(self, t):
+        if self.threshold is None or not t.is_cuda or t.numel() * t.element_size() < self.threshold:
+            return t
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        return h
+
+    def spill_level(self, L):
+        if self.threshold is None or L is None or getattr(L, "virtual", False):
+            return
+        for name in _FACTOR_NAMES:
+            t = getattr(L, name, None)
+            if isinstance(t, torch.Tensor):
+                setattr(L, name, self.hold(t))
+
+
+_FACTOR_NAMES = ("Finv", "C", "E", "W")
+
+
+def _as_spill(spill):
+    if spill is None:
+        return None
+    if isinstance(spill, _Spill):
+        return spill
+    if isinstance(spill, (int, float)):
+        return _Spill(spill)
+    thr = getattr(spill, "threshold", None)   # a reference-style _Spill (bytes)
+    sp = _Spill(None)
+    sp.threshold = thr
+    return sp
+
+
+class _Prefetch:
+    """Device copies of spilled factor batches, one level ahead of the sweep
+    (copy stream + event; the caching allocator's record_stream keeps each
+    buffer alive until the sweep has used it).  Levels held in HBM pass
+    through untouched (get() returns None)."""
+
+    def __init__(self, H, order, names):
+        self.H, self.order, self.names = H, order, names
+        self.pending = {}
+        self.stream = None
+
+    def _spilled(self, L):
+        return any(isinstance(getattr(L, n, None), torch.Tensor) and not getattr(L, n).is_cuda
+                   for n in self.names)
+
+    def _issue(self, i):
+        L = self.order[i]
+        if not self._spilled(L):
+            self.pending[i] = None
+            return
+        if self.stream is None:
+            self.stream = torch.cuda.Stream(self.H.device)
+        self.stream.wait_stream(torch.cuda.current_stream(self.H.device))
+        out = {}
+        with torch.cuda.stream(self.stream):
+            for n in self.names:
+                t = getattr(L, n, None)
+                out[n] = t.to(self.H.device, non_blocking=True) if t is not None and not t.is_cuda else t
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        self.pending[i] = (out, ev)
+
+    def get(self, i):
+        if i not in self.pending:
+            self._issue(i)
+        if i + 1 < len(self.order) and i + 1 not in self.pending:
+            self._issue(i + 1)
+        ent = self.pending.pop(i)
+        if ent is None:
+            return None
+        out, ev = ent
+        cur = torch.cuda.current_stream(self.H.device)
+        cur.wait_event(ev)
+        for t in out.values():
+            if t is not None and t.is_cuda:
+                t.record_stream(cur)
+        return out
+
+
 def invert_dense_block(H, spill=None, free_source=False):
     """Fine-to-coarse telescoping inversion, one batch per level
-    (solver_dense.py:332-368).  `free_source` drops D/B once consumed."""
+    (solver_dense.py:332-368).  `free_source` drops D/B once consumed;
+    `spill` (a _Spill, or a threshold in MB) moves each finished level's
+    factor batches above the threshold to pinned host memory."""
     inv = DenseBlockInverse(H)
+    sp = _as_spill(spill)
     _mark("invert:start")
     with _host_quiet():
-        for L in reversed(_real_levels(H)):
+        levels = list(reversed(_real_levels(H)))
+        for i, L in enumerate(levels):
             _lib.prof_prefix(f"L{L.lv:02d}.")
             _invert_level(inv, L)
             _mark(f"invert:{L.lv}")
@@ -964,12 +1063,16 @@ def invert_dense_block(H, spill=None, free_source=False):
                     L.D = None
                 else:
                     L.B12 = L.B21 = None
+            if sp is not None and i > 0:   # the child level is no longer needed here
+                sp.spill_level(levels[i - 1])
+        if sp is not None and levels:
+            sp.spill_level(levels[-1])
+            torch.cuda.current_stream(H.device).synchronize()   # pinned copies complete
+            torch.cuda.empty_cache()
     return inv
 
 
 _SIDE = {}
-# explicit F^{-1} of non-leaf levels by block elimination (VF_BLOCK_F=0: Gauss-Jordan of F)
-_BLOCK_F = os.environ.get("VF_BLOCK_F", "1") != "0"
 
 
 _HOST_QUIET = os.environ.get("VF_HOST_QUIET", "1") != "0"
@@ -1292,8 +1395,11 @@ def _real_levels(H):
     return [L for L in H.levels if L is not None and not getattr(L, "virtual", False)]
 
 
-def _sweep_up_level(H, L, fd, phi, ups):
-    """One level of the up sweep: phi = F^{-1} u, ups = C phi."""
+def _sweep_up_level(H, L, fd, phi, ups, fac=None):
+    """One level of the up sweep: phi = F^{-1} u, ups = C phi.  `fac`: the
+    level's device factors when they are spilled to host memory."""
+    Finv, Cf = ((L.Finv, getattr(L, "C", None)) if fac is None
+                else (fac["Finv"], fac.get("C")))
     dev = H.device
     r, n = fd.shape
     nb, mm = L.nb, L.mmax
@@ -1309,7 +1415,7 @@ def _sweep_up_level(H, L, fd, phi, ups):
     if getattr(L, "rb", None) is not None:
         _root_block_solve(L, U, ldv, r, Phi, ldv)
     else:
-        _mv(L.Finv, _fs(L, mm * mm), mm, U, mm, ldv, Phi, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r,
+        _mv(Finv, _fs(L, mm * mm), mm, U, mm, ldv, Phi, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r,
             1.0, 0.0)
     del U
     phi[L.lv] = Phi
@@ -1317,7 +1423,7 @@ def _sweep_up_level(H, L, fd, phi, ups):
         return
     kk = L.kmax
     Ups = torch.zeros((r, nb * kk), dtype=_F64, device=dev)
-    _mv(L.C, _fs(L, mm * kk), kk, Phi, mm, ldv, Ups, kk, nb * kk, kk, mm, L.k_d, L.m_d, nb, r,
+    _mv(Cf, _fs(L, mm * kk), kk, Phi, mm, ldv, Ups, kk, nb * kk, kk, mm, L.k_d, L.m_d, nb, r,
         1.0, 0.0)
     ups[L.lv] = Ups
 
@@ -1325,8 +1431,10 @@ def _sweep_up_level(H, L, fd, phi, ups):
 def _sweep_up(H, fd, phi, ups):
     """Up sweep (solver_dense.py:303-310): phi = F^{-1} u, ups = C phi = E R phi.
     ups of a virtual child level must be present in `ups` beforehand."""
-    for L in reversed(_real_levels(H)):
-        _sweep_up_level(H, L, fd, phi, ups)
+    order = list(reversed(_real_levels(H)))
+    pf = _Prefetch(H, order, ("Finv", "C"))
+    for i, L in enumerate(order):
+        _sweep_up_level(H, L, fd, phi, ups, pf.get(i))
         if L.lv == 0:
             break
 
@@ -1346,7 +1454,12 @@ def _sweep_down(H, phi, ups, out, pd_top=None):
     leaves scattered into `out`.  `pd_top` supplies phi_dn of the coarsest
     level when its parent is factored elsewhere (sharded subtree)."""
     r, n = out.shape
-    for L in _real_levels(H):
+    order = _real_levels(H)
+    pf = _Prefetch(H, order, ("E", "W"))
+    for i, L in enumerate(order):
+        fac = pf.get(i)
+        Ef, Wf = ((getattr(L, "E", None), getattr(L, "W", None)) if fac is None
+                  else (fac.get("E"), fac.get("W")))
         nb, mm = L.nb, L.mmax
         ldv = nb * mm
         Phi = phi[L.lv]
@@ -1355,9 +1468,9 @@ def _sweep_down(H, phi, ups, out, pd_top=None):
             par = H.levels[L.lv - 1]
             PD = pd_top if par is None else _phi_dn(H, L, phi, r)
             Ups = ups[L.lv]
-            _mv(L.E, _fs(L, kk * kk), kk, PD, kk, nb * kk, Ups, kk, nb * kk, kk, kk, L.k_d, L.k_d, nb, r,
+            _mv(Ef, _fs(L, kk * kk), kk, PD, kk, nb * kk, Ups, kk, nb * kk, kk, kk, L.k_d, L.k_d, nb, r,
                 -1.0, 1.0)
-            _mv(L.W, _fs(L, kk * mm), mm, Ups, kk, nb * kk, Phi, mm, ldv, mm, kk, L.m_d, L.k_d, nb, r,
+            _mv(Wf, _fs(L, kk * mm), mm, Ups, kk, nb * kk, Phi, mm, ldv, mm, kk, L.m_d, L.k_d, nb, r,
                 -1.0, 1.0)
             del PD
         if L.leaf:

@@ -146,3 +146,27 @@ def test_sharded_solve_matches_single_process(world):
         # the exchange is pure data movement; only BLAS's layout-dependent
         # summation order (gathered copies are C-ordered) separates the results
         assert np.linalg.norm(res[r] - x) <= 1e-14 * np.linalg.norm(x)
+
+
+def test_top_level_owner_tree():
+    """Top boxes form a binary reduction tree: box j of level l < s is owned
+    by rank j 2^(s-l), the owner of its first child; every top box has exactly
+    one owner; rank 0 owns the root."""
+    from paper_1303_5466_b200.distributed import top_boxes, top_owner
+    tree = build_tree(Grid(64), 64)
+    for world in (2, 4, 8):
+        plan = subtree_plan(tree, world)
+        s = plan.split
+        owned = {}
+        for g in range(world):
+            for lv, j in top_boxes(plan, g):
+                assert top_owner(plan, lv, j) == g
+                owned[(lv, j)] = g
+        assert sorted(owned) == sorted((lv, j) for lv in range(s) for j in range(1 << lv))
+        for lv in range(s):
+            for j in range(1 << lv):
+                assert top_owner(plan, lv, j) == top_owner(plan, lv + 1, 2 * j)
+                assert top_owner(plan, lv + 1, 2 * j + 1) != top_owner(plan, lv, j)
+        assert top_owner(plan, 0, 0) == 0
+        # level s owners are the subtree ranks
+        assert [top_owner(plan, s, g) for g in range(world)] == list(range(world))

@@ -427,3 +427,35 @@ def test_rhs_dtypes_follow_result_type():
     assert H.matvec(np.zeros((grid.n, 0))).shape == (grid.n, 0)
     with pytest.raises(ValueError):
         inv.apply(np.zeros(grid.n + 1))
+
+
+def test_spill_to_host_memory_solves_bitwise():
+    """invert_dense_block(spill=_Spill(threshold_mb)) (the reference's _Spill
+    tier, solver_dense.py:37-55): factor batches above the threshold live in
+    pinned host memory and are streamed back level by level during the solve;
+    the solution is bitwise the in-HBM one and HBM holds far less."""
+    P, sd = _api()
+    spec = P.KernelSpec("laplace2d", b_field=P.make_field("centre_bump", scale=math.pi / 2),
+                        c_field=P.make_field("one"))
+    grid = P.Grid(128)
+    tree = P.build_tree(grid, 64)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=None)
+    f = np.random.default_rng(5).standard_normal((grid.n, 3))
+    H = sd.compress_outer(spec, grid, tree, 1e-10, opts, P.CELL)
+    x_ref = sd.invert_dense_block(H).apply(f)
+    x1_ref = sd.invert_dense_block(H).apply(f[:, 0])
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    base = torch.cuda.memory_allocated()
+    inv = sd.invert_dense_block(H, spill=sd._Spill(0))
+    held = torch.cuda.memory_allocated() - base
+    host = [getattr(L, n) for L in H.levels for n in ("Finv", "C", "E", "W")
+            if isinstance(getattr(L, n, None), torch.Tensor)]
+    assert host and all(not t.is_cuda and t.is_pinned() for t in host)
+    assert held < 0.1 * inv.nbytes(), (held, inv.nbytes())
+    np.testing.assert_array_equal(inv.apply(f), x_ref)
+    np.testing.assert_array_equal(inv.apply(f[:, 0]), x1_ref)
+    # threshold above every block: nothing moves
+    inv2 = sd.invert_dense_block(H, spill=1e6)
+    assert all(getattr(L, "Finv", None) is None or L.Finv.is_cuda for L in H.levels)
+    np.testing.assert_array_equal(inv2.apply(f), x_ref)
