@@ -124,6 +124,11 @@ typedef struct {
                                          squares solution of A(:, :k) T = A(:, k:m)
                                          (solver_compressed.py:223-266 _interp_lowrank, full
                                          rank).  Requires p >= min(m, 32*ceil(k/32)). */
+  int pairs;                          /* 1: columns (2t, 2t+1) are the two real components of
+                                         one complex unknown (realified complex kernels): pivots
+                                         are taken pairwise (the partner of pivot 2s is pivot
+                                         2s+1) and ranks are even, so the skeleton is a point set
+                                         and the real ID is the realification of a complex one */
 } vief_id_desc;
 int vief_id_batched(const vief_id_desc* d, void* stream); /* synchronises stream */
 

@@ -11,7 +11,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("VF_LIB") or os.path.join(_HERE, "_lib", "libvief_b200.so")  # VF_LIB: A/B builds
+LIB_PATH = os.path.join(_HERE, "_lib", "libvief_b200.so")
 
 VF_OK, VF_ECUDA, VF_EARG, VF_ESINGULAR, VF_ENOMEM = range(5)
 
@@ -40,7 +40,7 @@ class IdDesc(ctypes.Structure):
                 ("maxp", c_int), ("maxm", c_int), ("count", c_int), ("group", c_int),
                 ("eps", c_double), ("rank", c_vp), ("perm", c_vp),
                 ("T", c_vp), ("sT", c_ll), ("ldT", c_int), ("seed", ctypes.c_ulonglong),
-                ("force_blocked", c_int), ("kfix", c_vp)]
+                ("force_blocked", c_int), ("kfix", c_vp), ("pairs", c_int)]
 
 
 # name -> argtypes (all return int unless listed in _RET)

@@ -417,36 +417,15 @@ extern "C" int vief_dgemm_batched(const vief_gemm_desc* d, void* stream) {
   if (d->batch > 65535) { set_error("dgemm: batch %d > 65535", d->batch); return VF_EARG; }
   cudaStream_t st = (cudaStream_t)stream;
   // skinny M: 32 x 128 tiles (no idle DMMA rows); otherwise 64 x 64
-  static int tile = -1;  // VF_GEMM_TILE (A/B timing of CTA / warp tilings)
-  if (tile < 0) {
-    const char* e = getenv("VF_GEMM_TILE");
-    tile = !e ? 0 : !strcmp(e, "64x64w16") ? 1 : !strcmp(e, "64x64w32") ? 2
-         : !strcmp(e, "128x64w16") ? 3 : !strcmp(e, "64x128w16") ? 4
-         : !strcmp(e, "64x128w64") ? 5 : !strcmp(e, "128x64w64") ? 6 : 0;
-  }
-  int rc;
-  if (d->M <= 32) rc = dispatch_gemm<32, 128>(d, st);
-  else if (tile == 1) rc = dispatch_gemm<64, 64, 32, 16>(d, st);
-  else if (tile == 3) rc = dispatch_gemm<128, 64, 32, 32>(d, st);
-  else if (tile == 4) rc = dispatch_gemm<64, 128, 32, 16>(d, st);
-  else if (tile == 5) rc = dispatch_gemm<64, 128, 32, 64>(d, st);
-  else if (tile == 6) rc = dispatch_gemm<128, 64, 64, 32>(d, st);
-  else rc = dispatch_gemm<64, 64, 32, 32>(d, st);
+  const int rc = d->M <= 32 ? dispatch_gemm<32, 128>(d, st) : dispatch_gemm<64, 64>(d, st);
   if (rc) return rc;
   ++g_launches;
   VF_LAUNCH_CHECK("k_dgemm");
   return VF_OK;
 }
 
-// CTAs in flight the notrans GEMV aims for (VF_GEMV_CTAS overrides, for A/B timing)
-static int gv_target_ctas() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("VF_GEMV_CTAS");
-    v = e ? std::max(1, atoi(e)) : 8 * 148;
-  }
-  return v;
-}
+// CTAs in flight the notrans GEMV aims for (8 per SM)
+constexpr int GV_TARGET_CTAS = 8 * 148;
 
 extern "C" int vief_dgemv_batched(const vief_gemm_desc* d, void* stream) {
   if (!d || d->batch <= 0 || d->M <= 0) return VF_OK;
@@ -455,7 +434,7 @@ extern "C" int vief_dgemv_batched(const vief_gemm_desc* d, void* stream) {
     const int tiles = (int)cdiv(d->M, GV_ROWS) * d->batch;
     // K split (cluster size) so that ~4 CTAs per SM stream concurrently; each
     // CTA keeps at least 8 columns per warp
-    int cs = std::max(1, std::min(8, (int)cdiv(gv_target_ctas(), tiles)));
+    int cs = std::max(1, std::min(8, (int)cdiv(GV_TARGET_CTAS, tiles)));
     cs = std::max(1, std::min(cs, d->K / (8 * GV_WARPS)));
     const int kchunk = (int)cdiv(cdiv(d->K, cs), GV_WARPS) * GV_WARPS;
     cudaLaunchConfig_t cfg = {};

@@ -418,7 +418,8 @@ struct XSel {
 template <bool WIDE>  // WIDE: more than PT columns per CTA (two per thread per pass)
 __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, long long sY,
                                                   const int* mv, const int* active, const int* bsv,
-                                                  int J, int cols_per, int* swaps) {
+                                                  int J, int cols_per, int* swaps,
+                                                  const int* perm, int ldperm) {
   cg::cluster_group cl = cg::this_cluster();
   const int cs = cl.num_blocks(), cr = cl.block_rank();
   const int b = blockIdx.x / cs;
@@ -465,8 +466,14 @@ __global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, lon
   // warp 0 picks the winner and orthogonalises its sketch column against the
   // chosen ones (no block barriers), then every thread downdates its columns'
   // residual norms and keeps its next candidate (1 barrier)
+  const int* pm = perm ? perm + (long long)b * ldperm + J : nullptr;  // pair mode
   for (int i = 0; i < bs; ++i) {
     XSel& x = xch[i & 1];
+    if (pm && (i & 1)) {  // pivot 2s+1: the partner component of pivot 2s
+      const int want = pm[sel[i - 1]] ^ 1;
+      for (int c = tid; c < nc; c += PT)
+        if (nrm[c] >= 0.0 && pm[c0 + c] == want) { bv = 1e300; bi = c0 + c; }
+    }
     double v = bv;
     int iv = bi;
     warp_argmax(v, iv);
@@ -1077,16 +1084,6 @@ static int launch_cluster(const void* fn, int count, int cs, size_t smem, cudaSt
 // cluster size: enough CTAs that one slice fits `max_slice` rows/cols, and,
 // when there are few matrices, split further (down to 256 per CTA) so the
 // cluster work spreads over the SMs
-// VF_PANEL=cl / rr forces the smem-resident / register-resident panels (A/B timing)
-static int panel_mode() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("VF_PANEL");
-    mode = !e ? 0 : (e[0] == 'c' ? 1 : (e[0] == 'r' ? 2 : 0));
-  }
-  return mode;
-}
-
 static int pick_cs(int total, int max_slice, int count) {
   int cs = (total + max_slice - 1) / max_slice;
   if (count * cs < 120) cs = std::max(cs, (total + 255) / 256);
@@ -1102,24 +1099,15 @@ int lu_panel(const double* A, long long sA, int lda, int n, int c0, int nbs, int
     // measured: the register-resident panel wins for tall panels; for short
     // ones in large batches the smem kernel's higher occupancy wins
     int rpt = R <= PT ? 1 : (R <= 16 * 2 * PT ? 2 : (R <= 16 * 3 * PT ? 3 : 0));
-    if (panel_mode() == 1 || (panel_mode() == 0 && R <= 320)) rpt = 0;
+    if (R <= 320) rpt = 0;
     if (rpt) {
       const int cs = (R + rpt * PT - 1) / (rpt * PT);
       void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&n, (void*)&c0, (void*)&nbs,
                       (void*)&ipiv, (void*)&sPiv, (void*)&Ainv, (void*)&sAi,
                       (void*)&pivmin, (void*)&pivmax};
-      static int unr = -1;  // VF_LU_UNR = 1 | 2 | 4: column steps per register rotation (2: measured 1-2 % faster GJ)
-      if (unr < 0) { const char* e = getenv("VF_LU_UNR"); unr = e ? atoi(e) : 2; }
-      const void* fn;
-      if (unr == 2)
-        fn = rpt == 1 ? (const void*)k_lu_panel_rr<1, 2>
-           : rpt == 2 ? (const void*)k_lu_panel_rr<2, 2> : (const void*)k_lu_panel_rr<3, 2>;
-      else if (unr == 4)
-        fn = rpt == 1 ? (const void*)k_lu_panel_rr<1, 4>
-           : rpt == 2 ? (const void*)k_lu_panel_rr<2, 4> : (const void*)k_lu_panel_rr<3, 4>;
-      else
-        fn = rpt == 1 ? (const void*)k_lu_panel_rr<1>
-           : rpt == 2 ? (const void*)k_lu_panel_rr<2> : (const void*)k_lu_panel_rr<3>;
+      // two column steps per register rotation (measured 1-2 % faster GJ than one or four)
+      const void* fn = rpt == 1 ? (const void*)k_lu_panel_rr<1, 2>
+                     : rpt == 2 ? (const void*)k_lu_panel_rr<2, 2> : (const void*)k_lu_panel_rr<3, 2>;
       return launch_cluster(fn, batch, cs, 0, st, args);
     }
   }
@@ -1138,9 +1126,7 @@ int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* a
              const int* bsv, int J, int maxp, int count, double* Vw, long long sV, int ldv,
              double* Tt, double* Rt, cudaStream_t st) {
   const int rows = maxp - J;  // panel rows J..p-1
-  static int short_ok = -1;  // VF_QR_SHORT=0 disables the small-CTA path (A/B timing)
-  if (short_ok < 0) { const char* e = getenv("VF_QR_SHORT"); short_ok = !(e && e[0] == '0'); }
-  if (short_ok && rows <= 2 * 128 && panel_mode() != 1) {  // short panels: small CTAs, several per SM
+  if (rows <= 2 * 128) {  // short panels: small CTAs, several per SM
     void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
                     (void*)&J, (void*)&Vw, (void*)&sV, (void*)&ldv, (void*)&Tt, (void*)&Rt};
     const int nt = rows <= 128 ? 64 : 128;
@@ -1149,7 +1135,7 @@ int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* a
                                  : (const void*)k_qr_panel_rr<2, 128>;
     return launch_cluster(fn, count, 1, 0, st, args, nt);
   }
-  if (rows <= 16 * 3 * PT && panel_mode() != 1) {
+  if (rows <= 16 * 3 * PT) {
     const int rpt = rows <= PT ? 1 : (rows <= 16 * 2 * PT ? 2 : 3);
     const int cs = (rows + rpt * PT - 1) / (rpt * PT);
     void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
@@ -1179,7 +1165,8 @@ int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* a
 template <int NT>  // threads = columns per CTA slot (cols_per <= NT); <= 128 registers
 __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) k_select_hh(const double* Yg, int ldy, long long sY,
                                                   const int* mv, const int* active, const int* bsv,
-                                                  int J, int cols_per, int* swaps) {
+                                                  int J, int cols_per, int* swaps,
+                                                  const int* perm, int ldperm) {
   cg::cluster_group cl = cg::this_cluster();
   const int cs = cl.num_blocks(), cr = cl.block_rank();
   const int b = blockIdx.x / cs;
@@ -1215,11 +1202,14 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) k_select_hh(cons
     }
     if (own) nrm = (s0 + s1) + (s2 + s3);
   }
+  const int* pm = perm ? perm + (long long)b * ldperm + J : nullptr;  // pair mode
+  const int myid = pm && own ? pm[c0 + tid] : -1;
   for (int i = 0; i < bs; ++i) {
     XSel& x = xch[i & 1];
     double v = nrm;
     int iv = own && nrm >= 0.0 ? c0 + tid : 0x7fffffff;
     if (!(nrm >= 0.0)) v = -1.0;
+    else if (pm && (i & 1) && myid == (pm[sel[i - 1]] ^ 1)) v = 1e300;  // partner of pivot i-1
     const double myv = v;
     const int myi = iv;
     warp_argmax(v, iv);
@@ -1297,17 +1287,18 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) k_select_hh(cons
 }
 
 int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const int* active,
-                  const int* bsv, int J, int maxm, int count, int* swaps, cudaStream_t st) {
+                  const int* bsv, int J, int maxm, int count, int* swaps, const int* perm,
+                  int ldperm, cudaStream_t st) {
   const int n = maxm - J;
   if (n <= 0) return VF_OK;
   int cs = pick_cs(n, 512, count);
   int cols_per = (n + cs - 1) / cs;
   size_t smem = ((size_t)(HSK + 1) * cols_per + (size_t)cols_per) * sizeof(double);
   void* args[] = {(void*)&Y, (void*)&ldy, (void*)&sY, (void*)&mv, (void*)&active, (void*)&bsv,
-                  (void*)&J, (void*)&cols_per, (void*)&swaps};
-  static int hh = -1;  // VF_SELECT_HH=0: Gram-Schmidt selection everywhere (A/B)
-  if (hh < 0) { const char* e = getenv("VF_SELECT_HH"); hh = !(e && e[0] == '0'); }
-  if (hh && cols_per <= 512) {
+                  (void*)&J, (void*)&cols_per, (void*)&swaps, (void*)&perm, (void*)&ldperm};
+  // Householder selection while a thread owns one column; wider slices
+  // (maxm > 16 x 512, 2048^2 and up) use the Gram-Schmidt kernel
+  if (cols_per <= 512) {
     const int nt = cols_per <= 128 ? 128 : (cols_per <= 256 ? 256 : 512);
     const void* fn = nt == 128 ? (const void*)k_select_hh<128>
                    : nt == 256 ? (const void*)k_select_hh<256> : (const void*)k_select_hh<512>;

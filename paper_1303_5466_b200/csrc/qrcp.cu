@@ -43,123 +43,6 @@ extern std::atomic<long long> g_launches;
 // small path: classical QRCP in shared memory
 constexpr int QS_THREADS = 256;
 
-__global__ void __launch_bounds__(QS_THREADS) k_qrcp_smem(
-    const double* A, long long sA, int lda, const int* pv, const int* mv, int* perm, int ldperm,
-    double* Rm, long long sR, int ldR, double* diag, int lddiag, double* colmax) {
-  extern __shared__ double sm[];
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw = QS_THREADS / 32;
-  const int p = pv[b], m = mv[b];
-  const int ld = p | 1;  // odd stride: column-parallel warps hit different banks
-  double* a = sm;                        // ld x m
-  double* vn1 = a + (long long)ld * m;   // m
-  double* vn2 = vn1 + m;                 // m
-  __shared__ double redv[32];
-  __shared__ int redi[32];
-  __shared__ double s_tau, s_beta;
-  int* pm = perm + b * ldperm;
-  const double* Ab = A + b * sA;
-  for (int idx = tid; idx < p * m; idx += QS_THREADS) {
-    int i = idx % p, j = idx / p;
-    a[j * ld + i] = Ab[(long long)j * lda + i];
-  }
-  for (int j = tid; j < m; j += QS_THREADS) pm[j] = j;
-  __syncthreads();
-  for (int j = warp; j < m; j += nw) {
-    double s = 0.0;
-    for (int i = lane; i < p; i += 32) s = fma(a[j * ld + i], a[j * ld + i], s);
-    s = sqrt(warp_sum(s));
-    if (lane == 0) { vn1[j] = s; vn2[j] = s; }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double mx = 0.0;
-    for (int j = 0; j < m; ++j) mx = fmax(mx, vn1[j]);
-    colmax[b] = mx;
-  }
-  const int kmax = min(p, m);
-  const double tol3z = sqrt(2.220446049250313e-16);
-  double* Rb = Rm + b * sR;
-  double* db = diag + b * lddiag;
-  for (int i = 0; i < kmax; ++i) {
-    // pivot: first maximum of vn1[i:m]
-    double v = -1.0;
-    int iv = 0x7fffffff;
-    for (int j = i + tid; j < m; j += QS_THREADS)
-      if (vn1[j] > v) { v = vn1[j]; iv = j; }
-    block_argmax(v, iv, redv, redi);
-    const int pvt = iv;
-    if (pvt != i) {
-      for (int r = tid; r < p; r += QS_THREADS) {
-        double t = a[pvt * ld + r]; a[pvt * ld + r] = a[i * ld + r]; a[i * ld + r] = t;
-      }
-      if (tid == 0) {
-        int t = pm[pvt]; pm[pvt] = pm[i]; pm[i] = t;
-        vn1[pvt] = vn1[i]; vn2[pvt] = vn2[i];
-      }
-    }
-    __syncthreads();
-    // dlarfg on a(i:p, i)
-    double s = 0.0;
-    for (int r = i + 1 + tid; r < p; r += QS_THREADS) s = fma(a[i * ld + r], a[i * ld + r], s);
-    s = block_sum(s, redv);
-    if (tid == 0) {
-      double alpha = a[i * ld + i];
-      double xn = sqrt(s);
-      if (xn == 0.0) { s_tau = 0.0; s_beta = alpha; }
-      else {
-        double beta = -copysign(hypot(alpha, xn), alpha);
-        s_tau = (beta - alpha) / beta;
-        s_beta = beta;
-        a[i * ld + i] = 1.0 / (alpha - beta);  // temporary: scale factor
-      }
-    }
-    __syncthreads();
-    const double tau = s_tau, beta = s_beta;
-    if (tau != 0.0) {
-      const double sc = a[i * ld + i];
-      for (int r = i + 1 + tid; r < p; r += QS_THREADS) a[i * ld + r] *= sc;
-      __syncthreads();
-      if (tid == 0) a[i * ld + i] = 1.0;  // v(0) = 1 during the apply
-      __syncthreads();
-      // apply H = I - tau v v^T to columns i+1..m-1 (warp per column)
-      for (int j = i + 1 + warp; j < m; j += nw) {
-        double w = 0.0;
-        for (int r = i + lane; r < p; r += 32) w = fma(a[i * ld + r], a[j * ld + r], w);
-        w = warp_sum(w) * tau;
-        for (int r = i + lane; r < p; r += 32) a[j * ld + r] = fma(-w, a[i * ld + r], a[j * ld + r]);
-      }
-      __syncthreads();
-    }
-    if (tid == 0) { a[i * ld + i] = beta; db[i] = fabs(beta); }
-    // partial column norm update (dlaqp2)
-    for (int j = i + 1 + warp; j < m; j += nw) {
-      double nv1 = vn1[j];
-      if (nv1 != 0.0) {
-        double t = fabs(a[j * ld + i]) / nv1;
-        double temp = fmax(1.0 - t * t, 0.0);
-        double r = nv1 / vn2[j];
-        double temp2 = temp * r * r;
-        if (temp2 <= tol3z) {
-          double ss = 0.0;
-          for (int rr = i + 1 + lane; rr < p; rr += 32) ss = fma(a[j * ld + rr], a[j * ld + rr], ss);
-          ss = sqrt(warp_sum(ss));
-          if (lane == 0) { vn1[j] = ss; vn2[j] = ss; }
-        } else if (lane == 0) {
-          vn1[j] = nv1 * sqrt(temp);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  for (int i = kmax + tid; i < m; i += QS_THREADS) db[i] = 0.0;
-  // R (upper trapezoid, kmax x m) -> Rm
-  for (int idx = tid; idx < kmax * m; idx += QS_THREADS) {
-    int i = idx % kmax, j = idx / kmax;
-    Rb[(long long)j * ldR + i] = (i <= j) ? a[j * ld + i] : 0.0;
-  }
-}
-
 // Same factorization (dlaqp2 semantics) with two CTA barriers per column
 // instead of ~10: warp 0 alone does the pivot swap and the reflector
 // (p <= ~200 rows: a warp reduction, no block reduction), then every warp
@@ -170,7 +53,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_qrcp_smem(
 constexpr int QS_CH = 4;
 __global__ void __launch_bounds__(QS_THREADS) k_qrcp_smem2(
     const double* A, long long sA, int lda, const int* pv, const int* mv, int* perm, int ldperm,
-    double* Rm, long long sR, int ldR, double* diag, int lddiag, double* colmax) {
+    double* Rm, long long sR, int ldR, double* diag, int lddiag, double* colmax, int pairs) {
   extern __shared__ double sm[];
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nw = QS_THREADS / 32;
@@ -219,6 +102,14 @@ __global__ void __launch_bounds__(QS_THREADS) k_qrcp_smem2(
       int pvt = redi[0];
       for (int w = 1; w < nw; ++w)
         if (redv[w] > bv || (redv[w] == bv && redi[w] < pvt)) { bv = redv[w]; pvt = redi[w]; }
+      if (pairs && (i & 1)) {  // pivot 2s+1 is the partner component of pivot 2s
+        const int want = pm[i - 1] ^ 1;
+        int at = 0x7fffffff;
+        for (int j = i + lane; j < m; j += 32)
+          if (pm[j] == want) at = j;
+        for (int o = 16; o > 0; o >>= 1) at = min(at, __shfl_xor_sync(0xffffffffu, at, o));
+        if (at < m) pvt = at;
+      }
       if (pvt != i && pvt < m) {
         for (int r = lane; r < p; r += 32) {
           double t = a[pvt * ld + r]; a[pvt * ld + r] = a[i * ld + r]; a[i * ld + r] = t;
@@ -314,7 +205,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_qrcp_smem2(
 
 // rank of small-path items: reference rule on |R_jj| (dense_core.py:81-89)
 __global__ void k_rank_small(const double* diag, int lddiag, const int* pv, const int* mv,
-                             int count, double eps, int* kout) {
+                             int count, double eps, int pairs, int* kout) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= count) return;
   const int kmax = min(pv[b], mv[b]);
@@ -328,6 +219,7 @@ __global__ void k_rank_small(const double* diag, int lddiag, const int* pv, cons
       for (int j = 0; j < kmax; ++j) if (d[j] <= cut) { k = j; break; }
     }
   }
+  if (pairs && (k & 1)) k = min(k + 1, kmax);  // whole pairs
   kout[b] = k;
 }
 
@@ -575,7 +467,8 @@ __global__ void k_store_rblock(HState S, double* Rm, long long sR, int ldR, int 
 // rank check after a block: own criterion, and k inside the block (exact
 // residual form of the reference's rule |R_jj| <= eps |R_00|).
 __global__ void __launch_bounds__(256) k_rank_check(HState S, const double* Rm, long long sR,
-                                                    int ldR, const int* pv, const int* mv, int J) {
+                                                    int ldR, const int* pv, const int* mv, int J,
+                                                    int pairs) {
   const int b = blockIdx.x, tid = threadIdx.x;
   if (!S.active[b] || S.done[b]) return;
   const int bs = S.bs[b];
@@ -638,6 +531,7 @@ __global__ void __launch_bounds__(256) k_rank_check(HState S, const double* Rm, 
     int k = J1;
     for (int t = 0; t <= bs; ++t)
       if (sqrt(best[t]) <= cut) { k = J + t; break; }
+    if (pairs && (k & 1)) ++k;  // whole pairs (blocks are even, so k+1 <= J1)
     if (k > kmax) k = kmax;
     S.k[b] = k;
     S.done[b] = 1;
@@ -896,13 +790,12 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   if (small) {
     prof_push(st, "id.small_qrcp");
     double* diag = buf.get<double>((size_t)maxm * count);
-    static int old_kernel = -1;  // VF_QRCP_OLD=1: the previous one-warp-per-column kernel (A/B)
-    if (old_kernel < 0) { const char* e = getenv("VF_QRCP_OLD"); old_kernel = e && e[0] == '1'; }
-    auto fn = old_kernel ? k_qrcp_smem : k_qrcp_smem2;
+    auto fn = k_qrcp_smem2;
     VF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small));
     fn<<<count, QS_THREADS, smem_small, st>>>(d->A, d->sA, d->lda, d->p, d->m, d->perm, maxm, Rm,
-                                              sR, ldR, diag, maxm, colmax);
-    k_rank_small<<<cdiv(count, 128), 128, 0, st>>>(diag, maxm, d->p, d->m, count, d->eps, kdev);
+                                              sR, ldR, diag, maxm, colmax, d->pairs);
+    k_rank_small<<<cdiv(count, 128), 128, 0, st>>>(diag, maxm, d->p, d->m, count, d->eps,
+                                                   d->pairs, kdev);
     k_group_max<<<cdiv(count / d->group, 128), 128, 0, st>>>(kdev, count, d->group);
     g_launches += 3;
     VF_LAUNCH_CHECK("qrcp small");
@@ -919,10 +812,6 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.Rt = buf.get<double>((size_t)HB * HB * count);
     S.Tt = buf.get<double>((size_t)HB * HB * count);
     S.D = maxm >= 4096 ? 8 : (maxm >= 2048 ? 4 : (maxm >= 512 ? 2 : 1));
-    if (const char* e = getenv("VF_ID_DPOLICY")) {  // A/B timing of the delay depth
-      if (e[0] == '1') S.D = maxm >= 1024 ? 8 : (maxm >= 256 ? 4 : (maxm >= 128 ? 2 : 1));
-      if (e[0] == '2') S.D = maxm >= 512 ? 8 : (maxm >= 128 ? 4 : 2);
-    }
     const int D = S.D, ldU = HB * D;
     S.Vw = buf.get<double>((size_t)maxp * HB * D * count);
     S.Up = buf.get<double>((size_t)ldU * maxm * count);
@@ -992,7 +881,8 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       k_block_setup<<<cdiv(count, 128), 128, 0, st>>>(J, Jf, d->p, d->m, count, S);
       ++g_launches;
       if (!fixed) {
-        if ((rc = sketch_select(S.Y, HS, sY, d->m, S.active, S.bs, J, maxm, count, S.swaps, st)))
+        if ((rc = sketch_select(S.Y, HS, sY, d->m, S.active, S.bs, J, maxm, count, S.swaps,
+                                d->pairs ? d->perm : nullptr, maxm, st)))
           return rc;
         prof_push(st, "id.swaps");
         k_apply_perm<<<dim3(cdiv(std::max(std::max(maxp, HS), std::max(J, kp)), AP_T), count),
@@ -1142,7 +1032,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         ++g_launches;
         continue;
       } else {
-        k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J);
+        k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J, d->pairs);
         k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
         g_launches += 2;
       }

@@ -27,7 +27,6 @@ buffer (column-major, leading dimension = level maximum).
 import contextlib
 import ctypes
 import gc
-import os
 import math
 
 import numpy as np
@@ -462,7 +461,8 @@ def _compress_level_id(H, L, pad, seed):
     perm = torch.zeros((count, mm), dtype=_I32, device=dev)
     T = torch.zeros((count, mm, mm), dtype=_F64, device=dev)
     _id_batched(dev, A, mm * ldA, ldA, pv, mv, int(p.max()), mm, count, g, float(H.eps), rank,
-                perm, T, int(seed) * 1000003 + L.lv, int(getattr(H, "_force_blocked", 0)))
+                perm, T, int(seed) * 1000003 + L.lv, int(getattr(H, "_force_blocked", 0)),
+                pairs=H.realified)
     del A
     L.k = rank[0::g].cpu().numpy().astype(np.int32)
     L.kmax = max(int(L.k.max()), 1)
@@ -581,14 +581,14 @@ def _compress_level_apriori(H, L, layers):
         L.cskel = L.rskel
 
 
-# The IDs of a level run as VF_ID_SPLIT (default 2) slices of the batch on as
+# The IDs of a level run as _ID_SPLIT = 2 slices of the batch on as
 # many streams, each driven by its own host thread (the blocked ID
 # synchronises its stream twice per column block; ctypes releases the GIL):
 # one slice's latency-bound panel and pivot-selection kernels overlap the
 # others' GEMMs.  Every item's arithmetic is unchanged except for batch-wide
 # choices (GEMM split-K, the shared flush schedule), so results are
-# deterministic for a given split.  VF_ID_SPLIT=1 runs one batch.
-_ID_SPLIT = max(1, int(os.environ.get("VF_ID_SPLIT", "2")))
+# deterministic for a given split.
+_ID_SPLIT = 2
 _ID_SIDE = {}
 
 
@@ -605,15 +605,16 @@ def _id_side(dev, n):
 
 
 def _id_batched(dev, A, sA, ldA, pv, mv, maxp, mm, count, g, eps, rank, perm, T, seed, forced,
-                kfix=None):
+                kfix=None, pairs=False):
     """vief_id_batched over `count` items (groups of g share a rank); `kfix`
-    (device int32, count) fixes the ranks and disables pivoting."""
+    (device int32, count) fixes the ranks and disables pivoting; `pairs`: the
+    columns are realified complex unknowns, pivoted pairwise."""
     def desc(lo, n):
         return _lib.IdDesc(_lib.ptr(A) + 8 * lo * sA, sA, ldA, _lib.ptr(pv) + 4 * lo,
                            _lib.ptr(mv) + 4 * lo, maxp, mm, n, g, eps, _lib.ptr(rank) + 4 * lo,
                            _lib.ptr(perm) + 4 * lo * mm, _lib.ptr(T) + 8 * lo * mm * mm, mm * mm,
                            mm, seed, forced,
-                           None if kfix is None else _lib.ptr(kfix) + 4 * lo)
+                           None if kfix is None else _lib.ptr(kfix) + 4 * lo, int(pairs))
     nb = count // g
     parts = min(_ID_SPLIT, nb)
     if parts < 2:
@@ -1075,7 +1076,6 @@ def invert_dense_block(H, spill=None, free_source=False):
 _SIDE = {}
 
 
-_HOST_QUIET = os.environ.get("VF_HOST_QUIET", "1") != "0"
 _QUIET_DEPTH = [0]
 
 
@@ -1101,9 +1101,8 @@ def _host_quiet():
         spin after every call and starved the stream-driving threads (measured
         at 1024^2: random 100-480 ms stalls of a level, none with one thread);
       * Python's cyclic GC held (a collection stops every thread at the GIL;
-        the loops create no reference cycles).
-    VF_HOST_QUIET=0 disables both."""
-    if not _HOST_QUIET or _QUIET_DEPTH[0] > 0:
+        the loops create no reference cycles)."""
+    if _QUIET_DEPTH[0] > 0:
         yield
         return
     gc_was = gc.isenabled()
