@@ -783,35 +783,102 @@ def _invert_level_F_block(inv, L, checks=None):
     L.Finv = F
 
 
-def _invert_level_F(inv, L, checks=None):
-    """F = D (leaf) or [[E1, B12], [B21, E2]] and its inverse."""
-    H = inv.H
+def _assemble_F(H, L):
+    """The level's F blocks, nb x mm x mm padded with identity: D at the leaves,
+    [[E1, B12], [B21, E2]] above (solver_dense.py:346-352)."""
     dev = H.device
     nb, mm = L.nb, L.mmax
-    C1 = H.levels[L.lv + 1] if L.lv + 1 < len(H.levels) else None
-    if not L.leaf and getattr(C1, "Gkeep", None) is not None:
-        if L.lv == 0:
-            return _invert_root_block(inv, L, checks)
-        return _invert_level_F_block(inv, L, checks)
-    _lib.prof_mark("py.F_assemble")
     F = torch.zeros((nb, mm, mm), dtype=_F64, device=dev)
     if L.leaf:
         F.copy_(L.D)
     else:
         C = H.levels[L.lv + 1]
         kc = C.kmax
-        k1, k2 = C.k[0::2].astype(np.int64), C.k[1::2].astype(np.int64)
+        CE = C.E if C.E.is_cuda else C.E.to(dev)
+        k1 = C.k[0::2].astype(np.int64)
         k1d, k2d = C.k_d[0::2].contiguous(), C.k_d[1::2].contiguous()
         base = np.arange(nb, dtype=np.int64) * mm * mm
         # F[:k1,:k1] = E1 ; F[k1:,k1:] = E2 ; F[:k1,k1:] = B12 ; F[k1:,:k1] = B21
-        _lib.copy2d(C.E, 2 * kc * kc, kc, F, mm * mm, mm, k1d, kc, k1d, kc, nb)
-        _lib.copy2d(_lib.ptr(C.E) + 8 * kc * kc, 2 * kc * kc, kc, None, 0, mm, k2d, kc, k2d, kc, nb,
+        _lib.copy2d(CE, 2 * kc * kc, kc, F, mm * mm, mm, k1d, kc, k1d, kc, nb)
+        _lib.copy2d(_lib.ptr(CE) + 8 * kc * kc, 2 * kc * kc, kc, None, 0, mm, k2d, kc, k2d, kc, nb,
                     dstp=_ptrs(F, base + k1 * mm + k1, dev))
         _lib.copy2d(L.B12, kc * kc, kc, None, 0, mm, k1d, kc, k2d, kc, nb,
                     dstp=_ptrs(F, base + k1 * mm, dev))
         _lib.copy2d(L.B21, kc * kc, kc, None, 0, mm, k2d, kc, k1d, kc, nb,
                     dstp=_ptrs(F, base + k1, dev))
     _lib.pad_identity(F, mm * mm, mm, L.m_d, mm, nb)
+    return F
+
+
+# Ill-conditioned box solves.  The factors hold explicit inverses (F^-1 and E
+# by Gauss-Jordan, W = F^-1 L by GEMM); applying an explicit inverse to a
+# vector is not backward stable, so where F is badly conditioned (near-
+# resonant Helmholtz boxes: cond(F) ~ 1e10+ at kappa = 40, config c3) the
+# sweeps' x = F^-1 u would leave residuals cond(F) eps |F| |x|, where the
+# reference's LU solves (solver_dense.py:309,321 lu_solve) leave eps |F| |x|.
+# Such levels refine every box solve against F itself (x += F^-1 (u - F x),
+# _REFINE_STEPS times), which restores the LU solve's accuracy (measured at
+# c3: one-shot E = ||f - H x|| / ||f|| 17 -> the reference's 1e-4).  A level
+# is flagged when max|F| max|F^-1| (a cheap lower bound on cond_max(F))
+# exceeds _REFINE_COND; well-conditioned problems (all Laplace configs) run
+# the plain sweeps.
+_REFINE_COND = 1e8
+_REFINE_STEPS = 2
+_BLOCK_E_MAX = 1e4   # largest child |E| entry for which F^-1 is formed by block elimination
+
+
+def _level_cond_est(H, L):
+    """Device scalar max|F| * max|F^-1| of the level (no host sync)."""
+    if getattr(L, "rb", None) is not None:          # root in block form
+        G1, B12, B21, Sinv = L.rb[:4]
+        xinv = torch.maximum(G1.abs().amax(), Sinv.abs().amax())
+    else:
+        xinv = L.Finv.abs().amax()
+    if L.leaf:
+        fmax = L.D.abs().amax()
+    else:
+        C = H.levels[L.lv + 1]
+        fmax = torch.maximum(torch.maximum(L.B12.abs().amax(), L.B21.abs().amax()),
+                             C.E.abs().amax().to(H.device))
+    return xinv * fmax
+
+
+def _flag_refinement(H, ests):
+    """ests: {level: device scalar}; one host read for all levels."""
+    if not ests:
+        return
+    lv = list(ests)
+    vals = torch.stack([ests[l] for l in lv]).cpu().numpy()
+    for l, v in zip(lv, vals):
+        H.levels[l].refine = bool(not np.isfinite(v) or v > _REFINE_COND)
+
+
+def _invert_level_F(inv, L, checks=None):
+    """F = D (leaf) or [[E1, B12], [B21, E2]] and its inverse; records the
+    level's conditioning estimate for _flag_refinement."""
+    _invert_level_F_impl(inv, L, checks)
+    ests = getattr(inv, "_ests", None)
+    if ests is None:
+        ests = inv._ests = {}
+    ests[L.lv] = _level_cond_est(inv.H, L)
+
+
+def _invert_level_F_impl(inv, L, checks=None):
+    H = inv.H
+    dev = H.device
+    nb, mm = L.nb, L.mmax
+    C1 = H.levels[L.lv + 1] if L.lv + 1 < len(H.levels) else None
+    if not L.leaf and getattr(C1, "Gkeep", None) is not None:
+        # block elimination substitutes G1 = E1^{-1} for the children's explicit
+        # E1; with an ill-conditioned G1 (|E| >> 1: near-resonant boxes) the two
+        # differ by cond(G1) eps |E1|, so such levels invert the assembled F
+        if float(C1.E.abs().amax()) <= _BLOCK_E_MAX:
+            if L.lv == 0:
+                return _invert_root_block(inv, L, checks)
+            return _invert_level_F_block(inv, L, checks)
+        C1.Gkeep = None
+    _lib.prof_mark("py.F_assemble")
+    F = _assemble_F(H, L)
     pmin, pmax = _lib.inv_batched(F, mm * mm, mm, mm, nb)
     if checks is None:
         _check_singular(H, L, pmin, pmax, "F")
@@ -1059,8 +1126,11 @@ def invert_dense_block(H, spill=None, free_source=False):
             _lib.prof_prefix(f"L{L.lv:02d}.")
             _invert_level(inv, L)
             _mark(f"invert:{L.lv}")
-            if free_source:
-                if L.leaf:
+            if free_source:  # a level whose box solves are refined keeps its F blocks
+                _flag_refinement(H, {L.lv: inv._ests.pop(L.lv)})
+                if L.refine:
+                    pass
+                elif L.leaf:
                     L.D = None
                 else:
                     L.B12 = L.B21 = None
@@ -1070,6 +1140,7 @@ def invert_dense_block(H, spill=None, free_source=False):
             sp.spill_level(levels[-1])
             torch.cuda.current_stream(H.device).synchronize()   # pinned copies complete
             torch.cuda.empty_cache()
+        _flag_refinement(H, inv.__dict__.pop("_ests", {}))
     return inv
 
 
@@ -1129,6 +1200,9 @@ def factor_solve(spec, grid, tree, eps, opts, f, quad=PLAIN, apriori=None):
     with _host_quiet():
         H, inv, (fd, single, phi, ups) = _factorize(spec, grid, tree, eps, opts, quad, rhs=f,
                                                     apriori=apriori)
+        if any(getattr(L, "refine", False) for L in _real_levels(H)):
+            phi, ups = {}, {}      # refined box solves: the pipelined up sweep ran without
+            _sweep_up(H, fd, phi, ups)
         out = torch.zeros_like(fd)
         _sweep_down(H, phi, ups, out)
         return H, inv, _from_device(out, f, single, H.realified)
@@ -1169,6 +1243,7 @@ def _factorize(spec, grid, tree, eps, opts, quad=PLAIN, rhs=None, apriori=None):
     checks, inv._checks = inv._checks, []
     for L, pmin, pmax, what in checks:
         _check_singular(H, L, pmin, pmax, what)
+    _flag_refinement(H, inv.__dict__.pop("_ests", {}))
     return H, inv, solve
 
 
@@ -1411,11 +1486,11 @@ def _sweep_up_level(H, L, fd, phi, ups, fac=None):
         _lib.gather_rows(ups[C.lv], 2 * C.kmax, C.nb * C.kmax, L.cat_idx, mm, U, mm, ldv,
                          L.m_d, mm, None, r, nb)
     Phi = torch.zeros((r, ldv), dtype=_F64, device=dev)
-    if getattr(L, "rb", None) is not None:
-        _root_block_solve(L, U, ldv, r, Phi, ldv)
-    else:
-        _mv(Finv, _fs(L, mm * mm), mm, U, mm, ldv, Phi, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r,
-            1.0, 0.0)
+    _apply_Finv(L, Finv, U, Phi, r, 0.0)
+    if getattr(L, "refine", False):
+        _refine_box_solve(H, L, Finv, U, Phi, r)
+        if L.lv > 0:
+            phi[("u", L.lv)] = U      # the down sweep refines against the same u
     del U
     phi[L.lv] = Phi
     if L.lv == 0:
@@ -1425,6 +1500,61 @@ def _sweep_up_level(H, L, fd, phi, ups, fac=None):
     _mv(Cf, _fs(L, mm * kk), kk, Phi, mm, ldv, Ups, kk, nb * kk, kk, mm, L.k_d, L.m_d, nb, r,
         1.0, 0.0)
     ups[L.lv] = Ups
+
+
+def _apply_Finv(L, Finv, U, Out, r, beta):
+    """Out = F^{-1} U + beta Out for the level's boxes (vectors: (r, nb*mm))."""
+    nb, mm = L.nb, L.mmax
+    ldv = nb * mm
+    if getattr(L, "rb", None) is not None:
+        if beta == 0.0:
+            _root_block_solve(L, U, ldv, r, Out, ldv)
+        else:
+            T = torch.zeros_like(Out)
+            _root_block_solve(L, U, ldv, r, T, ldv)
+            Out.add_(T)
+    else:
+        _mv(Finv, _fs(L, mm * mm), mm, U, mm, ldv, Out, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r,
+            1.0, beta)
+
+
+def _level_Fmat(H, L):
+    """F of a refined level (cached; the leaves' D is used as is)."""
+    if L.leaf:
+        return L.D
+    F = getattr(L, "_Fmat", None)
+    if F is None:
+        F = L._Fmat = _assemble_F(H, L)
+    return F
+
+
+def _refine_box_solve(H, L, Finv, U, X, r):
+    """X += F^{-1} (U - F X), _REFINE_STEPS times (iterative refinement of
+    the level's box solves against F; see _REFINE_COND)."""
+    nb, mm = L.nb, L.mmax
+    ldv = nb * mm
+    F = _level_Fmat(H, L)
+    for _ in range(_REFINE_STEPS):
+        R = U.clone()
+        _mv(F, mm * mm, mm, X, mm, ldv, R, mm, ldv, mm, mm, L.m_d, L.m_d, nb, r, -1.0, 1.0)
+        _apply_Finv(L, Finv, R, X, r, 1.0)
+
+
+def _apply_L(H, L, D, r):
+    """Z = L D per box (interp_L: D to perm_r[:k], Tr^T D to perm_r[k:],
+    solver_dense.py:75-80); D: (r, nb*kk) -> Z: (r, nb*mm)."""
+    dev = H.device
+    nb, mm, kk = L.nb, L.mmax, L.kmax
+    ldv = nb * mm
+    Tmp = torch.zeros((r, ldv), dtype=_F64, device=dev)
+    _lib.copy2d(D, kk, nb * kk, Tmp, mm, ldv, L.k_d, kk, None, r, nb)
+    base = np.arange(nb, dtype=np.int64) * mm + L.k.astype(np.int64)
+    _lib.gemm(L.Tr, D, None, M=L.ntmax, N=r, K=kk, lda=kk, ldb=nb * kk, ldc=ldv,
+              sA=0 if getattr(L, "ti", False) else L.ntmax * kk, sB=kk, tA=1, alpha=1.0,
+              beta=0.0, batch=nb, Mb=L.nT_d, Kb=L.k_d, Cptr=_ptrs(Tmp, base, dev))
+    Z = torch.zeros((r, ldv), dtype=_F64, device=dev)
+    _lib.scatter_rows(Tmp, mm, ldv, L.perm_r, mm, Z, mm, ldv, L.m_d, mm, None, r, nb)
+    return Z
 
 
 def _sweep_up(H, fd, phi, ups):
@@ -1472,6 +1602,11 @@ def _sweep_down(H, phi, ups, out, pd_top=None):
             _mv(Wf, _fs(L, kk * mm), mm, Ups, kk, nb * kk, Phi, mm, ldv, mm, kk, L.m_d, L.k_d, nb, r,
                 -1.0, 1.0)
             del PD
+        if L.lv > 0 and getattr(L, "refine", False):  # res = F^{-1} (u - L (ups - E phi_dn))
+            U = phi.pop(("u", L.lv)) - _apply_L(H, L, Ups, r)
+            Finv = L.Finv if L.Finv.is_cuda else L.Finv.to(H.device)
+            _refine_box_solve(H, L, Finv, U, Phi, r)
+            del U
         if L.leaf:
             _lib.scatter_rows(Phi, mm, ldv, L.rows, mm, out, 0, n, L.m_d, mm, None, r, nb)
 

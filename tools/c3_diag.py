@@ -21,7 +21,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--noblock", action="store_true")
 ap.add_argument("--n", type=int, default=256)
 ap.add_argument("--tol", type=float, default=1e-8)
+ap.add_argument("--steps", type=int, default=None)
+ap.add_argument("--cond", type=float, default=None)
 a = ap.parse_args()
+if a.steps is not None:
+    sd._REFINE_STEPS = a.steps
+if a.cond is not None:
+    sd._REFINE_COND = a.cond
 
 if a.noblock:
     orig = sd._invert_level_F
@@ -47,7 +53,9 @@ es = []
 for r in range(3):
     es.append(float(np.linalg.norm(f - H.matvec(x)) / np.linalg.norm(f)))
     x = x + inv.apply(f - H.matvec(x))
-print(f"n={a.n} noblock={a.noblock}: E per round {['%.2e' % e for e in es]}")
+print(f"n={a.n} noblock={a.noblock} steps={sd._REFINE_STEPS} cond={sd._REFINE_COND:.0e}: "
+      f"E per round {['%.2e' % e for e in es]}; refined levels "
+      f"{[L.lv for L in H.levels if getattr(L, 'refine', False)]}")
 for L in H.levels[1:]:
     E = getattr(L, "E", None)
     if E is None:

@@ -29,6 +29,7 @@ ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--nrhs", type=int, default=256)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--out", default="gpurun_out/kernel_trace.json")
+ap.add_argument("--dump", default="", help="also write every kernel (name, stream, start, dur, grid) here (.json.gz)")
 a = ap.parse_args()
 
 spec = KernelSpec("laplace2d", b_field=make_field("centre_bump", scale=math.pi / 2),
@@ -55,6 +56,17 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     ev1.record()
     torch.cuda.synchronize()
 step_ms = ev0.elapsed_time(ev1)
+if a.dump:
+    import gzip
+    import tempfile
+    with tempfile.NamedTemporaryFile(suffix=".json") as tf:
+        prof.export_chrome_trace(tf.name)
+        tr = json.load(open(tf.name))
+    rows = [(e["name"][:80], e["args"].get("stream"), e["ts"], e["dur"], e["args"].get("grid"),
+             e["args"].get("block"))
+            for e in tr["traceEvents"] if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
+    with gzip.open(a.dump, "wt") as fo:
+        json.dump(rows, fo)
 kern = []
 for e in prof.events():
     if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0:
