@@ -311,8 +311,10 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
   // main stream finishes the outer update of all other columns.  The two
   // touch disjoint columns of A and disjoint work buffers (the side stream
   // owns Pw/Rw/Ai/ipiv-block/scratch/pairs until `inner_done` is waited on).
-  static cudaStream_t side = nullptr;
-  if (!side) {  // highest priority: its CTAs are scheduled ahead of the trailing GEMM's
+  // per call (no process-wide state: the caller's device and stream decide),
+  // highest priority: its CTAs are scheduled ahead of the trailing GEMM's
+  cudaStream_t side = nullptr;
+  {
     int lo = 0, hi = 0;
     VF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     VF_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
@@ -397,6 +399,7 @@ extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int bat
     if ((rc = outer_gemm(C0, NB, N1 + NB1, n - N1 - NB1, st))) break;
   }
   if (pending) VF_CUDA(cudaStreamWaitEvent(st, inner_done, 0));
+  cudaStreamDestroy(side);  // released once its queued work completes
   cudaEventDestroy(ev_next);
   cudaEventDestroy(inner_done);
   prof_push(st, "gj.colswap");

@@ -45,13 +45,15 @@ class IdFactor:
         return self.right_matrix(dtype).T
 
 
-def interp_decomp_batched(mats, eps, group=1, force_blocked=False, seed=0, kfix=None):
+def interp_decomp_batched(mats, eps, group=1, force_blocked=False, seed=0, kfix=None,
+                          pairs=False):
     """IDs of a list of real matrices in one K2 launch sequence.  Matrices in
     consecutive groups of `group` share a rank (max over the group), as the
     row/column IDs of one box do in compress_outer.  `kfix` (one rank per
     matrix) turns pivoting off: T is then the least-squares solution of
-    A[:, :k] T = A[:, k:] (the compressed path's interpolation).  Returns
-    [(perm, k, T), ...]."""
+    A[:, :k] T = A[:, k:] (the compressed path's interpolation).  `pairs`:
+    columns (2t, 2t+1) are the two real components of one complex unknown
+    (pivoted pairwise, even ranks).  Returns [(perm, k, T), ...]."""
     _lib.require_cuda()
     dev = torch.device("cuda")
     count = len(mats)
@@ -77,7 +79,8 @@ def interp_decomp_batched(mats, eps, group=1, force_blocked=False, seed=0, kfix=
     kd = None if kf is None else torch.as_tensor(kf, device=dev)
     d = _lib.IdDesc(_lib.ptr(A), maxm * ldA, ldA, _lib.ptr(pv), _lib.ptr(mv), maxp, maxm, count,
                     group, float(eps), _lib.ptr(rank), _lib.ptr(perm), _lib.ptr(T), maxm * maxm,
-                    maxm, int(seed), int(force_blocked), None if kd is None else _lib.ptr(kd))
+                    maxm, int(seed), int(force_blocked), None if kd is None else _lib.ptr(kd),
+                    int(pairs))
     _lib.call("vief_id_batched", ctypes.byref(d), _lib.stream_handle())
     rank = rank.cpu().numpy()
     perm = perm.cpu().numpy()
@@ -89,31 +92,64 @@ def interp_decomp_batched(mats, eps, group=1, force_blocked=False, seed=0, kfix=
     return out
 
 
+def _realify_cols(A):
+    """Complex p x n -> real 2p x 2n whose columns (2j, 2j+1) represent
+    column j acting on Re / Im of the unknown: [Re a; Im a], [-Im a; Re a]."""
+    p, n = A.shape
+    R = np.empty((2 * p, 2 * n))
+    R[:p, 0::2], R[p:, 0::2] = A.real, A.imag
+    R[:p, 1::2], R[p:, 1::2] = -A.imag, A.real
+    return R
+
+
+def _id_real(A, eps, min_rank, max_rank, force_blocked, pairs):
+    """(perm, k, T) of a real A with the rank clamps; a clamped rank re-solves
+    T = R11^{-1} R12 for the same pivot order on the device (fixed-rank mode)."""
+    m, n = A.shape
+    perm, k, T = interp_decomp_batched([A], eps, force_blocked=force_blocked, pairs=pairs)[0]
+    unit = 2 if pairs else 1
+    k2 = max(k, min(unit * min_rank, m, n))
+    if max_rank is not None:
+        k2 = min(k2, unit * max_rank)
+    if k2 != k:
+        k = k2
+        if k == 0 or k >= n:
+            T = np.zeros((k, n - k), A.dtype)
+        else:  # same pivots, no pivoting, rank k
+            _, _, T = interp_decomp_batched([np.ascontiguousarray(A[:, perm])], eps,
+                                            force_blocked=True, kfix=[k])[0]
+    return perm, k, T
+
+
 def interp_decomp(A, eps, min_rank=0, max_rank=None, eps_abs=None, force_blocked=False):
     """Column ID by pivoted QR (dense_core.py:67-100): rank = first j with
     |R_jj| <= eps |R_00| (residual form on the blocked path), then the
-    min_rank / max_rank clamps; T = R11^{-1} R12."""
+    min_rank / max_rank clamps; T = R11^{-1} R12.  Complex A runs realified
+    with pairwise pivoting (each complex column is a pair of real columns), so
+    the skeleton is a set of complex columns and T the complex interpolation."""
     A = np.asarray(A)
     m, n = A.shape
-    if np.iscomplexobj(A):
-        raise NotImplementedError("complex IDs are not implemented on the B200 path yet")
     if n == 0 or m == 0:
         return IdFactor(np.zeros(0, np.int64), np.zeros((0, n), A.dtype), np.arange(n), 0.0)
     if eps_abs:
         raise NotImplementedError("eps_abs (O(N)-path option) is not supported")
-    perm, k, T = interp_decomp_batched([A], eps, force_blocked=force_blocked)[0]
-    k2 = max(k, min(min_rank, m, n))
-    if max_rank is not None:
-        k2 = min(k2, max_rank)
-    if k2 != k:
-        # rank clamp: recompute T for the requested rank from the same pivots
-        Ap = A[:, perm]
-        if k2 == 0:
-            T = np.zeros((0, n), A.dtype)
-        else:
-            q, r = np.linalg.qr(Ap[:, :k2])
-            T = np.linalg.solve(r, q.T @ Ap[:, k2:]) if k2 < n else np.zeros((k2, 0))
-        k = k2
+    if np.iscomplexobj(A):
+        perm2, k2, T2 = _id_real(_realify_cols(A), eps, min_rank, max_rank, force_blocked, True)
+        k = k2 // 2
+        sk = perm2[:k2:2] // 2                    # pivots come in (Re, Im) pairs
+        rest = perm2[k2:] // 2
+        _, first = np.unique(rest, return_index=True)
+        rest = rest[np.sort(first)]               # the remaining complex columns
+        perm = np.concatenate([sk, rest]).astype(np.int64)
+        pos = np.empty(2 * n, np.int64)
+        pos[perm2] = np.arange(2 * n)
+        # realified T: rows = skeleton real columns, columns = the others; the
+        # (Re, Im) block of t is [[Re t, -Im t], [Im t, Re t]] (realify_cols)
+        T = (T2[np.ix_(pos[2 * sk], pos[2 * rest] - k2)]
+             + 1j * T2[np.ix_(pos[2 * sk + 1], pos[2 * rest] - k2)]) if k and n > k else \
+            np.zeros((k, n - k), np.complex128)
+    else:
+        perm, k, T = _id_real(A, eps, min_rank, max_rank, force_blocked, False)
     if k == 0:
         return IdFactor(np.zeros(0, np.int64), np.zeros((0, n), A.dtype), perm, 0.0)
     return IdFactor(perm[:k], T if k < n else np.zeros((k, 0), A.dtype), perm)

@@ -135,3 +135,31 @@ def test_fixed_rank_is_least_squares():
             continue
         ref = np.linalg.lstsq(A[:, :k], A[:, k:], rcond=None)[0]
         assert np.linalg.norm(T - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("blocked", PATHS)
+def test_complex_id_vs_lapack(blocked):
+    """Complex IDs (realified, pairwise pivots): a planted-spectrum complex
+    matrix is reconstructed to ~eps like the reference's complex ?geqp3 ID,
+    with the same rank (dense_core.py:67-100 on complex input)."""
+    import scipy.linalg as sla
+    from paper_1303_5466_b200.dense_core import interp_decomp
+    rng = np.random.default_rng(7)
+    m, n = 180, 120
+    sv = np.logspace(0, -14, min(m, n))
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    A = (u * sv) @ v.conj().T
+    eps = 1e-8
+    f = interp_decomp(A, eps, force_blocked=blocked)
+    assert f.T.dtype == np.complex128
+    assert np.unique(f.perm).size == n
+    err = np.linalg.norm(A - reconstruct(A, f), 2) / np.linalg.norm(A, 2)
+    _, r, _ = sla.qr(A, mode="economic", pivoting=True)
+    d = np.abs(np.diag(r))
+    k_ref = int(np.argmax(d <= eps * d[0])) if (d <= eps * d[0]).any() else d.size
+    assert err <= 100 * eps, err
+    assert abs(f.rank - k_ref) <= 2, (f.rank, k_ref)
+    g = interp_decomp(A, eps, min_rank=f.rank + 5, force_blocked=blocked)   # clamp on the device
+    assert g.rank == f.rank + 5
+    assert np.linalg.norm(A - reconstruct(A, g), 2) / np.linalg.norm(A, 2) <= 100 * eps
