@@ -203,6 +203,220 @@ __global__ void __launch_bounds__(QS_THREADS) k_qrcp_smem2(
   }
 }
 
+// Register-resident variant for the leaf level (p <= 160, m <= 64): the same
+// dlaqp2 factorization with the matrix held in registers -- warp w owns
+// columns 8w..8w+7, lane l rows l + 32q (q < 5), 40 doubles per thread --
+// instead of shared memory (two 83 KB items per SM, one shared-memory load per
+// FMA).  Columns never move: pivoting only permutes the position bookkeeping
+// (col_at, the output perm), with LAPACK's first-maximum-by-position rule.
+// Per step: every warp picks the pivot from the shared partial norms
+// (redundantly, no barrier), the pivot column's warp forms the reflector
+// (dlarfg) and publishes it, one barrier, every warp reflects its unprocessed
+// columns and the owner of row i downdates their norms (dlaqp2's test), one
+// barrier.
+constexpr int QR_RPL = 5, QR_CPW = 8;  // rows per lane, columns per warp (8 warps)
+__global__ void __launch_bounds__(256, 2) k_qrcp_reg(
+    const double* A, long long sA, int lda, const int* pv, const int* mv, int* perm, int ldperm,
+    double* Rm, long long sR, int ldR, double* diag, int lddiag, double* colmax, int pairs) {
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int p = pv[b], m = mv[b];
+  __shared__ double vn1[64], vn2[64], vbuf[32 * QR_RPL];
+  __shared__ int col_at[64];
+  __shared__ unsigned char done[64];
+  __shared__ double s_tau;
+  __shared__ double redv[8];
+  const double* Ab = A + b * sA;
+  double a[QR_RPL][QR_CPW];
+#pragma unroll
+  for (int t = 0; t < QR_CPW; ++t) {
+    const int c = QR_CPW * warp + t;
+#pragma unroll
+    for (int q = 0; q < QR_RPL; ++q) {
+      const int r = lane + 32 * q;
+      a[q][t] = (c < m && r < p) ? Ab[(long long)c * lda + r] : 0.0;
+    }
+  }
+  // column norms (warp per column, its own registers)
+  double cmax = 0.0;
+#pragma unroll
+  for (int t = 0; t < QR_CPW; ++t) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < QR_RPL; ++q) s = fma(a[q][t], a[q][t], s);
+    s = sqrt(warp_sum(s));
+    const int c = QR_CPW * warp + t;
+    if (lane == 0 && c < 64) { vn1[c] = c < m ? s : -1.0; vn2[c] = s; done[c] = c >= m; }
+    cmax = fmax(cmax, c < m ? s : 0.0);
+  }
+  if (lane == 0) redv[warp] = cmax;
+  if (tid < 64) col_at[tid] = tid;
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int w = 0; w < 8; ++w) mx = fmax(mx, redv[w]);
+    colmax[b] = mx;
+  }
+  const int kmax = min(p, m);
+  const double tol3z = sqrt(2.220446049250313e-16);
+  double* db = diag + b * lddiag;
+  int prev = -1;  // physical column pivoted at the previous step
+  for (int i = 0; i < kmax; ++i) {
+    // pivot: first maximum of vn1 over positions i..m-1 (every warp, same answer)
+    int pos = 0x7fffffff;
+    double bv = -2.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = i + lane + 32 * h;
+      if (j < m) {
+        const double v = vn1[col_at[j]];
+        if (v > bv) { bv = v; pos = j; }
+      }
+    }
+    warp_argmax(bv, pos);
+    if (pairs && (i & 1)) {  // pivot 2s+1: the partner component of pivot 2s
+      const int want = prev ^ 1;
+      int at = 0x7fffffff;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = i + lane + 32 * h;
+        if (j < m && col_at[j] == want) at = j;
+      }
+      for (int o = 16; o > 0; o >>= 1) at = min(at, __shfl_xor_sync(0xffffffffu, at, o));
+      if (at < m) pos = at;
+    }
+    const int cp = col_at[pos];  // physical pivot column
+    prev = cp;
+    const int wp = cp / QR_CPW, tp = cp % QR_CPW;
+    const int qi = i >> 5, li = i & 31;
+    if (warp == wp) {
+      // dlarfg on rows i..p-1 of column cp
+      double x[QR_RPL];
+#pragma unroll
+      for (int q = 0; q < QR_RPL; ++q) {
+        double v = 0.0;
+#pragma unroll
+        for (int t = 0; t < QR_CPW; ++t) v = (t == tp) ? a[q][t] : v;
+        x[q] = v;
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < QR_RPL; ++q)
+        if (lane + 32 * q > i) s = fma(x[q], x[q], s);
+      s = warp_sum(s);
+      double xi = 0.0;
+#pragma unroll
+      for (int q = 0; q < QR_RPL; ++q) xi = (q == qi) ? x[q] : xi;
+      const double alpha = __shfl_sync(0xffffffffu, xi, li);
+      double tau = 0.0, beta = alpha, sc = 0.0;
+      if (s != 0.0) {
+        beta = -copysign(hypot(alpha, sqrt(s)), alpha);
+        tau = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+      }
+#pragma unroll
+      for (int q = 0; q < QR_RPL; ++q) {
+        const int r = lane + 32 * q;
+        vbuf[r] = r < i ? 0.0 : (r == i ? 1.0 : x[q] * sc);
+        if (r == i) {  // R(i, cp) = beta; rows below become the (unused) reflector
+#pragma unroll
+          for (int t = 0; t < QR_CPW; ++t) if (t == tp) a[q][t] = beta;
+        }
+      }
+      if (lane == 0) { s_tau = tau; db[i] = fabs(beta); }
+    }
+    __syncthreads();  // every warp has read col_at / vn1 for this step's pivot
+    if (tid == 0) {
+      done[cp] = 1;
+      vn1[cp] = -1.0;
+      const int c0 = col_at[i];  // LAPACK's interchange of positions i and pos
+      col_at[i] = cp;
+      col_at[pos] = c0;
+    }
+    const double tau = s_tau;
+    // reflect this warp's unprocessed columns: a -= tau v (v^T a), rows >= i
+    bool live[QR_CPW];
+#pragma unroll
+    for (int t = 0; t < QR_CPW; ++t) {
+      const int c = QR_CPW * warp + t;
+      live[t] = !done[c] && c != cp;
+    }
+    if (tau != 0.0) {
+      double vr[QR_RPL];
+#pragma unroll
+      for (int q = 0; q < QR_RPL; ++q) vr[q] = vbuf[lane + 32 * q];
+      double w[QR_CPW];
+#pragma unroll
+      for (int t = 0; t < QR_CPW; ++t) {
+        double d = 0.0;
+#pragma unroll
+        for (int q = 0; q < QR_RPL; ++q) d = fma(vr[q], a[q][t], d);
+        w[t] = d;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int t = 0; t < QR_CPW; ++t) w[t] += __shfl_xor_sync(0xffffffffu, w[t], o);
+#pragma unroll
+      for (int t = 0; t < QR_CPW; ++t) {
+        if (!live[t]) continue;
+        const double f = tau * w[t];
+#pragma unroll
+        for (int q = 0; q < QR_RPL; ++q) a[q][t] = fma(-f, vr[q], a[q][t]);
+      }
+    }
+    // partial norm downdate (dlaqp2) of this warp's unprocessed columns: the
+    // lane holding row i has R(i, c)
+#pragma unroll
+    for (int t = 0; t < QR_CPW; ++t) {
+      const int c = QR_CPW * warp + t;
+      if (!live[t]) continue;
+      double rij = 0.0;
+#pragma unroll
+      for (int q = 0; q < QR_RPL; ++q) rij = (q == qi) ? a[q][t] : rij;
+      rij = __shfl_sync(0xffffffffu, rij, li);
+      const double nv1 = vn1[c];
+      double nv = nv1;
+      bool exact = false;
+      if (nv1 != 0.0) {
+        const double tt = fabs(rij) / nv1;
+        const double temp = fmax(1.0 - tt * tt, 0.0);
+        const double rr = nv1 / vn2[c];
+        if (temp * rr * rr <= tol3z) exact = true;
+        else nv = nv1 * sqrt(temp);
+      }
+      if (exact) {  // warp-uniform: recompute from rows i+1..p-1
+        double ss = 0.0;
+#pragma unroll
+        for (int q = 0; q < QR_RPL; ++q)
+          if (lane + 32 * q > i) ss = fma(a[q][t], a[q][t], ss);
+        nv = sqrt(warp_sum(ss));
+        if (lane == 0) vn2[c] = nv;
+      }
+      if (lane == 0) vn1[c] = nv;
+    }
+    __syncthreads();
+  }
+  for (int i = kmax + tid; i < m; i += 256) db[i] = 0.0;
+  // R (kmax x m, positions) -> Rm; perm
+  double* Rb = Rm + b * sR;
+  int* pm = perm + b * ldperm;
+  if (tid < m) pm[tid] = col_at[tid];
+  __shared__ int pos_of[64];
+  if (tid < 64) pos_of[tid < m ? col_at[tid] : tid] = tid;
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < QR_CPW; ++t) {
+    const int c = QR_CPW * warp + t;
+    if (c >= m) continue;
+    const int j = pos_of[c];
+#pragma unroll
+    for (int q = 0; q < QR_RPL; ++q) {
+      const int r = lane + 32 * q;
+      if (r < kmax) Rb[(long long)j * ldR + r] = r <= j ? a[q][t] : 0.0;
+    }
+  }
+}
+
 // rank of small-path items: reference rule on |R_jj| (dense_core.py:81-89)
 __global__ void k_rank_small(const double* diag, int lddiag, const int* pv, const int* mv,
                              int count, double eps, int pairs, int* kout) {
@@ -215,8 +429,11 @@ __global__ void k_rank_small(const double* diag, int lddiag, const int* pv, cons
     const double top = d[0], cut = eps * top;
     if (top == 0.0 || top <= cut) k = 0;
     else {
+      // pair mode: only the even steps pivot on the largest residual (odd steps
+      // take the partner), so only they carry the |R_jj| <= eps |R_00| test
+      const int step = pairs ? 2 : 1;
       k = kmax;
-      for (int j = 0; j < kmax; ++j) if (d[j] <= cut) { k = j; break; }
+      for (int j = 0; j < kmax; j += step) if (d[j] <= cut) { k = j; break; }
     }
   }
   if (pairs && (k & 1)) k = min(k + 1, kmax);  // whole pairs
@@ -468,9 +685,11 @@ __global__ void k_store_rblock(HState S, double* Rm, long long sR, int ldR, int 
 // residual form of the reference's rule |R_jj| <= eps |R_00|).
 __global__ void __launch_bounds__(256) k_rank_check(HState S, const double* Rm, long long sR,
                                                     int ldR, const int* pv, const int* mv, int J,
-                                                    int pairs) {
+                                                    int pairs, int skip_need) {
   const int b = blockIdx.x, tid = threadIdx.x;
   if (!S.active[b] || S.done[b]) return;
+  // an item whose norms need an exact recompute decides after it (second pass)
+  if (skip_need && S.flagany[b] && !S.certany[b]) return;
   const int bs = S.bs[b];
   const int m = mv[b], p = pv[b];
   const int kmax = min(p, m);
@@ -790,10 +1009,15 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   if (small) {
     prof_push(st, "id.small_qrcp");
     double* diag = buf.get<double>((size_t)maxm * count);
-    auto fn = k_qrcp_smem2;
-    VF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small));
-    fn<<<count, QS_THREADS, smem_small, st>>>(d->A, d->sA, d->lda, d->p, d->m, d->perm, maxm, Rm,
-                                              sR, ldR, diag, maxm, colmax, d->pairs);
+    if (maxp <= 32 * QR_RPL && maxm <= 8 * QR_CPW) {  // leaf-size items: registers
+      k_qrcp_reg<<<count, 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m, d->perm, maxm, Rm, sR,
+                                        ldR, diag, maxm, colmax, d->pairs);
+    } else {
+      auto fn = k_qrcp_smem2;
+      VF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small));
+      fn<<<count, QS_THREADS, smem_small, st>>>(d->A, d->sA, d->lda, d->p, d->m, d->perm, maxm, Rm,
+                                                sR, ldR, diag, maxm, colmax, d->pairs);
+    }
     k_rank_small<<<cdiv(count, 128), 128, 0, st>>>(diag, maxm, d->p, d->m, count, d->eps,
                                                    d->pairs, kdev);
     k_group_max<<<cdiv(count / d->group, 128), 128, 0, st>>>(kdev, count, d->group);
@@ -821,7 +1045,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.Om = buf.get<double>((size_t)HS * maxp * count);
     S.OV = buf.get<double>((size_t)HS * HB * count);
     S.OVT = buf.get<double>((size_t)HS * HB * count);
-    S.any = buf.get<int>(1);
+    S.any = buf.get<int>(2);   // [0]: some group unfinished, [1]: some item needs exact norms
     S.ldtn = maxm;
     double* Om = buf.get<double>((size_t)HS * maxp);
     if (!S.Y || !S.Vw || !S.Up || !S.X || !S.Om || !Om || !S.any) {
@@ -866,6 +1090,20 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     // The sketch is kept in original coordinates: Omega_i = Omega H_1..H_i,
     // Y_trail -= Omega_i(:, J block) R(J block, trail).
     int pend = 0, Jf = 0;
+    // trailing update A(Jf:p, T0:m) -= V_cat U_cat(:, T0:m) of the pending blocks (K = 32 pend)
+    auto flush = [&](int T0) -> int {
+      prof_push(st, "id.gemm_update");
+      vief_gemm_desc u{};
+      u.A = S.Vw + Jf; u.strideA = sV; u.lda = maxp;
+      u.B = S.Up + (long long)T0 * ldU; u.strideB = sU; u.ldb = ldU;
+      u.C = d->A + (long long)T0 * d->lda + Jf; u.strideC = d->sA; u.ldc = d->lda;
+      u.M = maxp - Jf; u.N = maxm; u.K = pend * HB; u.Mb = S.pf; u.Nb = S.nrem;
+      u.alpha = -1.0; u.beta = 1.0; u.batch = count;
+      const int r = vief_dgemm_batched(&u, st);
+      pend = 0;
+      Jf = T0;
+      return r;
+    };
     int kfix_max = -1;  // fixed ranks: the block count is known up front (no per-block sync)
     if (fixed) {
       std::vector<int> hk(count);
@@ -992,56 +1230,56 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         }
       }
       // norms: downdate; columns near the cut (or with lost digits) need exact values,
-      // which are only formed on a current A (after a flush)
-      int need = 0;
-      if (!fixed) {
+      // which are only formed on a current A (after a flush).  One host round trip per
+      // block: the rank check runs for every item that needs no exact norms, and the
+      // host reads both flags at once; the rare exact-norm pass costs a second one.
+      ++pend;
+      if (fixed) {
+        if (pend == D) {
+          if ((rc = flush(T0))) return rc;
+        }
+        VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
+        k_fixed_update<<<cdiv(count, 128), 128, 0, st>>>(S, d->kfix, d->m, J, count);
+        ++g_launches;
+        continue;
+      }
       prof_push(st, "id.norms+rank");
-      VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
+      VF_CUDA(cudaMemsetAsync(S.any, 0, 2 * sizeof(int), st));
       VF_CUDA(cudaMemsetAsync(S.certany, 0, sizeof(int) * 2 * count, st));
       k_norm_downdate<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(
           d->p, d->m, S.active, S.bs, J, Rm, sR, ldR, S.tn, S.tn0, S.flag, maxm, S.cut,
           S.certany, S.flagany);
-      k_need_exact<<<cdiv(count, 128), 128, 0, st>>>(S.active, S.certany, S.flagany, count, S.any);
+      k_need_exact<<<cdiv(count, 128), 128, 0, st>>>(S.active, S.certany, S.flagany, count,
+                                                      S.any + 1);
       g_launches += 2;
-      VF_CUDA(cudaMemcpyAsync(&need, S.any, sizeof(int), cudaMemcpyDeviceToHost, st));
-      VF_CUDA(cudaStreamSynchronize(st));
-      }
-      ++pend;
-      if (pend == D || need) {  // flush: A(Jf:p, trail) -= V_cat U_cat(:, trail)  (K = 32 pend)
-        prof_push(st, "id.gemm_update");
-        vief_gemm_desc u{};
-        u.A = S.Vw + Jf; u.strideA = sV; u.lda = maxp;
-        u.B = S.Up + (long long)T0 * ldU; u.strideB = sU; u.ldb = ldU;
-        u.C = d->A + (long long)T0 * d->lda + Jf; u.strideC = d->sA; u.ldc = d->lda;
-        u.M = maxp - Jf; u.N = maxm; u.K = pend * HB; u.Mb = S.pf; u.Nb = S.nrem;
-        u.alpha = -1.0; u.beta = 1.0; u.batch = count;
-        if ((rc = vief_dgemm_batched(&u, st))) return rc;
-        pend = 0;
-        Jf = J + HB;
-        if (need) {
-          prof_push(st, "id.norms+rank");
-          k_norm_exact<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(
-              d->A, d->sA, d->lda, d->p, d->m, S.active, S.bs, J, S.tn, S.tn0, S.flag, maxm);
-          ++g_launches;
-        }
+      if (pend == D) {
+        if ((rc = flush(T0))) return rc;
       }
       prof_push(st, "id.norms+rank");
-      VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
-      if (fixed) {
-        k_fixed_update<<<cdiv(count, 128), 128, 0, st>>>(S, d->kfix, d->m, J, count);
-        ++g_launches;
-        continue;
-      } else {
-        k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J, d->pairs);
-        k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
-        g_launches += 2;
-      }
+      k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J, d->pairs, 1);
+      k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
+      g_launches += 2;
       VF_LAUNCH_CHECK("id rank");
       prof_push(st, "id.hostsync");
-      int any = 0;
-      VF_CUDA(cudaMemcpyAsync(&any, S.any, sizeof(int), cudaMemcpyDeviceToHost, st));
+      int flags[2] = {0, 0};
+      VF_CUDA(cudaMemcpyAsync(flags, S.any, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
       VF_CUDA(cudaStreamSynchronize(st));
-      if (!any) break;
+      if (flags[1]) {  // exact norms of the flagged columns on a current A, then decide
+        if (pend > 0) {
+          if ((rc = flush(T0))) return rc;
+        }
+        prof_push(st, "id.norms+rank");
+        k_norm_exact<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(
+            d->A, d->sA, d->lda, d->p, d->m, S.active, S.bs, J, S.tn, S.tn0, S.flag, maxm);
+        VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
+        k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J, d->pairs, 0);
+        k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
+        g_launches += 3;
+        VF_LAUNCH_CHECK("id rank (exact)");
+        VF_CUDA(cudaMemcpyAsync(flags, S.any, sizeof(int), cudaMemcpyDeviceToHost, st));
+        VF_CUDA(cudaStreamSynchronize(st));
+      }
+      if (!flags[0]) break;
     }
   }
   // Kmax and T

@@ -128,6 +128,16 @@ def ensure_apriori_skeletons(spec, tree, opts, support_mask=None):
     return layers
 
 
+def _levels_uniform(tree):
+    """Every level's boxes have one width and height (all translates)."""
+    for r in tree.rects:
+        r = np.asarray(r)
+        wh = np.stack([r[:, 1] - r[:, 0], r[:, 3] - r[:, 2]], 1)
+        if not (wh == wh[0]).all():
+            return False
+    return True
+
+
 def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti_mode=False,
                      support_mask=None):
     opts = opts or SolverOptions(eps=eps)
@@ -142,8 +152,12 @@ def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti
         inv.dense_matvec_source = H
         return inv
     layers = ensure_apriori_skeletons(spec, tree, opts, support_mask)
-    H, inv.factors = factorize(spec, grid, tree, eps, opts, quad, apriori=layers)
-    if ti_mode:
+    # TI mode factors the first box of every level only (solver_compressed.py:
+    # 548-552) when every box is a translate of it: uniform levels, no support
+    # mask; otherwise every box is factored and uniform levels share a record
+    share = ti_mode and support_mask is None and _levels_uniform(tree)
+    H, inv.factors = factorize(spec, grid, tree, eps, opts, quad, apriori=layers, ti=share)
+    if ti_mode and not share:
         share_level_records(inv.factors)
     inv.dense_delegate = inv.factors
     inv.dense_matvec_source = H

@@ -494,6 +494,29 @@ def _compress_level_id(H, L, pad, seed):
         L.cskel = L.rskel
 
 
+class _View:
+    """Attribute overrides over a _Level: a subset of its boxes presented to
+    the per-level routines (TI mode runs them on the first box only)."""
+
+    def __init__(self, base, **over):
+        self.__dict__["_base"] = base
+        self.__dict__.update(over)
+
+    def __getattr__(self, name):
+        return getattr(self.__dict__["_base"], name)
+
+
+def _first_box(L, attrs):
+    """One-box view of L: the per-box arrays / tensors named in `attrs` cut to
+    box 0; padded sizes (mmax, kmax, ...) stay the level's."""
+    over = dict(nb=1, ids=L.ids[:1], rects=L.rects[:1], sl=(L.sl[0], L.sl[0] + 1))
+    for a in attrs:
+        v = getattr(L, a, None)
+        if v is not None:
+            over[a] = v[:1]
+    return _View(L, **over)
+
+
 def _compress_level_apriori(H, L, layers):
     """Second half of a level's compression on the compressed path
     (solver_compressed.py:223-266, 437-483): the skeleton is the a-priori
@@ -501,7 +524,10 @@ def _compress_level_apriori(H, L, layers):
     T_up (column fields c) / T_dn (row fields b) is the least-squares solution
     of K(Z, X_sk) T = K(Z, X_rs) against the `layers` proxy rings Z.  It runs
     as the batched blocked Householder QR of [A_sk | A_rs] without pivoting
-    and with the rank fixed to |sk| (vief_id_batched, kfix): T = R11^-1 R12."""
+    and with the rank fixed to |sk| (vief_id_batched, kfix): T = R11^-1 R12.
+    TI sharing (H.ti_share, translation-invariant kernel, every box a
+    translate of the first): the fit runs for the first box only and its T is
+    every box's (solver_compressed.py:548-552 factors boxes[0] only)."""
     dev = H.device
     prob = ctypes.byref(H.problem)
     st = _lib.stream_handle
@@ -529,31 +555,34 @@ def _compress_level_apriori(H, L, layers):
                           "skeleton points (least-squares interpolation needs p >= k)")
     pv = np.maximum(p, kup).astype(np.int32)
     L.p = pp
-    _, pmax, src_xy, src_g = _level_sources(H, L, layers)   # proxy rings come first
-    p_d = _dev_i32(pp, dev)
     L.perm_r = _dev_i32(wperm, dev)
-    pts = torch.zeros((nb, mm), dtype=_I32, device=dev)       # [sk, rs] order
-    _lib.gather_int(L.rows, mm, L.perm_r, mm, pts, mm, L.m_d, mm, nb)
-    ldA = _even(pv.max())
-    A = torch.zeros((nb * g, mm, ldA), dtype=_F64, device=dev)
+    ti = bool(getattr(H, "ti_share", False)) and nb > 1
+    Fv = _first_box(L, ("m", "m_d", "rows", "cols", "perm_r")) if ti else L
+    nf = Fv.nb
+    _, pmax, src_xy, src_g = _level_sources(H, Fv, layers)   # proxy rings come first
+    p_d = _dev_i32(pp[:nf], dev)
+    pts = torch.zeros((nf, mm), dtype=_I32, device=dev)       # [sk, rs] order
+    _lib.gather_int(Fv.rows, mm, Fv.perm_r, mm, pts, mm, Fv.m_d, mm, nf)
+    ldA = _even(pv[:nf].max())
+    A = torch.zeros((nf * g, mm, ldA), dtype=_F64, device=dev)
     # kind 0: h^2 b_i K(x_i, z) (row fields: T_dn); kind 1: h^2 K(z, x_j) c_j (T_up)
-    _lib.call("vief_gen_idmat", prob, 0, _lib.ptr(pts), mm, _lib.ptr(L.m_d), mm,
+    _lib.call("vief_gen_idmat", prob, 0, _lib.ptr(pts), mm, _lib.ptr(Fv.m_d), mm,
               _lib.ptr(src_xy), _lib.ptr(src_g), pmax, _lib.ptr(p_d), pmax, _lib.ptr(A),
-              g * mm * ldA, ldA, nb, st())
+              g * mm * ldA, ldA, nf, st())
     if g == 2:
-        _lib.call("vief_gen_idmat", prob, 1, _lib.ptr(pts), mm, _lib.ptr(L.m_d), mm,
+        _lib.call("vief_gen_idmat", prob, 1, _lib.ptr(pts), mm, _lib.ptr(Fv.m_d), mm,
                   _lib.ptr(src_xy), _lib.ptr(src_g), pmax, _lib.ptr(p_d), pmax,
-                  _lib.ptr(A) + 8 * mm * ldA, g * mm * ldA, ldA, nb, st())
+                  _lib.ptr(A) + 8 * mm * ldA, g * mm * ldA, ldA, nf, st())
     del src_xy, src_g, pts
-    count = nb * g
-    pvd = _dev_i32(np.repeat(pv, g), dev)
-    mv = _dev_i32(np.repeat(L.m, g), dev)
-    kfix = _dev_i32(np.repeat(k, g), dev)
+    count = nf * g
+    pvd = _dev_i32(np.repeat(pv[:nf], g), dev)
+    mv = _dev_i32(np.repeat(L.m[:nf], g), dev)
+    kfix = _dev_i32(np.repeat(k[:nf], g), dev)
     rank = torch.zeros(count, dtype=_I32, device=dev)
     perm = torch.zeros((count, mm), dtype=_I32, device=dev)
     T = torch.zeros((count, mm, mm), dtype=_F64, device=dev)
-    _id_batched(dev, A, mm * ldA, ldA, pvd, mv, int(pv.max()), mm, count, g, float(H.eps), rank,
-                perm, T, 0, 1, kfix)
+    _id_batched(dev, A, mm * ldA, ldA, pvd, mv, int(pv[:nf].max()), mm, count, g, float(H.eps),
+                rank, perm, T, 0, 1, kfix)
     del A, perm
     L.k = k
     L.kmax = max(int(k.max()), 1)
@@ -562,16 +591,19 @@ def _compress_level_apriori(H, L, layers):
     L.ntmax = max(int(nT.max()), 1)
     L.nT_d = _dev_i32(nT, dev)
     L.perm_c = L.perm_r
-    L.Tr = torch.zeros((nb, L.ntmax, L.kmax), dtype=_F64, device=dev)
+    L.Tr = torch.zeros((nf, L.ntmax, L.kmax), dtype=_F64, device=dev)
     _lib.copy2d(T, g * mm * mm, mm, L.Tr, L.ntmax * L.kmax, L.kmax, L.k_d, L.kmax, L.nT_d,
-                L.ntmax, nb)
+                L.ntmax, nf)
     if g == 2:
         L.Tc = torch.zeros_like(L.Tr)
         _lib.copy2d(_lib.ptr(T) + 8 * mm * mm, g * mm * mm, mm, L.Tc, L.ntmax * L.kmax, L.kmax,
-                    L.k_d, L.kmax, L.nT_d, L.ntmax, nb)
+                    L.k_d, L.kmax, L.nT_d, L.ntmax, nf)
     else:
         L.Tc = L.Tr
     del T
+    if ti:  # every box's interpolation is the first box's
+        L.Tr = L.Tr.expand(nb, -1, -1).contiguous()
+        L.Tc = L.Tr if g == 1 else L.Tc.expand(nb, -1, -1).contiguous()
     L.rskel = torch.zeros((nb, L.kmax), dtype=_I32, device=dev)
     _lib.gather_int(L.rows, mm, L.perm_r, mm, L.rskel, L.kmax, L.k_d, L.kmax, nb)
     if g == 2:
@@ -708,6 +740,7 @@ def _invert_root_block(inv, L, checks=None):
     k2d = C.k_d[1:2].contiguous()
     _lib.pad_identity(S, kc * kc, kc, k2d, kc, 1)
     pmin, pmax = _lib.inv_batched(S, kc * kc, kc, kc, 1)
+    L._fpiv = (pmin, pmax)
     if checks is None:
         _check_singular(H, L, pmin, pmax, "F")
     else:
@@ -761,6 +794,7 @@ def _invert_level_F_block(inv, L, checks=None):
               alpha=-1.0, beta=1.0, batch=nb, Mb=k2d, Nb=k2d, Kb=k1d)
     _lib.pad_identity(S, s2, kc, k2d, kc, nb)
     pmin, pmax = _lib.inv_batched(S, s2, kc, kc, nb)
+    L._fpiv = (pmin, pmax)
     if checks is None:
         _check_singular(H, L, pmin, pmax, "F")
     else:
@@ -800,6 +834,8 @@ def _assemble_F(H, L):
         C = H.levels[L.lv + 1]
         kc = C.kmax
         CE = C.E if C.E.is_cuda else C.E.to(dev)
+        if getattr(C, "ti", False) and CE.shape[0] < C.nb:   # one shared record
+            CE = CE[0:1].expand(C.nb, -1, -1).contiguous()
         k1 = C.k[0::2].astype(np.int64)
         k1d, k2d = C.k_d[0::2].contiguous(), C.k_d[1::2].contiguous()
         base = np.arange(nb, dtype=np.int64) * mm * mm
@@ -822,30 +858,22 @@ def _assemble_F(H, L):
 # sweeps' x = F^-1 u would leave residuals cond(F) eps |F| |x|, where the
 # reference's LU solves (solver_dense.py:309,321 lu_solve) leave eps |F| |x|.
 # Such levels refine every box solve against F itself (x += F^-1 (u - F x),
-# _REFINE_STEPS times), which restores the LU solve's accuracy (measured at
-# c3: one-shot E = ||f - H x|| / ||f|| 17 -> the reference's 1e-4).  A level
-# is flagged when max|F| max|F^-1| (a cheap lower bound on cond_max(F))
-# exceeds _REFINE_COND; well-conditioned problems (all Laplace configs) run
-# the plain sweeps.
-_REFINE_COND = 1e8
+# _REFINE_STEPS times), which restores the LU solve's accuracy.  A level is
+# flagged when the pivot spread of its elimination, max|U_ii| / min|U_ii| (a
+# lower bound on cond(F)), exceeds _REFINE_COND; well-conditioned problems
+# (all Laplace configs) run the plain sweeps.
+_REFINE_COND = 1e6
 _REFINE_STEPS = 2
 _BLOCK_E_MAX = 1e4   # largest child |E| entry for which F^-1 is formed by block elimination
 
 
 def _level_cond_est(H, L):
-    """Device scalar max|F| * max|F^-1| of the level (no host sync)."""
-    if getattr(L, "rb", None) is not None:          # root in block form
-        G1, B12, B21, Sinv = L.rb[:4]
-        xinv = torch.maximum(G1.abs().amax(), Sinv.abs().amax())
-    else:
-        xinv = L.Finv.abs().amax()
-    if L.leaf:
-        fmax = L.D.abs().amax()
-    else:
-        C = H.levels[L.lv + 1]
-        fmax = torch.maximum(torch.maximum(L.B12.abs().amax(), L.B21.abs().amax()),
-                             C.E.abs().amax().to(H.device))
-    return xinv * fmax
+    """Device scalar: the largest max|U_ii| / min|U_ii| of the level's
+    Gauss-Jordan eliminations of F (or of its Schur complement S in block
+    form) -- a lower bound on cond(F) that costs nothing (the kernel reports
+    the pivot extremes for the singularity test)."""
+    pmin, pmax = L.__dict__.pop("_fpiv")
+    return (pmax / pmin).amax()
 
 
 def _flag_refinement(H, ests):
@@ -855,6 +883,7 @@ def _flag_refinement(H, ests):
     lv = list(ests)
     vals = torch.stack([ests[l] for l in lv]).cpu().numpy()
     for l, v in zip(lv, vals):
+        H.levels[l].cond_est = float(v)
         H.levels[l].refine = bool(not np.isfinite(v) or v > _REFINE_COND)
 
 
@@ -885,6 +914,7 @@ def _invert_level_F_impl(inv, L, checks=None):
     _lib.prof_mark("py.F_assemble")
     F = _assemble_F(H, L)
     pmin, pmax = _lib.inv_batched(F, mm * mm, mm, mm, nb)
+    L._fpiv = (pmin, pmax)
     if checks is None:
         _check_singular(H, L, pmin, pmax, "F")
     else:
@@ -1213,15 +1243,18 @@ def factor_solve(spec, grid, tree, eps, opts, f, quad=PLAIN, apriori=None):
         return H, inv, _from_device(out, f, single, H.realified)
 
 
-def factorize(spec, grid, tree, eps, opts, quad=PLAIN, apriori=None):
+def factorize(spec, grid, tree, eps, opts, quad=PLAIN, apriori=None, ti=False):
     """`apriori` = boundary-layer width: skeletons from tree.annotate_skeletons
-    (the compressed path's a-priori choice) instead of the IDs."""
+    (the compressed path's a-priori choice) instead of the IDs.  `ti` (with
+    `apriori`, a translation-invariant kernel and uniform levels): factor the
+    first box of every level only and share its record (TI mode,
+    solver_compressed.py:548-552)."""
     with _host_quiet():
-        H, inv, _ = _factorize(spec, grid, tree, eps, opts, quad, apriori=apriori)
+        H, inv, _ = _factorize(spec, grid, tree, eps, opts, quad, apriori=apriori, ti=ti)
     return H, inv
 
 
-def _factorize(spec, grid, tree, eps, opts, quad=PLAIN, rhs=None, apriori=None):
+def _factorize(spec, grid, tree, eps, opts, quad=PLAIN, rhs=None, apriori=None, ti=False):
     """compress_outer + invert_dense_block with the levels pipelined over two
     CUDA streams: level l is inverted (side stream) while level l-1 is being
     compressed (current stream).  Inverting level l needs only level l's
@@ -1230,6 +1263,7 @@ def _factorize(spec, grid, tree, eps, opts, quad=PLAIN, rhs=None, apriori=None):
     GEMMs of the other.  Singularity checks run at the end (same exception)."""
     H = Hss2dMatrix(spec, grid, tree, eps, opts, quad)
     H.apriori = apriori
+    H.ti_share = bool(ti and apriori)
     pad = H.opts.resolved_proxy_layers(H.spec)
     inv = DenseBlockInverse(H)
     # compression on the caller's stream, inversions on a second stream (a
@@ -1315,6 +1349,47 @@ def _up_level_on(stream, H, L, fd, phi, ups):
         _sweep_up_level(H, L, fd, phi, ups)
 
 
+def _ti_child_view(C):
+    """The two children of a TI parent box, both the child level's one record
+    (solver_compressed.py:548-552: factor_of(c) is the level's record)."""
+    E2 = C.E[0:1].expand(2, -1, -1).contiguous()
+    return _View(C, nb=2, k=C.k[:2], k_d=C.k_d[:2].contiguous(), E=E2, Gkeep=None)
+
+
+def _ti_invert_F(inv, L, checks=None):
+    """TI sharing: F^-1 of the level's first box only (every box is its
+    translate); the parent's F is assembled from the child level's record."""
+    H = inv.H
+    V = _first_box(L, ("m", "m_d", "D", "B12", "B21"))
+    lv1 = L.lv + 1
+    swap = not L.leaf
+    saved = H.levels[lv1] if swap else None
+    if swap:
+        H.levels[lv1] = _ti_child_view(saved)
+    try:
+        _invert_level_F(inv, V, checks)
+    finally:
+        if swap:
+            H.levels[lv1] = saved
+    for name in ("Finv", "rb"):
+        if name in V.__dict__:
+            setattr(L, name, V.__dict__[name])
+    L._ti_view = V
+
+
+def _ti_invert_rest(inv, L, checks=None):
+    """W, G, E, C of the first box; the level then holds one shared record
+    (L.ti: the sweeps read it with batch stride 0)."""
+    V = L.__dict__.pop("_ti_view")
+    if L.lv > 0:
+        V.__dict__.update({a: getattr(L, a)[:1] for a in
+                           ("k", "k_d", "perm_r", "perm_c", "Tr", "Tc", "nT_d")})
+        _invert_level_rest(inv, V, checks)
+        for name in ("E", "W", "C"):
+            setattr(L, name, V.__dict__[name])
+    L.ti = L.nb > 1
+
+
 def _factorize_levels(H, inv, pad, main, side, third=None, solve=None):
     """Compression on this thread (main stream); the inversion work is
     enqueued on the side stream by a worker thread.  Enqueueing a large
@@ -1337,11 +1412,12 @@ def _factorize_levels(H, inv, pad, main, side, third=None, solve=None):
             _compress_level_blocks(H, L)
             ev = torch.cuda.Event()
             ev.record(main)
-            w.submit(box, _invert_level_F, (inv, L, checks), ev)
+            ti = bool(getattr(H, "ti_share", False))
+            w.submit(box, _ti_invert_F if ti else _invert_level_F, (inv, L, checks), ev)
             _compress_level_id(H, L, pad, H.opts.seed)
             ev = torch.cuda.Event()
             ev.record(main)
-            w.submit(box, _invert_level_rest, (inv, L, checks), ev)
+            w.submit(box, _ti_invert_rest if ti else _invert_level_rest, (inv, L, checks), ev)
             if solve is not None:
                 fd, _, phi, ups = solve
                 w.submit(box, _up_level_on, (third, H, L, fd, phi, ups), None)

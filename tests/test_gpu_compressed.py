@@ -192,6 +192,11 @@ def test_ti_record_sharing_and_accuracy():
     inv_nti = compress_inverse(spec, grid, eps=1e-10, opts=opts, ti_mode=False)
     assert inv_ti.record_count() == inv_ti.tree.depth + 1
     assert inv_ti.nbytes() < inv_nti.nbytes() / 2   # reference: 2.6 MB vs 6.3 MB
+    # the factorization itself ran on the first box of every level only (28^2
+    # with leaf 64 is uniform): one record per level, no per-box F^-1 computed
+    Hti = inv_ti.dense_matvec_source
+    assert Hti.ti_share
+    assert all(L.Finv.shape[0] == 1 for L in Hti.levels if L.lv > 0)
     A = P.assemble_dense(spec, grid, P.PLAIN, np.arange(grid.n), np.arange(grid.n))
     v = np.random.default_rng(3).standard_normal((grid.n, 2))
     x_ti, x_nti = inv_ti.apply(v), inv_nti.apply(v)

@@ -163,3 +163,44 @@ def test_complex_id_vs_lapack(blocked):
     g = interp_decomp(A, eps, min_rank=f.rank + 5, force_blocked=blocked)   # clamp on the device
     assert g.rank == f.rank + 5
     assert np.linalg.norm(A - reconstruct(A, g), 2) / np.linalg.norm(A, 2) <= 100 * eps
+
+
+def test_leaf_qrcp_matches_lapack():
+    """Leaf-size IDs (p <= 160, m <= 64: the register-resident dlaqp2 kernel)
+    against LAPACK's ?geqp3 ID on proxy-style kernel rows: same rank, nearly
+    the same pivots, reconstruction at the tolerance; pair mode keeps
+    (2t, 2t+1) columns together."""
+    import oracle.hssd as O
+    from paper_1303_5466_b200.dense_core import interp_decomp_batched
+    rng = np.random.default_rng(11)
+    mats = []
+    for _ in range(64):
+        p, m = int(rng.integers(100, 161)), int(rng.integers(40, 65)) & ~1
+        src = rng.uniform(-1, 1, (m, 2)) * 0.25
+        th = np.linspace(0, 2 * np.pi, p, endpoint=False)
+        tgt = np.column_stack([0.8 * np.cos(th), 0.8 * np.sin(th)]) + rng.normal(0, 0.02, (p, 2))
+        mats.append(np.log(np.hypot(*(tgt[:, None, :] - src[None, :, :]).transpose(2, 0, 1))))
+    eps = 1e-10
+    same = tot = 0
+    for pairs in (False, True):
+        res = interp_decomp_batched(mats, eps, pairs=pairs)
+        for A, (perm, k, T) in zip(mats, res):
+            m = A.shape[1]
+            R = np.zeros((k, m))
+            R[np.arange(k), perm[:k]] = 1.0
+            R[:, perm[k:]] = T
+            err = np.linalg.norm(A - A[:, perm[:k]] @ R) / np.linalg.norm(A)
+            ref = O.column_id(A, eps)
+            Rr = np.zeros((ref.k, m))
+            Rr[np.arange(ref.k), ref.perm[:ref.k]] = 1.0
+            Rr[:, ref.perm[ref.k:]] = ref.T
+            err_ref = np.linalg.norm(A - A[:, ref.perm[:ref.k]] @ Rr) / np.linalg.norm(A)
+            assert err <= max(50 * eps, 5 * err_ref), (err, err_ref)
+            assert sorted(perm.tolist()) == list(range(m))
+            if pairs:
+                assert k % 2 == 0 and (perm[:k:2] ^ 1 == perm[1:k:2]).all()
+                continue
+            assert abs(k - ref.k) <= 1, (k, ref.k)
+            same += int(np.intersect1d(perm[:k], ref.perm[:ref.k]).size)
+            tot += ref.k
+    assert same >= 0.95 * tot, (same, tot)

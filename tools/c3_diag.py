@@ -61,7 +61,8 @@ for L in H.levels[1:]:
     if E is None:
         continue
     nE = [float(torch.linalg.matrix_norm(E[b, :int(L.k[b]), :int(L.k[b])], 2)) for b in range(min(L.nb, 64))]
-    print(f"L{L.lv:02d} nb={L.nb} kmax={int(L.kmax)} max||E||_2={max(nE):.2e}")
+    print(f"L{L.lv:02d} nb={L.nb} kmax={int(L.kmax)} max||E||_2={max(nE):.2e} "
+          f"pivot spread {getattr(L, 'cond_est', float('nan')):.2e}")
 # realified skeletons: fraction of skeleton unknowns (2 point + component)
 # whose partner component is not a skeleton unknown, per level
 for L in H.levels[1:]:
