@@ -906,7 +906,7 @@ def _invert_level_F_impl(inv, L, checks=None):
         # block elimination substitutes G1 = E1^{-1} for the children's explicit
         # E1; with an ill-conditioned G1 (|E| >> 1: near-resonant boxes) the two
         # differ by cond(G1) eps |E1|, so such levels invert the assembled F
-        if float(C1.E.abs().amax()) <= _BLOCK_E_MAX:
+        if float(torch.linalg.vector_norm(C1.E, float("inf"))) <= _BLOCK_E_MAX:
             if L.lv == 0:
                 return _invert_root_block(inv, L, checks)
             return _invert_level_F_block(inv, L, checks)
