@@ -194,6 +194,17 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # our arm
 
+def _stage_traffic():
+    """DRAM bytes per step of the factorization stages at 1024^2 from the
+    committed ncu launch list (tools/ncu_levels.py under ncu)."""
+    try:
+        st = json.load(open(os.path.join(ROOT, "profiles", "r02_ncu_stage_traffic.json")))["stages"]
+    except Exception:
+        return {}
+    return {"id (compress_outer)": st["id"]["dram_bytes"] + st["blocks"]["dram_bytes"],
+            "lu_schur (invert_dense_block)": st["finv"]["dram_bytes"] + st["wgec"]["dram_bytes"]}
+
+
 def _algorithmic_work(H):
     """SURVEY §8(d) per-box formulas evaluated with this run's m, k, p."""
     id_fl = lu_fl = 0.0
@@ -497,10 +508,18 @@ def run_ours(a):
                                   "up; E, W down; each once) / sweep-pair time; the SURVEY "
                                   "formula counts the reference's F_lu/E/T read twice"},
     }
+    # DRAM traffic per step of each stage: dram__bytes_read.sum + dram__bytes_write.sum
+    # summed over the stage's kernels (ncu launch list at 1024^2, committed profile)
+    traffic = _stage_traffic() if n == 1024 else {}
+    for k, v in traffic.items():
+        if k in stages:
+            stages[k]["traffic"] = v
     dom = max(stages, key=lambda s: stages[s]["seconds"])
     roof = dict(stages[dom])
     roof = {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
-            "unit": roof["unit"], "frac": roof["frac"], "traffic": None, "stage": dom,
+            "unit": roof["unit"], "frac": roof["frac"], "traffic": traffic.get(dom),
+            "traffic_unit": "bytes per step (the stage's kernels, ncu, "
+                            "profiles/r02_ncu_stage_traffic.json)", "stage": dom,
             "peak_source": "measured DMMA mma.sync.m8n8k4.f64 issue rate 37.1 TFLOP/s "
                            "(cuBLAS DGEMM 35.5); MEASURED_PEAKS.json has no FP64 entry",
             "stage_timing": "stage seconds from one untimed back-to-back (unpipelined) "

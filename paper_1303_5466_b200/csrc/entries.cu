@@ -55,20 +55,61 @@ __device__ __forceinline__ cd block_entry(const vief_problem& P, int gi, int gj)
   return mulr(mulr(tab<CPLX>(P, q), P.hh), bc);
 }
 
+// One CTA = 128 rows x KC columns of one item.  The columns' lattice
+// coordinates and fields are staged in shared memory once per CTA (no integer
+// division or field load per entry); each thread then issues all KC table
+// gathers of its row before the products and the coalesced column stores
+// (warp = 32 consecutive rows = 256 B per column).  Same operations per entry
+// as block_entry (bit-identical).
+constexpr int KC = 16;
 template <bool CPLX>
-__global__ void k_gen_block(vief_problem P, const int* I, long long sI, const int* nI, int maxI,
-                            const int* J, long long sJ, const int* nJ, int maxJ,
-                            double* out, long long sOut, double* const* outp, int ldo) {
+__global__ void __launch_bounds__(128) k_gen_block(vief_problem P, const int* __restrict__ I,
+                            long long sI, const int* nI, int maxI, const int* __restrict__ J,
+                            long long sJ, const int* nJ, int maxJ, double* __restrict__ out,
+                            long long sOut, double* const* outp, int ldo) {
   const int b = blockIdx.z;
   const int ni = nI ? nI[b] : maxI, nj = nJ ? nJ[b] : maxJ;
+  const int j0 = blockIdx.y * KC;
+  if (j0 >= nj) return;
+  const int jn = min(KC, nj - j0);
+  const int n = P.n_side;
+  __shared__ int sx[KC], sy[KC], sg[KC];
+  __shared__ double scv[KC];
+  if (threadIdx.x < jn) {
+    const int gj = J[b * sJ + j0 + threadIdx.x];
+    sg[threadIdx.x] = gj;
+    sx[threadIdx.x] = gj % n;
+    sy[threadIdx.x] = gj / n;
+    scv[threadIdx.x] = fld<CPLX>(P.cv, gj);
+  }
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j0 = blockIdx.y * 8;
   if (i >= ni) return;
   const int gi = I[b * sI + i];
-  double* o = outp ? outp[b] : out + b * sOut;
-  for (int j = j0; j < min(j0 + 8, nj); ++j) {
-    int gj = J[b * sJ + j];
-    store<CPLX>(o, (long long)j * ldo + i, block_entry<CPLX>(P, gi, gj));
+  const int xi = gi % n, yi = gi / n;
+  const double bi = fld<CPLX>(P.bv, gi);
+  double* o = outp ? outp[b] : out + b * sOut;   // element (row, col) at col * ldo + row
+  const long long o0 = (long long)j0 * ldo + i;
+  cd t[KC];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    if (c < jn) {
+      const int dx = xi - sx[c], dy = yi - sy[c];
+      t[c] = tab<CPLX>(P, dx * dx + dy * dy);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    if (c < jn) {
+      cd v;
+      if (sg[c] == gi) {
+        v = block_entry<CPLX>(P, gi, gi);
+      } else {
+        const double bc = __dmul_rn(bi, scv[c]);
+        v = mulr(mulr(t[c], P.hh), bc);
+      }
+      store<CPLX>(o, o0 + (long long)c * ldo, v);
+    }
   }
 }
 
@@ -89,21 +130,59 @@ __device__ __forceinline__ cd idmat_entry(const vief_problem& P, int kind, int g
   return mulr(mulr(t, P.hh), bc);
 }
 
-// ID matrices (p x m): row i = source, column j = work point
+// ID matrices (p x m): row i = source, column j = work point.  Same staging
+// as k_gen_block: the KC work points' coordinates and fields in shared memory,
+// the row's source data in registers, all table gathers issued first.
 template <bool CPLX>
-__global__ void k_gen_idmat(vief_problem P, int kind, const int* pts, long long sPts, const int* m,
-                            int maxm, const int* src_xy, const int* src_g, long long sSrc,
-                            const int* p, int maxp, double* out, long long sOut, int ldo) {
+__global__ void __launch_bounds__(128) k_gen_idmat(vief_problem P, int kind,
+                            const int* __restrict__ pts, long long sPts, const int* m, int maxm,
+                            const int* __restrict__ src_xy, const int* __restrict__ src_g,
+                            long long sSrc, const int* p, int maxp, double* __restrict__ out,
+                            long long sOut, int ldo) {
   const int b = blockIdx.z;
   const int mb = m ? m[b] : maxm, pb = p ? p[b] : maxp;
+  const int j0 = blockIdx.y * KC;
+  if (j0 >= mb) return;
+  const int jn = min(KC, mb - j0);
+  const int n = P.n_side;
+  __shared__ int px[KC], py[KC];
+  __shared__ double pf[KC];   // the work point's field: b (kind 0) or c (kind 1)
+  if (threadIdx.x < jn) {
+    const int gp = pts[b * sPts + j0 + threadIdx.x];
+    px[threadIdx.x] = gp % n;
+    py[threadIdx.x] = gp / n;
+    pf[threadIdx.x] = kind == 0 ? fld<CPLX>(P.bv, gp) : fld<CPLX>(P.cv, gp);
+  }
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j0 = blockIdx.y * 8;
   if (i >= pb) return;
   const int sx = src_xy[2 * (b * sSrc + i)], sy = src_xy[2 * (b * sSrc + i) + 1];
   const int sg = src_g[b * sSrc + i];
+  // near grid point: the source's field of the other side (kind 0: c, kind 1: b)
+  const double sf = sg < 0 ? 0.0 : (kind == 0 ? fld<CPLX>(P.cv, sg) : fld<CPLX>(P.bv, sg));
   double* o = out + b * sOut;
-  for (int j = j0; j < min(j0 + 8, mb); ++j)
-    store<CPLX>(o, (long long)j * ldo + i, idmat_entry<CPLX>(P, kind, pts[b * sPts + j], sx, sy, sg));
+  const long long o0 = (long long)j0 * ldo + i;
+  cd t[KC];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    if (c < jn) {
+      const int dx = px[c] - sx, dy = py[c] - sy;
+      t[c] = tab<CPLX>(P, dx * dx + dy * dy);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    if (c < jn) {
+      cd v;
+      if (sg < 0) {  // proxy point: (K*b_i)*h^2 (kind 0) / (K*c_j)*h^2 (kind 1)
+        v = mulr(mulr(t[c], pf[c]), P.hh);
+      } else {       // near grid point: (K*h^2)*(b*c), b*c in the reference's order
+        const double bc = kind == 0 ? __dmul_rn(pf[c], sf) : __dmul_rn(sf, pf[c]);
+        v = mulr(mulr(t[c], P.hh), bc);
+      }
+      store<CPLX>(o, o0 + (long long)c * ldo, v);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -236,6 +315,7 @@ extern "C" int vief_gen_block(const vief_problem* P, const int* I, long long sI,
                               int batch, void* stream) {
   if (batch <= 0 || maxI <= 0 || maxJ <= 0) return VF_OK;
   dim3 grid(cdiv(maxI, 128), cdiv(maxJ, 8), batch);
+  if (!(P->is_complex && P->realify)) grid.y = cdiv(maxJ, KC);
   if (grid.y > 65535 || batch > 65535) { set_error("gen_block: grid too large"); return VF_EARG; }
   if (P->is_complex && P->realify)
     k_gen_block_r2<<<grid, 128, 0, (cudaStream_t)stream>>>(*P, I, sI, nI, maxI, J, sJ, nJ, maxJ, out, sOut, outp, ldo);
@@ -254,6 +334,7 @@ extern "C" int vief_gen_idmat(const vief_problem* P, int kind, const int* pts, l
                               int ldo, int batch, void* stream) {
   if (batch <= 0 || maxm <= 0 || maxp <= 0) return VF_OK;
   dim3 grid(cdiv((P->is_complex && P->realify) ? 2 * maxp : maxp, 128), cdiv(maxm, 8), batch);
+  if (!(P->is_complex && P->realify)) grid.y = cdiv(maxm, KC);
   if (grid.y > 65535 || batch > 65535) { set_error("gen_idmat: grid too large"); return VF_EARG; }
   if (P->is_complex && P->realify)
     k_gen_idmat_r2<<<grid, 128, 0, (cudaStream_t)stream>>>(*P, kind, pts, sPts, m, maxm, src_xy, src_g, sSrc, p, maxp, out, sOut, ldo);
