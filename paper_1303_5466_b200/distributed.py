@@ -251,10 +251,12 @@ class ShardedInverse:
         self.apriori = apriori
         s = plan.split
         for g in self.ranks:
+            # the subtree is factored like one GPU's problem: IDs and inversions
+            # pipelined over the compression / inversion streams
             Hl = sd.Hss2dMatrix(spec, grid, tree, eps, opts, quad, level_slices=plan.slices[g])
-            Hl.apriori = apriori
-            sd.compress_levels(Hl)
-            invl = sd.invert_dense_block(Hl)
+            with sd._host_quiet():
+                Hl, invl, _ = sd._factorize(spec, grid, tree, eps, opts, quad, apriori=apriori,
+                                            H=Hl)
             self.local[g] = (Hl, invl)
         self.dev = next(iter(self.local.values()))[0].device
         self.realified = next(iter(self.local.values()))[0].realified

@@ -1254,14 +1254,16 @@ def factorize(spec, grid, tree, eps, opts, quad=PLAIN, apriori=None, ti=False):
     return H, inv
 
 
-def _factorize(spec, grid, tree, eps, opts, quad=PLAIN, rhs=None, apriori=None, ti=False):
+def _factorize(spec, grid, tree, eps, opts, quad=PLAIN, rhs=None, apriori=None, ti=False,
+               H=None):
     """compress_outer + invert_dense_block with the levels pipelined over two
     CUDA streams: level l is inverted (side stream) while level l-1 is being
     compressed (current stream).  Inverting level l needs only level l's
     compression and level l+1's inversion, so this is the same computation in
     a different order; the latency-bound panels of one stage overlap the
     GEMMs of the other.  Singularity checks run at the end (same exception)."""
-    H = Hss2dMatrix(spec, grid, tree, eps, opts, quad)
+    if H is None:   # (a sharded slice passes its own object, distributed.py)
+        H = Hss2dMatrix(spec, grid, tree, eps, opts, quad)
     H.apriori = apriori
     H.ti_share = bool(ti and apriori)
     pad = H.opts.resolved_proxy_layers(H.spec)
