@@ -1,9 +1,11 @@
 // Batched FP64 GEMM / GEMV on B200.
 //
 // GEMM: DMMA tensor cores (mma.sync.aligned.m8n8k4.f64 — the only FP64 MMA on
-// sm_100a; tcgen05 has no f64 kind).  CTA tile 64x64, BK=16, 4 warps each
-// 32x32 (4x4 m8n8k4 tiles), 3-stage cp.async pipeline, shared tiles stored
-// k-major with a +4 double pad so fragment loads are bank-conflict free.
+// sm_100a; tcgen05 has no f64 kind).  CTA tile 64x64 (32x128 for M <= 32),
+// 4 warps each 32x32 (4x4 m8n8k4 tiles), cp.async pipeline: BK=16 x 3 stages
+// with 16-byte copies of element pairs when both operands are 16-byte aligned
+// with even leading dimensions, else BK=8 x 4 stages of 8-byte copies; shared
+// tiles padded (+4 doubles) so fragment loads are bank-conflict free.
 // Ragged batches: per-item M/N/K, tiles outside an item exit.
 //
 // GEMV: one pass over each matrix (HBM-streaming), column-major A read with
@@ -18,13 +20,10 @@
 namespace vf {
 extern std::atomic<long long> g_launches;
 
-#ifndef VF_GEMM_BK
-#define VF_GEMM_BK 8
-#endif
-#ifndef VF_GEMM_STAGES
-#define VF_GEMM_STAGES 4
-#endif
-constexpr int BK = VF_GEMM_BK, STAGES = VF_GEMM_STAGES, PAD = 4;
+// K-tile depth and pipeline stages: 16 x 3 when both operands load as 16-byte
+// pairs, 8 x 4 with 8-byte element copies (measured best for each)
+constexpr int PAD = 4;
+template <bool VEC2> struct KCfg { static constexpr int BK = VEC2 ? 16 : 8, STAGES = VEC2 ? 3 : 4; };
 
 struct GemmItem {
   const double* A; const double* B; double* C; int M, N, K;
@@ -48,7 +47,7 @@ __device__ __forceinline__ GemmItem gemm_item(const vief_gemm_desc& d, int b) {
 // contiguous in k is staged outer-major ([outer][k], stride BK+4 = 20).  Both
 // strides are 4 mod 16 doubles, so the 16 lanes of a half warp (g = 0..3,
 // t = 0..3) hit distinct 8-byte banks.
-template <int OUT, bool KCONTIG>
+template <int OUT, bool KCONTIG, int BK>
 struct Tile {
   static constexpr int LD = KCONTIG ? BK + PAD : OUT + PAD;
   static constexpr int SIZE = KCONTIG ? OUT * (BK + PAD) : BK * (OUT + PAD);
@@ -56,10 +55,49 @@ struct Tile {
 };
 
 // load one BK x OUT tile of an operand whose element (o, k) lives at
-// src[k*ld + o] (outer-contiguous) or src[o*ld + k] (k-contiguous)
-template <int OUT, bool KCONTIG, int NT>
+// src[k*ld + o] (outer-contiguous) or src[o*ld + k] (k-contiguous).
+// VEC: 16-byte cp.async of element pairs along the contiguous dimension (the
+// caller guarantees a 16-byte aligned base and an even ld); a pair that
+// straddles the item's edge falls back to one 8-byte copy.
+template <int OUT, bool KCONTIG, int NT, bool VEC, int BK>
 __device__ __forceinline__ void load_tile(double* S, const double* src, int ld, int o0, int k0,
                                           int O, int K, int tid) {
+  if constexpr (VEC) {
+    if (!KCONTIG) {  // pairs along o
+      constexpr int HO = OUT / 2;
+      static_assert(NT % HO == 0 || HO % NT == 0, "tile/threads");
+      constexpr int KQ = NT / HO > 0 ? NT / HO : 1;
+      constexpr int N_IT = OUT * BK / (2 * NT);
+      static_assert(N_IT >= 1, "tile/threads");
+      const int o = 2 * (tid % HO), kq = tid / HO;
+      const int go = o0 + o;
+#pragma unroll
+      for (int i = 0; i < N_IT; ++i) {
+        const int k = kq + KQ * i, gk = k0 + k;
+        double* d = S + Tile<OUT, false, BK>::at(o, k);
+        const double* g = src + (long long)gk * ld + go;
+        if (gk < K && go + 1 < O) cp_async16(d, g, 16);
+        else if (gk < K && go < O) { cp_async8(d, g, true); cp_async8(d + 1, src, false); }
+        else cp_async16(d, src, 0);
+      }
+    } else {  // pairs along k
+      constexpr int HK = BK / 2;
+      constexpr int N_IT = OUT * BK / (2 * NT);
+      static_assert(N_IT >= 1, "tile/threads");
+      const int k = 2 * (tid % HK), oq = tid / HK;
+      const int gk = k0 + k;
+#pragma unroll
+      for (int i = 0; i < N_IT; ++i) {
+        const int o = oq + (NT / HK) * i, go = o0 + o;
+        double* d = S + Tile<OUT, true, BK>::at(o, k);
+        const double* g = src + (long long)go * ld + gk;
+        if (go < O && gk + 1 < K) cp_async16(d, g, 16);
+        else if (go < O && gk < K) { cp_async8(d, g, true); cp_async8(d + 1, src, false); }
+        else cp_async16(d, src, 0);
+      }
+    }
+    return;
+  }
   constexpr int N_IT = OUT * BK / NT;
   static_assert(N_IT >= 1 && OUT * BK % NT == 0, "tile/threads");
   if (!KCONTIG) {
@@ -72,7 +110,7 @@ __device__ __forceinline__ void load_tile(double* S, const double* src, int ld, 
       for (int i = 0; i < N_IT; ++i) {
         const int k = kq + KQ * i, gk = k0 + k;
         const bool v = go < O && gk < K;
-        cp_async8(S + Tile<OUT, false>::at(o, k), v ? src + (long long)gk * ld + go : src, v);
+        cp_async8(S + Tile<OUT, false, BK>::at(o, k), v ? src + (long long)gk * ld + go : src, v);
       }
     }
   } else {
@@ -82,7 +120,7 @@ __device__ __forceinline__ void load_tile(double* S, const double* src, int ld, 
     for (int i = 0; i < N_IT; ++i) {
       const int o = oq + (NT / BK) * i, go = o0 + o;
       const bool v = go < O && gk < K;
-      cp_async8(S + Tile<OUT, true>::at(o, k), v ? src + (long long)go * ld + gk : src, v);
+      cp_async8(S + Tile<OUT, true, BK>::at(o, k), v ? src + (long long)go * ld + gk : src, v);
     }
   }
 }
@@ -95,13 +133,14 @@ __device__ __forceinline__ void load_tile(double* S, const double* src, int ld, 
 // ksplit + chunk; chunk s covers k in [s*kchunk, (s+1)*kchunk) and writes
 // alpha * partial to ws[z] (M x N, ld M of the descriptor); k_splitk_reduce
 // then sums the chunks in fixed order (deterministic) and applies beta.
-template <int BMT, int BNT, int WTM, int WTN, bool TA, bool TB>
+template <int BMT, int BNT, int WTM, int WTN, bool TA, bool TB, bool VA = false, bool VB = false>
 __global__ void __launch_bounds__((BMT / WTM) * (BNT / WTN) * 32)
     k_dgemm(vief_gemm_desc d, int ksplit, int kchunk, double* ws) {
   constexpr int NT = (BMT / WTM) * (BNT / WTN) * 32;  // one warp per WTM x WTN warp tile
   constexpr int FI = WTM / 8, FJ = WTN / 8;           // m8n8 fragments per warp
-  using TAt = Tile<BMT, TA>;    // A^T stored K x M col-major -> contiguous in k
-  using TBt = Tile<BNT, !TB>;   // B stored K x N col-major   -> contiguous in k
+  constexpr int BK = KCfg<VA && VB>::BK, STAGES = KCfg<VA && VB>::STAGES;
+  using TAt = Tile<BMT, TA, BK>;    // A^T stored K x M col-major -> contiguous in k
+  using TBt = Tile<BNT, !TB, BK>;   // B stored K x N col-major   -> contiguous in k
   constexpr int WNW = BNT / WTN;  // warps along N
   const int b = blockIdx.z / ksplit, chunk = blockIdx.z % ksplit;
   GemmItem it = gemm_item(d, b);
@@ -128,8 +167,8 @@ __global__ void __launch_bounds__((BMT / WTM) * (BNT / WTN) * 32)
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       if (s < nk) {
-        load_tile<BMT, TA, NT>(As + s * TAt::SIZE, it.A, d.lda, m0, kbeg + s * BK, it.M, kend, tid);
-        load_tile<BNT, !TB, NT>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, kbeg + s * BK, it.N, kend, tid);
+        load_tile<BMT, TA, NT, VA, BK>(As + s * TAt::SIZE, it.A, d.lda, m0, kbeg + s * BK, it.M, kend, tid);
+        load_tile<BNT, !TB, NT, VB, BK>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, kbeg + s * BK, it.N, kend, tid);
       }
       cp_async_commit();
     }
@@ -139,8 +178,8 @@ __global__ void __launch_bounds__((BMT / WTM) * (BNT / WTN) * 32)
       const int nxt = kt + STAGES - 1;
       if (nxt < nk) {
         const int s = nxt % STAGES;
-        load_tile<BMT, TA, NT>(As + s * TAt::SIZE, it.A, d.lda, m0, kbeg + nxt * BK, it.M, kend, tid);
-        load_tile<BNT, !TB, NT>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, kbeg + nxt * BK, it.N, kend, tid);
+        load_tile<BMT, TA, NT, VA, BK>(As + s * TAt::SIZE, it.A, d.lda, m0, kbeg + nxt * BK, it.M, kend, tid);
+        load_tile<BNT, !TB, NT, VB, BK>(Bs + s * TBt::SIZE, it.B, d.ldb, n0, kbeg + nxt * BK, it.N, kend, tid);
       }
       cp_async_commit();
       const double* as = As + (kt % STAGES) * TAt::SIZE;
@@ -227,12 +266,13 @@ __global__ void k_splitk_reduce(vief_gemm_desc d, int ksplit, const double* ws) 
   }
 }
 
-template <int BMT, int BNT, int WTM, int WTN, bool TA, bool TB>
+template <int BMT, int BNT, int WTM, int WTN, bool TA, bool TB, bool VA, bool VB>
 static int launch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
-  constexpr int smem = STAGES * (Tile<BMT, TA>::SIZE + Tile<BNT, !TB>::SIZE) * sizeof(double);
+  constexpr int BK = KCfg<VA && VB>::BK, STAGES = KCfg<VA && VB>::STAGES;
+  constexpr int smem = STAGES * (Tile<BMT, TA, BK>::SIZE + Tile<BNT, !TB, BK>::SIZE) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    VF_CUDA(cudaFuncSetAttribute(k_dgemm<BMT, BNT, WTM, WTN, TA, TB>,
+    VF_CUDA(cudaFuncSetAttribute(k_dgemm<BMT, BNT, WTM, WTN, TA, TB, VA, VB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
@@ -253,7 +293,7 @@ static int launch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
   if (ksplit > 1) {
     VF_CUDA(cudaMallocAsync(&ws, sizeof(double) * (size_t)d->M * d->N * d->batch * ksplit, st));
   }
-  k_dgemm<BMT, BNT, WTM, WTN, TA, TB><<<grid, (BMT / WTM) * (BNT / WTN) * 32, smem, st>>>(
+  k_dgemm<BMT, BNT, WTM, WTN, TA, TB, VA, VB><<<grid, (BMT / WTM) * (BNT / WTN) * 32, smem, st>>>(
       *d, ksplit, kchunk, ws);
   if (ksplit > 1) {
     const long long mn = (long long)d->M * d->N;
@@ -266,12 +306,29 @@ static int launch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
   return VF_OK;
 }
 
+// 16-byte operand loads when every item's base is 16-byte aligned and the
+// leading dimension is even (host-checkable: no per-item pointer arrays)
+static bool vec_ok(const double* base, long long stride, int ld, const void* ptrs) {
+  return !ptrs && base && ((reinterpret_cast<uintptr_t>(base) & 15) == 0) && !(stride & 1) &&
+         !(ld & 1);
+}
+
+template <int BMT, int BNT, int WTM, int WTN, bool TA, bool TB>
+static int launch_vec(const vief_gemm_desc* d, cudaStream_t st) {
+  const bool va = vec_ok(d->A, d->strideA, d->lda, d->Aptr);
+  const bool vb = vec_ok(d->B, d->strideB, d->ldb, d->Bptr);
+  if (va && vb) return launch_gemm<BMT, BNT, WTM, WTN, TA, TB, true, true>(d, st);
+  if (va) return launch_gemm<BMT, BNT, WTM, WTN, TA, TB, true, false>(d, st);
+  if (vb) return launch_gemm<BMT, BNT, WTM, WTN, TA, TB, false, true>(d, st);
+  return launch_gemm<BMT, BNT, WTM, WTN, TA, TB, false, false>(d, st);
+}
+
 template <int BMT, int BNT, int WTM = 32, int WTN = 32>
 static int dispatch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
-  if (!d->transA && !d->transB) return launch_gemm<BMT, BNT, WTM, WTN, false, false>(d, st);
-  if (!d->transA && d->transB) return launch_gemm<BMT, BNT, WTM, WTN, false, true>(d, st);
-  if (d->transA && !d->transB) return launch_gemm<BMT, BNT, WTM, WTN, true, false>(d, st);
-  return launch_gemm<BMT, BNT, WTM, WTN, true, true>(d, st);
+  if (!d->transA && !d->transB) return launch_vec<BMT, BNT, WTM, WTN, false, false>(d, st);
+  if (!d->transA && d->transB) return launch_vec<BMT, BNT, WTM, WTN, false, true>(d, st);
+  if (d->transA && !d->transB) return launch_vec<BMT, BNT, WTM, WTN, true, false>(d, st);
+  return launch_vec<BMT, BNT, WTM, WTN, true, true>(d, st);
 }
 
 // ---------------------------------------------------------------------------
