@@ -994,8 +994,9 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   if (d->ldT < d->maxm) { set_error("id: ldT must be >= maxm"); return VF_EARG; }
   Buf buf(st);
   const int maxm = d->maxm, maxp = d->maxp;
-  const long long sR = (long long)maxm * maxm;
-  const int ldR = maxm;
+  const int ldv = maxp + (maxp & 1);  // even: the V operands load as 16-byte pairs
+  const int ldR = maxm + (maxm & 1);   // even: R rows load as 16-byte pairs (sketch GEMM)
+  const long long sR = (long long)ldR * maxm;
   double* Rm = buf.get<double>((size_t)sR * count);
   double* colmax = buf.get<double>(count);
   if (!Rm || !colmax) { set_error("id: out of device memory"); return VF_ENOMEM; }
@@ -1037,7 +1038,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.Tt = buf.get<double>((size_t)HB * HB * count);
     S.D = maxm >= 4096 ? 8 : (maxm >= 2048 ? 4 : (maxm >= 512 ? 2 : 1));
     const int D = S.D, ldU = HB * D;
-    S.Vw = buf.get<double>((size_t)maxp * HB * D * count);
+    S.Vw = buf.get<double>((size_t)ldv * HB * D * count);
     S.Up = buf.get<double>((size_t)ldU * maxm * count);
     S.X = buf.get<double>((size_t)HB * maxm * count);
     S.G = buf.get<double>((size_t)HB * HB * D * count);
@@ -1053,7 +1054,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       return VF_ENOMEM;
     }
     prof_push(st, "id.init+sketch");
-    const long long sY = (long long)HS * maxm, sV = (long long)maxp * HB * D;
+    const long long sY = (long long)HS * maxm, sV = (long long)ldv * HB * D;
     const long long sU = (long long)ldU * maxm, sX = (long long)HB * maxm;
     const long long sOm = (long long)HS * maxp;
     k_iota<<<dim3(cdiv(maxm, 128), count), 128, 0, st>>>(d->perm, maxm, d->m, count);
@@ -1094,7 +1095,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     auto flush = [&](int T0) -> int {
       prof_push(st, "id.gemm_update");
       vief_gemm_desc u{};
-      u.A = S.Vw + Jf; u.strideA = sV; u.lda = maxp;
+      u.A = S.Vw + Jf; u.strideA = sV; u.lda = ldv;
       u.B = S.Up + (long long)T0 * ldU; u.strideB = sU; u.ldb = ldU;
       u.C = d->A + (long long)T0 * d->lda + Jf; u.strideC = d->sA; u.ldc = d->lda;
       u.M = maxp - Jf; u.N = maxm; u.K = pend * HB; u.Mb = S.pf; u.Nb = S.nrem;
@@ -1129,22 +1130,22 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         g_launches += 2;
         VF_LAUNCH_CHECK("id select/swap");
       }
-      double* Vi = S.Vw + (long long)kp * maxp;
+      double* Vi = S.Vw + (long long)kp * ldv;
       if (pend > 0) {  // make the panel current: A(Jf:p, J:J+bs) -= V_cat U_cat(:, J:J+bs)
         prof_push(st, "id.panel_catchup");
         vief_gemm_desc c{};
-        c.A = S.Vw + Jf; c.strideA = sV; c.lda = maxp;
+        c.A = S.Vw + Jf; c.strideA = sV; c.lda = ldv;
         c.B = S.Up + (long long)J * ldU; c.strideB = sU; c.ldb = ldU;
         c.C = d->A + (long long)J * d->lda + Jf; c.strideC = d->sA; c.ldc = d->lda;
         c.M = maxp - Jf; c.N = HB; c.K = kp; c.Mb = S.pf; c.Nb = S.bs;
         c.alpha = -1.0; c.beta = 1.0; c.batch = count;
         if ((rc = vief_dgemm_batched(&c, st))) return rc;
-        k_zero_rows<<<dim3(cdiv((J - Jf) * HB, 256), count), 256, 0, st>>>(Vi, sV, maxp, Jf, J,
+        k_zero_rows<<<dim3(cdiv((J - Jf) * HB, 256), count), 256, 0, st>>>(Vi, sV, ldv, Jf, J,
                                                                         S.active);
         ++g_launches;
       }
       prof_push(st, "id.panel_qr");
-      if ((rc = qr_panel(d->A, d->sA, d->lda, d->p, S.active, S.bs, J, maxp, count, Vi, sV, maxp,
+      if ((rc = qr_panel(d->A, d->sA, d->lda, d->p, S.active, S.bs, J, maxp, count, Vi, sV, ldv,
                          S.Tt, S.Rt, st)))
         return rc;
       k_store_rblock<<<count, 256, 0, st>>>(S, Rm, sR, ldR, J);
@@ -1153,7 +1154,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       {
         prof_push(st, "id.gemm_W");
         vief_gemm_desc x{};  // X_i = V_i^T A_stale(J:p, trail)
-        x.A = Vi + J; x.strideA = sV; x.lda = maxp; x.transA = 1;
+        x.A = Vi + J; x.strideA = sV; x.lda = ldv; x.transA = 1;
         x.B = d->A + (long long)T0 * d->lda + J; x.strideB = d->sA; x.ldb = d->lda;
         x.C = S.X + (long long)T0 * HB; x.strideC = sX; x.ldc = HB;
         x.M = HB; x.N = maxm; x.K = maxp - J; x.Mb = S.bs; x.Nb = S.nrem; x.Kb = S.pact;
@@ -1162,8 +1163,8 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         prof_push(st, "id.wy");
         if (pend > 0) {
           vief_gemm_desc g{};  // G = V_i^T V_cat(J:p, :)
-          g.A = Vi + J; g.strideA = sV; g.lda = maxp; g.transA = 1;
-          g.B = S.Vw + J; g.strideB = sV; g.ldb = maxp;
+          g.A = Vi + J; g.strideA = sV; g.lda = ldv; g.transA = 1;
+          g.B = S.Vw + J; g.strideB = sV; g.ldb = ldv;
           g.C = S.G; g.strideC = (long long)HB * HB * D; g.ldc = HB;
           g.M = HB; g.N = kp; g.K = maxp - J; g.Mb = S.bs; g.Kb = S.pact;
           g.alpha = 1.0; g.beta = 0.0; g.batch = count;
@@ -1189,7 +1190,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
                               maxm, count, st)))
           return rc;
         vief_gemm_desc r{};
-        r.A = S.Vw + J; r.strideA = sV; r.lda = maxp;
+        r.A = S.Vw + J; r.strideA = sV; r.lda = ldv;
         r.B = S.Up + (long long)T0 * ldU; r.strideB = sU; r.ldb = ldU;
         r.C = Rm + (long long)T0 * ldR + J; r.strideC = sR; r.ldc = ldR;
         r.M = HB; r.N = maxm; r.K = kp + HB; r.Mb = S.bs; r.Nb = S.nrem;
@@ -1201,7 +1202,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         prof_push(st, "id.sketch_downdate");
         vief_gemm_desc o1{};  // OV = Omega(:, J:p) V_i
         o1.A = S.Om + (long long)J * HS; o1.strideA = sOm; o1.lda = HS;
-        o1.B = Vi + J; o1.strideB = sV; o1.ldb = maxp;
+        o1.B = Vi + J; o1.strideB = sV; o1.ldb = ldv;
         o1.C = S.OV; o1.strideC = (long long)HS * HB; o1.ldc = HS;
         o1.M = HS; o1.N = HB; o1.K = maxp - J; o1.Mb = S.sact; o1.Nb = S.bs; o1.Kb = S.pact;
         o1.alpha = 1.0; o1.beta = 0.0; o1.batch = count;
@@ -1215,7 +1216,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         if ((rc = vief_dgemm_batched(&o2, st))) return rc;
         vief_gemm_desc o3{};  // Omega(:, J:p) -= OVT V_i^T
         o3.A = S.OVT; o3.strideA = (long long)HS * HB; o3.lda = HS;
-        o3.B = Vi + J; o3.strideB = sV; o3.ldb = maxp; o3.transB = 1;
+        o3.B = Vi + J; o3.strideB = sV; o3.ldb = ldv; o3.transB = 1;
         o3.C = S.Om + (long long)J * HS; o3.strideC = sOm; o3.ldc = HS;
         o3.M = HS; o3.N = maxp - J; o3.K = HB; o3.Mb = S.sact; o3.Nb = S.pact; o3.Kb = S.bs;
         o3.alpha = -1.0; o3.beta = 1.0; o3.batch = count;
