@@ -624,11 +624,12 @@ __global__ void k_bcast_omega(const double* Om, long long n, double* Omr, int co
 // originally at id[t] ends at pos[t]) to A (p rows), R rows < J, the pending
 // U rows, Y, perm and the norms.  Gather form: every source value of a row is
 // read (into shared memory) before any destination is written.
-constexpr int AP_T = 64;
-__global__ void __launch_bounds__(AP_T) k_apply_perm(double* A, long long sA, int lda, double* Y,
-                                                     long long sY, int ldy, int* perm, int ldperm,
-                                                     const int* pv, int J, HState S, double* Rm,
-                                                     long long sR, int ldR, int kp, int ldU) {
+constexpr int AP_T = 64, AP_Q = 4;  // rows per CTA, threads per row
+__global__ void __launch_bounds__(AP_T * AP_Q) k_apply_perm(double* A, long long sA, int lda,
+                                                           double* Y, long long sY, int ldy,
+                                                           int* perm, int ldperm, const int* pv,
+                                                           int J, HState S, double* Rm,
+                                                           long long sR, int ldR, int kp, int ldU) {
   const int b = blockIdx.y;
   if (!S.active[b]) return;
   constexpr int NM = 2 * PNB + 2;
@@ -637,19 +638,33 @@ __global__ void __launch_bounds__(AP_T) k_apply_perm(double* A, long long sA, in
   if (nm <= 0) return;
   __shared__ int ids[NM], pos[NM];
   __shared__ double vals[NM][AP_T];
-  for (int t = threadIdx.x; t < nm; t += AP_T) { ids[t] = rec[1 + t]; pos[t] = rec[1 + NM + t]; }
+  const int tid = threadIdx.x, rr = tid % AP_T, cq = tid / AP_T;
+  for (int t = tid; t < nm; t += AP_T * AP_Q) { ids[t] = rec[1 + t]; pos[t] = rec[1 + NM + t]; }
   __syncthreads();
-  const int r = blockIdx.x * AP_T + threadIdx.x;
+  const int r = blockIdx.x * AP_T + rr;
+  // the AP_Q threads of a row split its moved columns; every source value of
+  // the CTA's rows is read (into shared memory) before any destination is written
   auto apply = [&](double* base, long long ld, int nrows) {
-    if (r >= nrows) return;
-    for (int t0 = 0; t0 < nm; t0 += 8) {  // 8 independent loads in flight per thread
-      double v[8];
+    const bool on = r < nrows;
+    if (on) {
+      for (int t0 = cq; t0 < nm; t0 += 8 * AP_Q) {  // 8 independent loads in flight per thread
+        double v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = t0 + u < nm ? base[(long long)ids[t0 + u] * ld + r] : 0.0;
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + u * AP_Q;
+          v[u] = t < nm ? base[(long long)ids[t] * ld + r] : 0.0;
+        }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) if (t0 + u < nm) vals[t0 + u][threadIdx.x] = v[u];
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + u * AP_Q;
+          if (t < nm) vals[t][rr] = v[u];
+        }
+      }
     }
-    for (int t = 0; t < nm; ++t) base[(long long)pos[t] * ld + r] = vals[t][threadIdx.x];
+    __syncthreads();
+    if (on)
+      for (int t = cq; t < nm; t += AP_Q) base[(long long)pos[t] * ld + r] = vals[t][rr];
+    __syncthreads();
   };
   apply(A + b * sA, lda, pv[b]);
   apply(Rm + b * sR, ldR, J);                        // R rows of earlier blocks
@@ -661,10 +676,9 @@ __global__ void __launch_bounds__(AP_T) k_apply_perm(double* A, long long sA, in
     int* pm = perm + b * ldperm;
     double* tn = S.tn + (long long)b * S.ldtn;
     double* tn0 = S.tn0 + (long long)b * S.ldtn;
+    for (int t = tid; t < nm; t += AP_T * AP_Q) { ip[t] = pm[ids[t]]; d0[t] = tn[ids[t]]; d1[t] = tn0[ids[t]]; }
     __syncthreads();
-    for (int t = threadIdx.x; t < nm; t += AP_T) { ip[t] = pm[ids[t]]; d0[t] = tn[ids[t]]; d1[t] = tn0[ids[t]]; }
-    __syncthreads();
-    for (int t = threadIdx.x; t < nm; t += AP_T) { pm[pos[t]] = ip[t]; tn[pos[t]] = d0[t]; tn0[pos[t]] = d1[t]; }
+    for (int t = tid; t < nm; t += AP_T * AP_Q) { pm[pos[t]] = ip[t]; tn[pos[t]] = d0[t]; tn0[pos[t]] = d1[t]; }
   }
 }
 
@@ -1125,7 +1139,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
           return rc;
         prof_push(st, "id.swaps");
         k_apply_perm<<<dim3(cdiv(std::max(std::max(maxp, HS), std::max(J, kp)), AP_T), count),
-                       AP_T, 0, st>>>(d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S,
+                       AP_T * AP_Q, 0, st>>>(d->A, d->sA, d->lda, S.Y, sY, HS, d->perm, maxm, d->p, J, S,
                                       Rm, sR, ldR, kp, ldU);
         g_launches += 2;
         VF_LAUNCH_CHECK("id select/swap");
