@@ -1050,7 +1050,10 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.flag = buf.get<int>((size_t)maxm * count);
     S.Rt = buf.get<double>((size_t)HB * HB * count);
     S.Tt = buf.get<double>((size_t)HB * HB * count);
-    S.D = maxm >= 4096 ? 8 : (maxm >= 2048 ? 4 : (maxm >= 512 ? 2 : 1));
+// pending blocks per delayed trailing update (K = 32 D); measured per step at
+// 1024^2: 16/8/4/2 beats 8/4/2/1 by ~15 ms (fewer passes over the trailing
+// matrix at every level), other splits within noise
+    S.D = maxm >= 4096 ? 16 : (maxm >= 2048 ? 8 : (maxm >= 512 ? 4 : 2));
     const int D = S.D, ldU = HB * D;
     S.Vw = buf.get<double>((size_t)ldv * HB * D * count);
     S.Up = buf.get<double>((size_t)ldU * maxm * count);
