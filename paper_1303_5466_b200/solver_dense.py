@@ -613,32 +613,15 @@ def _compress_level_apriori(H, L, layers):
         L.cskel = L.rskel
 
 
-# The IDs of a level run as _ID_SPLIT = 2 slices of the batch on as
-# many streams, each driven by its own host thread (the blocked ID
-# synchronises its stream twice per column block; ctypes releases the GIL):
-# one slice's latency-bound panel and pivot-selection kernels overlap the
-# others' GEMMs.  Every item's arithmetic is unchanged except for batch-wide
-# choices (GEMM split-K, the shared flush schedule), so results are
-# deterministic for a given split.
-_ID_SPLIT = 2
-_ID_SIDE = {}
 # The IDs (compression) are the factorization's critical path; the inversions
-# fill the gaps.  Their streams get the highest priority, so the ID chain's
+# fill the gaps.  Their stream gets the highest priority, so the ID chain's
 # latency-bound cluster kernels (sketch selection, QR panels) are placed as soon
-# as SMs free up instead of queueing behind the inversion's GEMM waves.
+# as SMs free up instead of queueing behind the inversion's GEMM waves.  A
+# level's IDs run as one batch on that stream: splitting the batch over two or
+# more streams (each with its own host thread) was measured slower once the
+# inversion stream fills the ID chain's gaps (1913 ms/step with one batch vs
+# 1934 / 1946 / 1955 ms with 2 / 3 / 4 slices).
 _ID_PRIORITY = -100
-
-
-def _id_side(dev, n):
-    idx = torch.cuda.current_device() if dev.index is None else dev.index
-    ent = _ID_SIDE.get(idx)
-    if ent is None or len(ent[1]) < n:
-        from concurrent.futures import ThreadPoolExecutor
-        pool = ThreadPoolExecutor(n, thread_name_prefix="vief-id",
-                                  initializer=torch.cuda.set_device, initargs=(idx,))
-        ent = (pool, [torch.cuda.Stream(device=idx, priority=_ID_PRIORITY) for _ in range(n)])
-        _ID_SIDE[idx] = ent
-    return ent
 
 
 def _id_batched(dev, A, sA, ldA, pv, mv, maxp, mm, count, g, eps, rank, perm, T, seed, forced,
@@ -646,32 +629,10 @@ def _id_batched(dev, A, sA, ldA, pv, mv, maxp, mm, count, g, eps, rank, perm, T,
     """vief_id_batched over `count` items (groups of g share a rank); `kfix`
     (device int32, count) fixes the ranks and disables pivoting; `pairs`: the
     columns are realified complex unknowns, pivoted pairwise."""
-    def desc(lo, n):
-        return _lib.IdDesc(_lib.ptr(A) + 8 * lo * sA, sA, ldA, _lib.ptr(pv) + 4 * lo,
-                           _lib.ptr(mv) + 4 * lo, maxp, mm, n, g, eps, _lib.ptr(rank) + 4 * lo,
-                           _lib.ptr(perm) + 4 * lo * mm, _lib.ptr(T) + 8 * lo * mm * mm, mm * mm,
-                           mm, seed, forced,
-                           None if kfix is None else _lib.ptr(kfix) + 4 * lo, int(pairs))
-    nb = count // g
-    parts = min(_ID_SPLIT, nb)
-    if parts < 2:
-        _lib.call("vief_id_batched", ctypes.byref(desc(0, count)), _lib.stream_handle())
-        return
-    cut = [(nb * i // parts) * g for i in range(parts + 1)]
-    descs = [desc(cut[i], cut[i + 1] - cut[i]) for i in range(parts)]
-    pool, sides = _id_side(dev, parts - 1)
-    main = torch.cuda.current_stream(dev)
-    futs = []
-    try:
-        for d, st in zip(descs[1:], sides):
-            st.wait_stream(main)
-            futs.append(pool.submit(_lib.call, "vief_id_batched", ctypes.byref(d), st.cuda_stream))
-        _lib.call("vief_id_batched", ctypes.byref(descs[0]), main.cuda_stream)
-    finally:
-        for f in futs:
-            f.result()
-        for st in sides[:parts - 1]:
-            main.wait_stream(st)
+    d = _lib.IdDesc(_lib.ptr(A), sA, ldA, _lib.ptr(pv), _lib.ptr(mv), maxp, mm, count, g, eps,
+                    _lib.ptr(rank), _lib.ptr(perm), _lib.ptr(T), mm * mm, mm, seed, forced,
+                    None if kfix is None else _lib.ptr(kfix), int(pairs))
+    _lib.call("vief_id_batched", ctypes.byref(d), _lib.stream_handle())
 
 
 def compress_outer(spec, grid, tree, eps, opts, quad=PLAIN, spill=None):

@@ -35,7 +35,6 @@ def apply(setting):
         k, v = kv.split("=")
         setattr(sd, k, type(getattr(sd, k))(eval(v)))
     sd._SIDE.clear()
-    sd._ID_SIDE.clear()
     sd._WORKERS.clear()
     torch.cuda.synchronize()
     torch.cuda.empty_cache()

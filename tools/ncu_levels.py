@@ -36,7 +36,6 @@ def ranged(tag, fn):
     return wrap
 
 
-sd._ID_SPLIT = 1   # every kernel launched from this thread (NVTX ranges are per thread)
 sd._compress_level_blocks = ranged("blocks", sd._compress_level_blocks)
 sd._compress_level_id = ranged("id", sd._compress_level_id)
 sd._invert_level_F = ranged("finv", sd._invert_level_F)
