@@ -2,7 +2,7 @@
 // Gauss-Jordan), replacing lu_factor_checked + lu_solve(., I)
 // (dense_core.py:222-230, solver_dense.py:361-367).
 //
-// Two-level blocking.  Outer block columns of NBO = 256; inside each, inner
+// Two-level blocking.  Outer block columns of NBO = 128; inside each, inner
 // panels of 32:
 //   inner step on [c0, c0+32) (restricted to the outer block's columns):
 //     1. lu_panel  (cluster of CTAs per item, panels.cu): partial-pivoting LU
@@ -31,7 +31,9 @@ namespace vf {
 extern std::atomic<long long> g_launches;
 
 constexpr int GJ_NB = 32;    // inner panel
-constexpr int GJ_NBO = 256;  // outer block (K of the big update GEMM)
+// outer block (K of the big update GEMM); per step at 1024^2 128 beat 256 by
+// ~10 ms (shorter look-ahead chains), 64/96 and 384/512 were slower
+constexpr int GJ_NBO = 128;
 
 __global__ void k_gj_prep(double* A, long long sA, int lda, int n, int c0, int nbs, double* Pw,
                           long long sP) {
