@@ -1086,7 +1086,8 @@ static int launch_cluster(const void* fn, int count, int cs, size_t smem, cudaSt
 // cluster work spreads over the SMs
 static int pick_cs(int total, int max_slice, int count) {
   int cs = (total + max_slice - 1) / max_slice;
-  if (count * cs < 120) cs = std::max(cs, (total + 255) / 256);
+  // fewer than two CTAs per SM: spread each matrix over more, smaller CTAs
+  if (count * cs < 2 * 148) cs = std::max(cs, (total + 255) / 256);
   return std::min(16, std::max(cs, 1));
 }
 
@@ -1291,7 +1292,7 @@ int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const i
                   int ldperm, cudaStream_t st) {
   const int n = maxm - J;
   if (n <= 0) return VF_OK;
-  int cs = pick_cs(n, 512, count);
+  int cs = pick_cs(n, 256, count);   // <= 256 sketch columns per CTA (measured ~0.5 % faster than 512)
   int cols_per = (n + cs - 1) / cs;
   size_t smem = ((size_t)(HSK + 1) * cols_per + (size_t)cols_per) * sizeof(double);
   void* args[] = {(void*)&Y, (void*)&ldy, (void*)&sY, (void*)&mv, (void*)&active, (void*)&bsv,
