@@ -129,6 +129,18 @@ typedef struct {
                                          are taken pairwise (the partner of pivot 2s is pivot
                                          2s+1) and ranks are even, so the skeleton is a point set
                                          and the real ID is the realification of a complex one */
+  /* Optional cross-process rank coupling (distributed top boxes: the row ID
+   * runs on one rank and the column ID on another, and their ranks must
+   * agree, solver_dense.py:263-266 min_rank).  When set, the blocked path
+   * calls couple(0, unfinished, ctx) once per column block (the item keeps
+   * factoring, done or not, while the call returns nonzero), and both paths
+   * call couple(1, k, ctx) once at the end (returns the group's k = max over
+   * both sides: the small path factors every column, the blocked one has
+   * reached the later side's rank).  The two sides must call with the same sequence
+   * of modes; the callback does the exchange (e.g. NCCL/gloo send/recv).
+   * count must be 1 and kfix null.  NULL: no coupling. */
+  int (*couple)(int mode, int value, void* ctx);
+  void* couple_ctx;
 } vief_id_desc;
 int vief_id_batched(const vief_id_desc* d, void* stream); /* synchronises stream */
 

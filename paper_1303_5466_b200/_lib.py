@@ -40,7 +40,12 @@ class IdDesc(ctypes.Structure):
                 ("maxp", c_int), ("maxm", c_int), ("count", c_int), ("group", c_int),
                 ("eps", c_double), ("rank", c_vp), ("perm", c_vp),
                 ("T", c_vp), ("sT", c_ll), ("ldT", c_int), ("seed", ctypes.c_ulonglong),
-                ("force_blocked", c_int), ("kfix", c_vp), ("pairs", c_int)]
+                ("force_blocked", c_int), ("kfix", c_vp), ("pairs", c_int),
+                ("couple", c_vp), ("couple_ctx", c_vp)]
+
+
+# int couple(int mode, int value, void* ctx): cross-rank ID rank coupling
+COUPLE_FN = ctypes.CFUNCTYPE(c_int, c_int, c_int, c_vp)
 
 
 # name -> argtypes (all return int unless listed in _RET)

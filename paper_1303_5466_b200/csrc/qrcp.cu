@@ -773,7 +773,10 @@ __global__ void __launch_bounds__(256) k_rank_check(HState S, const double* Rm, 
 
 // group bookkeeping: a group stays active until all members are done; then
 // every member gets k = max over the group.
-__global__ void k_group_update(HState S, int count, int group) {
+// hold (cross-process coupling, vief_id_desc.couple): finished groups stay
+// active -- the other side's members may still be factoring, and the loop
+// ends when the callback says both sides are done.
+__global__ void k_group_update(HState S, int count, int group, int hold) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g * group >= count) return;
   bool all = true;
@@ -784,7 +787,10 @@ __global__ void k_group_update(HState S, int count, int group) {
     else mx = max(mx, S.k[b]);
   }
   if (all) {
-    for (int i = 0; i < group; ++i) { S.active[g * group + i] = 0; S.k[g * group + i] = mx; }
+    for (int i = 0; i < group; ++i) {
+      if (!hold) S.active[g * group + i] = 0;
+      S.k[g * group + i] = mx;
+    }
   } else {
     atomicOr(S.any, 1);
   }
@@ -1006,6 +1012,11 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   if (count > 65535) { set_error("id: count > 65535"); return VF_EARG; }
   if (d->group < 1 || count % d->group) { set_error("id: bad group"); return VF_EARG; }
   if (d->ldT < d->maxm) { set_error("id: ldT must be >= maxm"); return VF_EARG; }
+  if (d->couple && (count != 1 || d->kfix)) {
+    set_error("id: cross-process coupling needs count = 1 and no kfix");
+    return VF_EARG;
+  }
+  const int hold = d->couple ? 1 : 0;
   Buf buf(st);
   const int maxm = d->maxm, maxp = d->maxp;
   const int ldv = maxp + (maxp & 1);  // even: the V operands load as 16-byte pairs
@@ -1108,6 +1119,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     // The sketch is kept in original coordinates: Omega_i = Omega H_1..H_i,
     // Y_trail -= Omega_i(:, J block) R(J block, trail).
     int pend = 0, Jf = 0;
+    bool coupled_done = false;
     // trailing update A(Jf:p, T0:m) -= V_cat U_cat(:, T0:m) of the pending blocks (K = 32 pend)
     auto flush = [&](int T0) -> int {
       prof_push(st, "id.gemm_update");
@@ -1275,7 +1287,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
       }
       prof_push(st, "id.norms+rank");
       k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J, d->pairs, 1);
-      k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
+      k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group, hold);
       g_launches += 2;
       VF_LAUNCH_CHECK("id rank");
       prof_push(st, "id.hostsync");
@@ -1291,14 +1303,28 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
             d->A, d->sA, d->lda, d->p, d->m, S.active, S.bs, J, S.tn, S.tn0, S.flag, maxm);
         VF_CUDA(cudaMemsetAsync(S.any, 0, sizeof(int), st));
         k_rank_check<<<count, 256, 0, st>>>(S, Rm, sR, ldR, d->p, d->m, J, d->pairs, 0);
-        k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group);
+        k_group_update<<<cdiv(count / d->group, 128), 128, 0, st>>>(S, count, d->group, hold);
         g_launches += 3;
         VF_LAUNCH_CHECK("id rank (exact)");
         VF_CUDA(cudaMemcpyAsync(flags, S.any, sizeof(int), cudaMemcpyDeviceToHost, st));
         VF_CUDA(cudaStreamSynchronize(st));
       }
-      if (!flags[0]) break;
+      if (d->couple) flags[0] = d->couple(0, flags[0], d->couple_ctx);
+      if (!flags[0]) { coupled_done = true; break; }
     }
+    // the other side may run more blocks (a larger kcap): answer its per-block
+    // calls until it is done too (this side's item is finished at kcap)
+    if (d->couple && !fixed)
+      while (!coupled_done && d->couple(0, 0, d->couple_ctx)) {}
+  }
+  // coupled: group rank = max over both sides (the small path factors every
+  // column; the blocked path has factored as far as the later side's rank)
+  if (d->couple) {
+    int hk = 0;
+    VF_CUDA(cudaMemcpyAsync(&hk, kdev, sizeof(int), cudaMemcpyDeviceToHost, st));
+    VF_CUDA(cudaStreamSynchronize(st));
+    hk = d->couple(1, hk, d->couple_ctx);
+    VF_CUDA(cudaMemcpyAsync(kdev, &hk, sizeof(int), cudaMemcpyHostToDevice, st));
   }
   // Kmax and T
   {

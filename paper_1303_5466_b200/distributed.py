@@ -176,16 +176,28 @@ class TorchComm:
 
 
 class _LocalComm:
-    """Message passing between the emulated ranks of one process."""
+    """Message passing between the emulated ranks of one process (the two
+    sides of a split top box run on two threads: wait_recv blocks)."""
 
     def __init__(self):
+        import threading
         self.box = {}
+        self.cv = threading.Condition()
 
     def send(self, t, src, dst, tag):
-        self.box[(src, dst, tag)] = t
+        with self.cv:
+            self.box[(src, dst, tag)] = t
+            self.cv.notify_all()
 
     def recv(self, src, dst, tag):
-        return self.box.pop((src, dst, tag))
+        with self.cv:
+            return self.box.pop((src, dst, tag))
+
+    def wait_recv(self, src, dst, tag, timeout=600):
+        with self.cv:
+            if not self.cv.wait_for(lambda: (src, dst, tag) in self.box, timeout):
+                raise TimeoutError(f"emulated message {tag} from rank {src} never arrived")
+            return self.box.pop((src, dst, tag))
 
 
 # ---------------------------------------------------------------------------
@@ -201,6 +213,43 @@ def _interface(H, lv, item=0):
     G = getattr(L, "Gkeep", None)
     G1 = None if G is None else G[item // 2, :k, :k].contiguous()
     return k, rs, cs, E, G1
+
+
+class _Couple:
+    """vief_id_desc.couple for a top box whose row ID (side 0) and column ID
+    (side 1) run on two ranks: every call swaps one int with the peer through
+    `exchange(v) -> peer's v` and combines them (mode 0: either side still
+    factoring; mode 1: group rank = max)."""
+
+    def __init__(self, exchange):
+        self.exchange = exchange
+        self.error = None
+
+        def cb(mode, value, ctx):
+            try:
+                other = int(self.exchange(int(value)))
+            except BaseException as e:   # noqa: BLE001 -- re-raised by _id_batched
+                self.error = e
+                return 0
+            return max(value, other) if mode == 1 else int(bool(value) or bool(other))
+
+        self.fn = _lib.COUPLE_FN(cb)
+
+
+class _ThreadPair:
+    """Rendezvous of two host threads of one process (emulated ranks)."""
+
+    def __init__(self):
+        import threading
+        self.bar = threading.Barrier(2)
+        self.vals = [None, None]
+
+    def exchange(self, side, v):
+        self.vals[side] = v
+        self.bar.wait(timeout=600)
+        o = self.vals[1 - side]
+        self.bar.wait(timeout=600)
+        return o
 
 
 def _virtual_level(Ht, lv, parts, dev):
@@ -222,7 +271,8 @@ def _virtual_level(Ht, lv, parts, dev):
     for g, (k, rs, cs, E, G1) in enumerate(parts):
         V.rskel[g, :k] = rs.to(dev, _I32)
         V.cskel[g, :k] = cs.to(dev, _I32)
-        V.E[g, :k, :k] = E.to(dev)
+        if E is not None:   # (a helper computing only a column ID has no E)
+            V.E[g, :k, :k] = E.to(dev)
         if have_g and g % 2 == 0:
             V.Gkeep[g // 2, :k, :k] = G1.to(dev)
     return V
@@ -234,7 +284,7 @@ class ShardedInverse:
     all shards in this process (single-GPU validation of the sharded path)."""
 
     def __init__(self, spec, grid, tree, eps, opts, quad, world, comm=None, emulate=False,
-                 support_mask=None):
+                 support_mask=None, split_ids=True):
         self.spec, self.grid, self.tree, self.eps, self.opts, self.quad = spec, grid, tree, eps, opts, quad
         self.plan = plan = subtree_plan(tree, world)
         self.comm = comm
@@ -259,6 +309,11 @@ class ShardedInverse:
                                             H=Hl)
             self.local[g] = (Hl, invl)
         self.dev = next(iter(self.local.values()))[0].device
+        # top boxes: the row ID on the owner, the column ID on the second child's
+        # owner (idle at that level), ranks coupled per block (pivoted IDs of
+        # non-symmetric problems; a symmetric problem has one ID per box)
+        self.split_ids = (bool(split_ids) and apriori is None
+                          and next(iter(self.local.values()))[0].group == 2)
         self.realified = next(iter(self.local.values()))[0].realified
         # top boxes: (lv, j) -> (object, inverse), on the owning rank
         self.top = {}
@@ -271,18 +326,103 @@ class ShardedInverse:
                     self._send(self._iface(lv + 1, 2 * j + 1), src, owner, ("if", lv, j))
             for j in range(1 << lv):
                 owner = top_owner(plan, lv, j)
+                src = top_owner(plan, lv + 1, 2 * j + 1)
+                if self.split_ids:
+                    self._top_box_split(lv, j, owner, src)
+                    continue
                 if owner not in self.ranks:
                     continue
-                src = top_owner(plan, lv + 1, 2 * j + 1)
                 first = self._iface(lv + 1, 2 * j)
                 second = self._recv_iface(src, owner, ("if", lv, j))
-                Ht = sd.Hss2dMatrix(spec, grid, tree, eps, opts, quad,
-                                    level_slices={lv: (j, j + 1), lv + 1: (2 * j, 2 * j + 2)})
-                _virtual_level(Ht, lv + 1, [first, second], self.dev)
-                Ht.apriori = apriori
+                Ht = self._top_object(lv, j, [first, second])
                 sd.compress_levels(Ht)
                 self.top[(lv, j)] = (Ht, sd.invert_dense_block(Ht))
                 self._drop_g1(lv + 1, 2 * j)   # copied into the virtual level, consumed
+
+    def _top_object(self, lv, j, parts):
+        Ht = sd.Hss2dMatrix(self.spec, self.grid, self.tree, self.eps, self.opts, self.quad,
+                            level_slices={lv: (j, j + 1), lv + 1: (2 * j, 2 * j + 2)})
+        _virtual_level(Ht, lv + 1, parts, self.dev)
+        Ht.apriori = self.apriori
+        return Ht
+
+    def _top_box_split(self, lv, j, owner, helper):
+        """Top box j of level lv factored by two ranks: `owner` runs the row ID
+        and the whole inversion (F^-1 pipelined with its ID on the inversion
+        stream, then W, G, E, C), `helper` (the second child's owner, idle at
+        this level) runs the column ID; the IDs' ranks are coupled block by
+        block through the library callback.  Messages: the first child's
+        skeleton lists to the helper (k + 2k ints), the column ID's perm and T
+        (m ints, k (m - k) doubles) back to the owner."""
+        tag = ("top", lv, j)
+        first_here = owner in self.ranks
+        first = self._iface(lv + 1, 2 * j) if first_here else None
+        second = None
+        if first_here:
+            # the helper's interface first (it sent it before this call), then
+            # the first child's skeletons -> helper (no E: it only runs the ID)
+            second = self._recv_iface(helper, owner, ("if", lv, j))
+            k, rs, cs, _, _ = first
+            self._send_skel((k, rs, cs), owner, helper, tag + ("skel",))
+        if helper in self.ranks:
+            fk, frs, fcs = self._recv_skel(owner, helper, tag + ("skel",))
+        roles = []
+        if first_here:
+            roles.append(("owner", owner))
+        if helper in self.ranks:
+            roles.append(("helper", helper))
+        pair = _ThreadPair() if self.emulate else None
+        box = {}
+
+        def exch_for(side):
+            if self.emulate:
+                return lambda v: pair.exchange(side, v)
+            peer = helper if side == 0 else owner
+            return lambda v: self._swap_int(v, peer, first=(side == 0))
+
+        def run_owner():
+            Ht = self._top_object(lv, j, [first, second])
+            cp = _Couple(exch_for(0))
+            Ht.id_split = (0, cp, None, lambda: self._recv_col(helper, owner, tag))
+            with sd._host_quiet():
+                Ht, inv, _ = sd._factorize(self.spec, self.grid, self.tree, self.eps, self.opts,
+                                           self.quad, apriori=self.apriori, H=Ht)
+            Ht.id_split = None
+            box["owner"] = (Ht, inv)
+
+        def run_helper():
+            second = self._iface(lv + 1, 2 * j + 1)
+            Hh = self._top_object(lv, j, [(fk, frs, fcs, None, None), second])
+            cp = _Couple(exch_for(1))
+            Hh.id_split = (1, cp, lambda perm, T: self._send_col(perm, T, helper, owner, tag),
+                           None)
+            st = torch.cuda.Stream(self.dev)
+            with torch.cuda.stream(st):
+                sd.compress_levels(Hh)
+            st.synchronize()
+
+        if len(roles) == 2:   # emulated: both sides in this process, one thread each
+            import threading
+            errs = []
+
+            def guard(fn):
+                try:
+                    fn()
+                except BaseException as e:   # noqa: BLE001
+                    errs.append(e)
+            th = threading.Thread(target=guard, args=(run_helper,))
+            th.start()
+            guard(run_owner)
+            th.join()
+            if errs:
+                raise errs[0]
+        elif roles and roles[0][0] == "owner":
+            run_owner()
+        elif roles:
+            run_helper()
+        if "owner" in box:
+            self.top[(lv, j)] = box["owner"]
+            self._drop_g1(lv + 1, 2 * j)
 
     # -- messaging (emulated or torch.distributed) -----------------------------
     def _iface(self, lv, j):
@@ -315,6 +455,52 @@ class ShardedInverse:
         cs = self.comm.recv(src, torch.int64, self.dev)
         E = self.comm.recv(src, _F64, self.dev)
         return k, rs, cs, E, None
+
+    def _send_skel(self, skel, src, dst, tag):
+        if src == dst:
+            return
+        if self.emulate:
+            self._lc.send(skel, src, dst, tag)
+            return
+        k, rs, cs = skel
+        for t in (torch.tensor([k], dtype=torch.int64, device=self.dev), rs, cs):
+            self.comm.send(t, dst)
+
+    def _recv_skel(self, src, dst, tag):
+        if self.emulate:
+            return self._lc.recv(src, dst, tag)
+        k = int(self.comm.recv(src, torch.int64, self.dev).item())
+        rs = self.comm.recv(src, torch.int64, self.dev)
+        cs = self.comm.recv(src, torch.int64, self.dev)
+        return k, rs, cs
+
+    def _send_col(self, perm, T, src, dst, tag):
+        if self.emulate:
+            self._lc.send((perm, T), src, dst, tag + ("col",))
+            return
+        self.comm.send(perm, dst)
+        self.comm.send(T, dst)
+
+    def _recv_col(self, src, dst, tag):
+        if self.emulate:
+            return self._lc.wait_recv(src, dst, tag + ("col",))
+        perm = self.comm.recv(src, torch.int32, self.dev)
+        T = self.comm.recv(src, _F64, self.dev)
+        return perm, T
+
+    def _swap_int(self, v, peer, first):
+        """One int each way with `peer` (side 0 sends first)."""
+        dist = self.comm.dist
+        dev = "cpu" if self.comm.backend == "gloo" else self.dev
+        out = torch.tensor([v], dtype=torch.int64, device=dev)
+        got = torch.zeros(1, dtype=torch.int64, device=dev)
+        if first:
+            dist.send(out, peer)
+            dist.recv(got, peer)
+        else:
+            dist.recv(got, peer)
+            dist.send(out, peer)
+        return int(got.item())
 
     def _xfer(self, t, src, dst, tag):
         """Move tensor t (present on src) to dst; returns it on dst."""

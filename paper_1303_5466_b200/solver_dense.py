@@ -439,6 +439,8 @@ def _compress_level_id(H, L, pad, seed):
     # proxy + near sources and the ID matrices (solver_dense.py:250-263)
     p, pmax, src_xy, src_g = _level_sources(H, L, pad)
     L.p = p
+    if getattr(H, "id_split", None) is not None:
+        return _compress_level_id_split(H, L, p, pmax, src_xy, src_g, seed)
     g = H.group
     count = nb * g
     mm = L.mmax
@@ -492,6 +494,59 @@ def _compress_level_id(H, L, pad, seed):
         _lib.gather_int(L.cols, mm, L.perm_c, mm, L.cskel, L.kmax, L.k_d, L.kmax, nb)
     else:
         L.cskel = L.rskel
+
+
+def _compress_level_id_split(H, L, p, pmax, src_xy, src_g, seed):
+    """One side of a top box's ID pair on this process (distributed.py): the
+    row ID (side 0, the box's owner) or the column ID (side 1, a helper rank),
+    with the ranks coupled across the two processes by the library's per-block
+    callback (the reference's min_rank rule, solver_dense.py:263-266, as in the
+    single-process group of two).  Side 1 hands its perm / T to `send`; side 0
+    takes the column side's from `recv` and finishes the level as
+    _compress_level_id does."""
+    side, couple, send, recv = H.id_split
+    dev = H.device
+    prob = ctypes.byref(H.problem)
+    st = _lib.stream_handle
+    if L.nb != 1 or H.group != 2:
+        raise ValueError("split IDs take one box of a non-symmetric problem")
+    mm = L.mmax
+    p_d = _dev_i32(p, dev)
+    if H.realified:
+        p = 2 * p
+    ldA = _even(p.max())
+    A = torch.zeros((1, mm, ldA), dtype=_F64, device=dev)
+    _lib.call("vief_gen_idmat", prob, side, _lib.ptr(L.rows if side == 0 else L.cols), mm,
+              _lib.ptr(L.m_d), mm, _lib.ptr(src_xy), _lib.ptr(src_g), pmax, _lib.ptr(p_d), pmax,
+              _lib.ptr(A), mm * ldA, ldA, 1, st())
+    del src_xy, src_g
+    pv = _dev_i32(p, dev)
+    rank = torch.zeros(1, dtype=_I32, device=dev)
+    perm = torch.zeros((1, mm), dtype=_I32, device=dev)
+    T = torch.zeros((1, mm, mm), dtype=_F64, device=dev)
+    # the same per-item seed as the item's position in the single-process batch
+    _id_batched(dev, A, mm * ldA, ldA, pv, L.m_d, int(p.max()), mm, 1, 1, float(H.eps), rank,
+                perm, T, int(seed) * 1000003 + L.lv, int(getattr(H, "_force_blocked", 0)),
+                pairs=H.realified, couple=couple)
+    del A
+    L.k = rank.cpu().numpy().astype(np.int32)
+    L.kmax = max(int(L.k.max()), 1)
+    L.k_d = _dev_i32(L.k, dev)
+    nT = L.m - L.k
+    L.ntmax = max(int(nT.max()), 1)
+    L.nT_d = _dev_i32(nT, dev)
+    Tk = torch.zeros((1, L.ntmax, L.kmax), dtype=_F64, device=dev)
+    _lib.copy2d(T, mm * mm, mm, Tk, L.ntmax * L.kmax, L.kmax, L.k_d, L.kmax, L.nT_d, L.ntmax, 1)
+    del T
+    if side == 1:
+        send(perm, Tk)
+        return
+    L.perm_r, L.Tr = perm, Tk
+    L.perm_c, L.Tc = recv()
+    L.rskel = torch.zeros((1, L.kmax), dtype=_I32, device=dev)
+    _lib.gather_int(L.rows, mm, L.perm_r, mm, L.rskel, L.kmax, L.k_d, L.kmax, 1)
+    L.cskel = torch.zeros((1, L.kmax), dtype=_I32, device=dev)
+    _lib.gather_int(L.cols, mm, L.perm_c, mm, L.cskel, L.kmax, L.k_d, L.kmax, 1)
 
 
 class _View:
@@ -625,14 +680,19 @@ _ID_PRIORITY = -100
 
 
 def _id_batched(dev, A, sA, ldA, pv, mv, maxp, mm, count, g, eps, rank, perm, T, seed, forced,
-                kfix=None, pairs=False):
+                kfix=None, pairs=False, couple=None):
     """vief_id_batched over `count` items (groups of g share a rank); `kfix`
     (device int32, count) fixes the ranks and disables pivoting; `pairs`: the
-    columns are realified complex unknowns, pivoted pairwise."""
+    columns are realified complex unknowns, pivoted pairwise; `couple`: a
+    _lib.COUPLE_FN coupling this item's rank with another process's."""
     d = _lib.IdDesc(_lib.ptr(A), sA, ldA, _lib.ptr(pv), _lib.ptr(mv), maxp, mm, count, g, eps,
                     _lib.ptr(rank), _lib.ptr(perm), _lib.ptr(T), mm * mm, mm, seed, forced,
-                    None if kfix is None else _lib.ptr(kfix), int(pairs))
+                    None if kfix is None else _lib.ptr(kfix), int(pairs),
+                    None if couple is None else ctypes.cast(couple.fn, ctypes.c_void_p), None)
     _lib.call("vief_id_batched", ctypes.byref(d), _lib.stream_handle())
+    err = getattr(couple, "error", None)
+    if err is not None:
+        raise err
 
 
 def compress_outer(spec, grid, tree, eps, opts, quad=PLAIN, spill=None):

@@ -26,6 +26,36 @@ def test_emulated_shards_match_reference(world):
     assert np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"]) <= 1e-9
 
 
+@pytest.mark.parametrize("world", [2, 8])
+def test_split_top_ids_match_owner_only(world):
+    """Top boxes with the row ID on the owner and the column ID on a helper
+    rank (ranks coupled per block through the library callback, the two sides
+    on two threads here): same solution as the owner-only factorization and
+    as the reference, same skeleton sizes."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200.distributed import ShardedInverse
+    g = np.load(os.path.join(G, "solve_c1_128.npz"))
+    spec = P.KernelSpec("laplace2d", b_field=P.make_field("centre_bump", scale=math.pi / 2),
+                        c_field=P.make_field("one"))
+    grid = P.Grid(128)
+    tree = P.build_tree(grid, 64)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=None)
+    a = ShardedInverse(spec, grid, tree, 1e-10, opts, P.CELL, world, emulate=True)
+    b = ShardedInverse(spec, grid, tree, 1e-10, opts, P.CELL, world, emulate=True,
+                       split_ids=False)
+    assert a.split_ids and not b.split_ids
+    assert sorted(a.top) == sorted(b.top)
+    for key in a.top:
+        if key[0] == 0:
+            continue   # the root has no ID
+        La, Lb = a.top[key][0].levels[key[0]], b.top[key][0].levels[key[0]]
+        assert abs(int(La.k[0]) - int(Lb.k[0])) <= 2
+        assert La.perm_c.shape == La.perm_r.shape and La.Tc.shape == La.Tr.shape
+    xa, xb = a.apply(g["f"]), b.apply(g["f"])
+    assert np.linalg.norm(xa - g["x"]) / np.linalg.norm(g["x"]) <= 1e-9
+    assert np.linalg.norm(xa - xb) <= 1e-11 * np.linalg.norm(xb)
+
+
 def test_emulated_shards_equal_single_gpu():
     import paper_1303_5466_b200 as P
     from paper_1303_5466_b200 import solver_dense as sd

@@ -3,6 +3,8 @@
 steps (CUDA events), settings interleaved.
 
     python tools/ab_step.py _ID_PRIORITY=0 _ID_PRIORITY=-100 [--steps 3]
+    python tools/ab_step.py "env:VF_AB_D=16,8,4,2" "env:VF_AB_D=16,16,8,4"
+(settings: ';'-separated key=value; env:NAME sets an environment variable)
 """
 import argparse
 import math
@@ -31,9 +33,12 @@ F = torch.randn((grid.n, 256), dtype=torch.float64, device="cuda")
 
 
 def apply(setting):
-    for kv in setting.split(","):
-        k, v = kv.split("=")
-        setattr(sd, k, type(getattr(sd, k))(eval(v)))
+    for kv in setting.split(";"):
+        k, v = kv.split("=", 1)
+        if k.startswith("env:"):   # library knob read from the environment per call
+            os.environ[k[4:]] = v
+        else:
+            setattr(sd, k, type(getattr(sd, k))(eval(v)))
     sd._SIDE.clear()
     sd._WORKERS.clear()
     torch.cuda.synchronize()
