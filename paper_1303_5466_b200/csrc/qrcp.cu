@@ -9,7 +9,9 @@
 //    QRCP entirely in shared memory, one CTA per item, following LAPACK
 //    dlaqp2 (first-maximum pivot, partial-norm downdating with the
 //    sqrt(eps) recomputation test, dlarfg reflectors).  Rank rule as the
-//    reference: first j with |R_jj| <= eps*|R_00|.
+//    reference: first j with |R_jj| <= eps*|R_00|.  Leaf-size items
+//    (p <= 160, m <= 64) keep the matrix in registers, four lanes per column
+//    (k_qrcp_col4).
 //
 //  * large items: blocked randomized column pivoting (Martinsson et al.,
 //    HQRRP) so that the O(pmk) work runs as DMMA GEMMs instead of one BLAS-2
@@ -203,53 +205,54 @@ __global__ void __launch_bounds__(QS_THREADS) k_qrcp_smem2(
   }
 }
 
-// Register-resident variant for the leaf level (p <= 160, m <= 64): the same
-// dlaqp2 factorization with the matrix held in registers -- warp w owns
-// columns 8w..8w+7, lane l rows l + 32q (q < 5), 40 doubles per thread --
-// instead of shared memory (two 83 KB items per SM, one shared-memory load per
-// FMA).  Columns never move: pivoting only permutes the position bookkeeping
-// (col_at, the output perm), with LAPACK's first-maximum-by-position rule.
-// Per step: every warp picks the pivot from the shared partial norms
-// (redundantly, no barrier), the pivot column's warp forms the reflector
-// (dlarfg) and publishes it, one barrier, every warp reflects its unprocessed
-// columns and the owner of row i downdates their norms (dlaqp2's test), one
-// barrier.
-constexpr int QR_RPL = 5, QR_CPW = 8;  // rows per lane, columns per warp (8 warps)
-__global__ void __launch_bounds__(256, 2) k_qrcp_reg(
+// Leaf-size items, four threads per column: thread (c = tid/4, g = tid%4)
+// keeps rows g, g+4, g+8, ... of column c in registers, so every dot product
+// v^T a_c is RQ register FMAs plus a two-level shuffle inside the column's
+// four lanes (no warp-wide transpose reductions), and the reflector is read as
+// 16-byte broadcasts from a per-lane-group copy in shared memory.  Row i of
+// the current step always sits in register 0 of thread g = i % 4: after every
+// fourth step the registers rotate by one (rows advance by four), so no
+// register is ever indexed dynamically.  Rows of R are recorded per physical
+// column as they become final; columns never move.  Same dlaqp2 semantics as
+// k_qrcp_smem2 (first maximum by position, partial-norm downdating with the
+// sqrt(eps) recomputation test), same pair mode.
+template <int RQ>
+__global__ void __launch_bounds__(256, 2) k_qrcp_col4(
     const double* A, long long sA, int lda, const int* pv, const int* mv, int* perm, int ldperm,
     double* Rm, long long sR, int ldR, double* diag, int lddiag, double* colmax, int pairs) {
+  static_assert(RQ % 2 == 0, "RQ must be even (16-byte reflector loads)");
+  constexpr int VS = RQ + (((4 - RQ) % 16) + 16) % 16;  // VS = 4 mod 16: the four copies hit distinct banks
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = tid >> 2, g = tid & 3, gbase = lane & 28;
+  const unsigned gmask = 0xFu << gbase;
   const int p = pv[b], m = mv[b];
-  __shared__ double vn1[64], vn2[64], vbuf[32 * QR_RPL];
+  __shared__ __align__(16) double vb[4][VS];
+  __shared__ double Rrow[64][65];
+  __shared__ double vn1[64], vn2[64], redv[8];
   __shared__ int col_at[64];
   __shared__ unsigned char done[64];
   __shared__ double s_tau;
-  __shared__ double redv[8];
-  const double* Ab = A + b * sA;
-  double a[QR_RPL][QR_CPW];
+  const double* Ab = A + b * sA + (long long)c * lda;
+  double a[RQ];
 #pragma unroll
-  for (int t = 0; t < QR_CPW; ++t) {
-    const int c = QR_CPW * warp + t;
-#pragma unroll
-    for (int q = 0; q < QR_RPL; ++q) {
-      const int r = lane + 32 * q;
-      a[q][t] = (c < m && r < p) ? Ab[(long long)c * lda + r] : 0.0;
-    }
+  for (int q = 0; q < RQ; ++q) {
+    const int r = g + 4 * q;
+    a[q] = (c < m && r < p) ? Ab[r] : 0.0;
   }
-  // column norms (warp per column, its own registers)
-  double cmax = 0.0;
-#pragma unroll
-  for (int t = 0; t < QR_CPW; ++t) {
+  {
     double s = 0.0;
 #pragma unroll
-    for (int q = 0; q < QR_RPL; ++q) s = fma(a[q][t], a[q][t], s);
-    s = sqrt(warp_sum(s));
-    const int c = QR_CPW * warp + t;
-    if (lane == 0 && c < 64) { vn1[c] = c < m ? s : -1.0; vn2[c] = s; done[c] = c >= m; }
-    cmax = fmax(cmax, c < m ? s : 0.0);
+    for (int q = 0; q < RQ; ++q) s = fma(a[q], a[q], s);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s = sqrt(s);
+    if (g == 0) { vn1[c] = c < m ? s : -1.0; vn2[c] = s; done[c] = c >= m; }
+    double cm = c < m ? s : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+    if (lane == 0) redv[warp] = cm;
+    if (tid < 64) col_at[tid] = tid;
   }
-  if (lane == 0) redv[warp] = cmax;
-  if (tid < 64) col_at[tid] = tid;
   __syncthreads();
   if (tid == 0) {
     double mx = 0.0;
@@ -259,8 +262,11 @@ __global__ void __launch_bounds__(256, 2) k_qrcp_reg(
   const int kmax = min(p, m);
   const double tol3z = sqrt(2.220446049250313e-16);
   double* db = diag + b * lddiag;
-  int prev = -1;  // physical column pivoted at the previous step
+  int prev = -1;
+#pragma unroll 1
   for (int i = 0; i < kmax; ++i) {
+    const int ii = i & 3;
+    const bool below = g > ii;  // register 0 holds row i0 + g: below row i iff g > ii
     // pivot: first maximum of vn1 over positions i..m-1 (every warp, same answer)
     int pos = 0x7fffffff;
     double bv = -2.0;
@@ -284,47 +290,27 @@ __global__ void __launch_bounds__(256, 2) k_qrcp_reg(
       for (int o = 16; o > 0; o >>= 1) at = min(at, __shfl_xor_sync(0xffffffffu, at, o));
       if (at < m) pos = at;
     }
-    const int cp = col_at[pos];  // physical pivot column
+    const int cp = col_at[pos];
     prev = cp;
-    const int wp = cp / QR_CPW, tp = cp % QR_CPW;
-    const int qi = i >> 5, li = i & 31;
-    if (warp == wp) {
-      // dlarfg on rows i..p-1 of column cp
-      double x[QR_RPL];
+    if (c == cp) {  // dlarfg on rows i..p-1 of the pivot column (its four lanes)
+      double s = below ? a[0] * a[0] : 0.0;  // rows > i: register 0 iff g > ii, all others
 #pragma unroll
-      for (int q = 0; q < QR_RPL; ++q) {
-        double v = 0.0;
-#pragma unroll
-        for (int t = 0; t < QR_CPW; ++t) v = (t == tp) ? a[q][t] : v;
-        x[q] = v;
-      }
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < QR_RPL; ++q)
-        if (lane + 32 * q > i) s = fma(x[q], x[q], s);
-      s = warp_sum(s);
-      double xi = 0.0;
-#pragma unroll
-      for (int q = 0; q < QR_RPL; ++q) xi = (q == qi) ? x[q] : xi;
-      const double alpha = __shfl_sync(0xffffffffu, xi, li);
+      for (int q = 1; q < RQ; ++q) s = fma(a[q], a[q], s);
+      s += __shfl_xor_sync(gmask, s, 1);
+      s += __shfl_xor_sync(gmask, s, 2);
+      const double alpha = __shfl_sync(gmask, a[0], gbase | ii);
       double tau = 0.0, beta = alpha, sc = 0.0;
       if (s != 0.0) {
         beta = -copysign(hypot(alpha, sqrt(s)), alpha);
         tau = (beta - alpha) / beta;
         sc = 1.0 / (alpha - beta);
       }
+      vb[g][0] = below ? a[0] * sc : (g == ii ? 1.0 : 0.0);
 #pragma unroll
-      for (int q = 0; q < QR_RPL; ++q) {
-        const int r = lane + 32 * q;
-        vbuf[r] = r < i ? 0.0 : (r == i ? 1.0 : x[q] * sc);
-        if (r == i) {  // R(i, cp) = beta; rows below become the (unused) reflector
-#pragma unroll
-          for (int t = 0; t < QR_CPW; ++t) if (t == tp) a[q][t] = beta;
-        }
-      }
-      if (lane == 0) { s_tau = tau; db[i] = fabs(beta); }
+      for (int q = 1; q < RQ; ++q) vb[g][q] = a[q] * sc;
+      if (g == 0) { s_tau = tau; db[i] = fabs(beta); Rrow[i][cp] = beta; }
     }
-    __syncthreads();  // every warp has read col_at / vn1 for this step's pivot
+    __syncthreads();  // the reflector is published; every warp has read col_at / vn1
     if (tid == 0) {
       done[cp] = 1;
       vn1[cp] = -1.0;
@@ -333,87 +319,69 @@ __global__ void __launch_bounds__(256, 2) k_qrcp_reg(
       col_at[pos] = c0;
     }
     const double tau = s_tau;
-    // reflect this warp's unprocessed columns: a -= tau v (v^T a), rows >= i
-    bool live[QR_CPW];
+    const bool live = c < m && c != cp && !done[c];  // uniform over the column's lanes
+    if (live) {
+      if (tau != 0.0) {
+        double w0 = 0.0, w1 = 0.0;
 #pragma unroll
-    for (int t = 0; t < QR_CPW; ++t) {
-      const int c = QR_CPW * warp + t;
-      live[t] = !done[c] && c != cp;
-    }
-    if (tau != 0.0) {
-      double vr[QR_RPL];
+        for (int q = 0; q < RQ; q += 2) {
+          const double2 v2 = *reinterpret_cast<const double2*>(&vb[g][q]);
+          w0 = fma(v2.x, a[q], w0);
+          w1 = fma(v2.y, a[q + 1], w1);
+        }
+        double w = w0 + w1;
+        w += __shfl_xor_sync(gmask, w, 1);
+        w += __shfl_xor_sync(gmask, w, 2);
+        const double f = tau * w;
+        __syncwarp(gmask);  // reload the reflector below instead of holding RQ more registers
 #pragma unroll
-      for (int q = 0; q < QR_RPL; ++q) vr[q] = vbuf[lane + 32 * q];
-      double w[QR_CPW];
-#pragma unroll
-      for (int t = 0; t < QR_CPW; ++t) {
-        double d = 0.0;
-#pragma unroll
-        for (int q = 0; q < QR_RPL; ++q) d = fma(vr[q], a[q][t], d);
-        w[t] = d;
+        for (int q = 0; q < RQ; q += 2) {
+          const double2 v2 = *reinterpret_cast<const double2*>(&vb[g][q]);
+          a[q] = fma(-f, v2.x, a[q]);
+          a[q + 1] = fma(-f, v2.y, a[q + 1]);
+        }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int t = 0; t < QR_CPW; ++t) w[t] += __shfl_xor_sync(0xffffffffu, w[t], o);
-#pragma unroll
-      for (int t = 0; t < QR_CPW; ++t) {
-        if (!live[t]) continue;
-        const double f = tau * w[t];
-#pragma unroll
-        for (int q = 0; q < QR_RPL; ++q) a[q][t] = fma(-f, vr[q], a[q][t]);
-      }
-    }
-    // partial norm downdate (dlaqp2) of this warp's unprocessed columns: the
-    // lane holding row i has R(i, c)
-#pragma unroll
-    for (int t = 0; t < QR_CPW; ++t) {
-      const int c = QR_CPW * warp + t;
-      if (!live[t]) continue;
-      double rij = 0.0;
-#pragma unroll
-      for (int q = 0; q < QR_RPL; ++q) rij = (q == qi) ? a[q][t] : rij;
-      rij = __shfl_sync(0xffffffffu, rij, li);
-      const double nv1 = vn1[c];
+      // partial norm downdate (dlaqp2); R(i, c) is register 0 of lane g = ii
+      const double rij = __shfl_sync(gmask, a[0], gbase | ii);
+      const double nv1 = vn1[c], nv2 = vn2[c];
       double nv = nv1;
       bool exact = false;
       if (nv1 != 0.0) {
         const double tt = fabs(rij) / nv1;
         const double temp = fmax(1.0 - tt * tt, 0.0);
-        const double rr = nv1 / vn2[c];
+        const double rr = nv1 / nv2;
         if (temp * rr * rr <= tol3z) exact = true;
         else nv = nv1 * sqrt(temp);
       }
-      if (exact) {  // warp-uniform: recompute from rows i+1..p-1
-        double ss = 0.0;
+      if (exact) {  // uniform over the column's lanes: recompute from rows i+1..p-1
+        double ss = below ? a[0] * a[0] : 0.0;
 #pragma unroll
-        for (int q = 0; q < QR_RPL; ++q)
-          if (lane + 32 * q > i) ss = fma(a[q][t], a[q][t], ss);
-        nv = sqrt(warp_sum(ss));
-        if (lane == 0) vn2[c] = nv;
+        for (int q = 1; q < RQ; ++q) ss = fma(a[q], a[q], ss);
+        ss += __shfl_xor_sync(gmask, ss, 1);
+        ss += __shfl_xor_sync(gmask, ss, 2);
+        nv = sqrt(ss);
       }
-      if (lane == 0) vn1[c] = nv;
+      __syncwarp(gmask);
+      if (g == 0) {
+        Rrow[i][c] = rij;
+        vn1[c] = nv;
+        if (exact) vn2[c] = nv;
+      }
+    }
+    if (ii == 3) {  // rows advance by four: row i+1 is register 0 of lane 0
+#pragma unroll
+      for (int q = 0; q < RQ - 1; ++q) a[q] = a[q + 1];
+      a[RQ - 1] = 0.0;
     }
     __syncthreads();
   }
   for (int i = kmax + tid; i < m; i += 256) db[i] = 0.0;
-  // R (kmax x m, positions) -> Rm; perm
-  double* Rb = Rm + b * sR;
   int* pm = perm + b * ldperm;
   if (tid < m) pm[tid] = col_at[tid];
-  __shared__ int pos_of[64];
-  if (tid < 64) pos_of[tid < m ? col_at[tid] : tid] = tid;
-  __syncthreads();
-#pragma unroll
-  for (int t = 0; t < QR_CPW; ++t) {
-    const int c = QR_CPW * warp + t;
-    if (c >= m) continue;
-    const int j = pos_of[c];
-#pragma unroll
-    for (int q = 0; q < QR_RPL; ++q) {
-      const int r = lane + 32 * q;
-      if (r < kmax) Rb[(long long)j * ldR + r] = r <= j ? a[q][t] : 0.0;
-    }
+  double* Rb = Rm + b * sR;
+  for (int idx = tid; idx < kmax * m; idx += 256) {
+    const int r = idx % kmax, j = idx / kmax;
+    Rb[(long long)j * ldR + r] = r <= j ? Rrow[r][col_at[j]] : 0.0;
   }
 }
 
@@ -1035,9 +1003,13 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   if (small) {
     prof_push(st, "id.small_qrcp");
     double* diag = buf.get<double>((size_t)maxm * count);
-    if (maxp <= 32 * QR_RPL && maxm <= 8 * QR_CPW) {  // leaf-size items: registers
-      k_qrcp_reg<<<count, 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m, d->perm, maxm, Rm, sR,
-                                        ldR, diag, maxm, colmax, d->pairs);
+    // leaf-size items: four lanes per column, registers (measured 2 CTAs/SM with a
+    // 164-byte spill 23.5 ms vs 1 CTA/SM without 34.9 ms at 1024^2; the previous
+    // lane-per-row layout with warp transpose reductions 40.6 ms)
+    if (maxp <= 160 && maxm <= 64) {
+      auto fn = maxp <= 96 ? k_qrcp_col4<24> : k_qrcp_col4<40>;
+      fn<<<count, 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m, d->perm, maxm, Rm, sR, ldR, diag,
+                                maxm, colmax, d->pairs);
     } else {
       auto fn = k_qrcp_smem2;
       VF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small));
