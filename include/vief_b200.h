@@ -99,6 +99,10 @@ typedef struct {
   const int* Mb; const int* Nb; const int* Kb; /* optional per-item sizes */
   double alpha, beta;
   int batch;
+  int kwin;                    /* dgemm only, 0 = off: run K in windows of kwin columns, one
+                                  launch per window (short CTAs for GEMMs that share the GPU
+                                  with latency-critical kernels of another stream); the
+                                  windows accumulate into C, so rounding differs from kwin = 0 */
 } vief_gemm_desc;
 
 /* C_b = alpha*op(A_b)*op(B_b) + beta*C_b. */

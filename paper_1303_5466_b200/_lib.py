@@ -32,7 +32,7 @@ class GemmDesc(ctypes.Structure):
                 ("transA", c_int), ("transB", c_int),
                 ("M", c_int), ("N", c_int), ("K", c_int),
                 ("Mb", c_vp), ("Nb", c_vp), ("Kb", c_vp),
-                ("alpha", c_double), ("beta", c_double), ("batch", c_int)]
+                ("alpha", c_double), ("beta", c_double), ("batch", c_int), ("kwin", c_int)]
 
 
 class IdDesc(ctypes.Structure):
@@ -167,6 +167,12 @@ def require_cuda():
 # ---------------------------------------------------------------------------
 # thin typed wrappers
 
+# K window of the GEMMs issued through gemm() (vief_gemm_desc.kwin; 0 = off).
+# Set by the pipelined factorization around the inversion / sweep work that
+# runs next to the ID chain (solver_dense._factorize_levels).
+GEMM_KWIN = 0
+
+
 def gemm(A, B, C, *, M, N, K, lda, ldb, ldc, sA=0, sB=0, sC=0, tA=0, tB=0,
          alpha=1.0, beta=0.0, batch=1, Mb=None, Nb=None, Kb=None,
          Aptr=None, Bptr=None, Cptr=None):
@@ -174,7 +180,7 @@ def gemm(A, B, C, *, M, N, K, lda, ldb, ldc, sA=0, sB=0, sC=0, tA=0, tB=0,
         return
     d = GemmDesc(ptr(A), ptr(B), ptr(C), sA, sB, sC, ptr(Aptr), ptr(Bptr), ptr(Cptr),
                  lda, ldb, ldc, tA, tB, M, N, K, ptr(Mb), ptr(Nb), ptr(Kb),
-                 float(alpha), float(beta), batch)
+                 float(alpha), float(beta), batch, GEMM_KWIN)
     call("vief_dgemm_batched", ctypes.byref(d), stream_handle())
 
 
@@ -184,7 +190,7 @@ def gemv(A, x, y, *, M, K, lda, sA=0, sx=0, sy=0, tA=0, alpha=1.0, beta=0.0, bat
         return
     d = GemmDesc(ptr(A), ptr(x), ptr(y), sA, sx, sy, ptr(Aptr), ptr(xptr), ptr(yptr),
                  lda, 1, 1, tA, 0, M, 1, K, ptr(Mb), None, ptr(Kb),
-                 float(alpha), float(beta), batch)
+                 float(alpha), float(beta), batch, 0)
     call("vief_dgemv_batched", ctypes.byref(d), stream_handle())
 
 

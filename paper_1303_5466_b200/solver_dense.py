@@ -1364,6 +1364,29 @@ class _Worker:
 _WORKERS = {}
 
 
+# K window of the background GEMMs while an ID chain shares the GPU
+# (vief_gemm_desc.kwin).  The chain's cluster kernels (sketch selection, QR
+# panels) need whole SMs and wait for resident GEMM CTAs to retire; at K = 8192
+# one 64 x 64 tile runs ~1 ms.  Measured at 1024^2 (compression stream / tail /
+# step, ms): off 1686 / 204 / 1890; see DESIGN section 8.
+_BG_KWIN = 1024
+
+
+def _windowed(kwin, fn):
+    """Worker task `fn` with _lib.GEMM_KWIN = kwin while it enqueues."""
+    if not kwin:
+        return fn
+
+    def run(*args):
+        old = _lib.GEMM_KWIN
+        _lib.GEMM_KWIN = kwin
+        try:
+            return fn(*args)
+        finally:
+            _lib.GEMM_KWIN = old
+    return run
+
+
 def _up_level_on(stream, H, L, fd, phi, ups):
     """Worker task: the up sweep of level L on `stream`, after the side
     stream's inversion of L (the task runs on the worker right after it)."""
@@ -1436,14 +1459,21 @@ def _factorize_levels(H, inv, pad, main, side, third=None, solve=None):
             ev = torch.cuda.Event()
             ev.record(main)
             ti = bool(getattr(H, "ti_share", False))
-            w.submit(box, _ti_invert_F if ti else _invert_level_F, (inv, L, checks), ev)
+            # work that runs next to an ID chain (this level's F^-1 next to this
+            # level's IDs, the rest and the up sweep next to the parent level's)
+            # issues its long-K GEMMs in K windows; level 1's rest, the root and
+            # the down sweep have the GPU to themselves
+            kw_rest = _BG_KWIN if L.lv >= 2 else 0
+            w.submit(box, _windowed(_BG_KWIN, _ti_invert_F if ti else _invert_level_F),
+                     (inv, L, checks), ev)
             _compress_level_id(H, L, pad, H.opts.seed)
             ev = torch.cuda.Event()
             ev.record(main)
-            w.submit(box, _ti_invert_rest if ti else _invert_level_rest, (inv, L, checks), ev)
+            w.submit(box, _windowed(kw_rest, _ti_invert_rest if ti else _invert_level_rest),
+                     (inv, L, checks), ev)
             if solve is not None:
                 fd, _, phi, ups = solve
-                w.submit(box, _up_level_on, (third, H, L, fd, phi, ups), None)
+                w.submit(box, _windowed(kw_rest, _up_level_on), (third, H, L, fd, phi, ups), None)
             _mark(f"compress:{L.lv}")
             if box["error"] is not None:
                 break
