@@ -135,7 +135,7 @@ __device__ __forceinline__ void load_tile(double* S, const double* src, int ld, 
 // then sums the chunks in fixed order (deterministic) and applies beta.
 template <int BMT, int BNT, int WTM, int WTN, bool TA, bool TB, bool VA = false, bool VB = false>
 __global__ void __launch_bounds__((BMT / WTM) * (BNT / WTN) * 32)
-    k_dgemm(vief_gemm_desc d, int ksplit, int kchunk, double* ws) {
+    k_dgemm(vief_gemm_desc d, int ksplit, int kchunk, double* ws, int koff, int klen) {
   constexpr int NT = (BMT / WTM) * (BNT / WTN) * 32;  // one warp per WTM x WTN warp tile
   constexpr int FI = WTM / 8, FJ = WTN / 8;           // m8n8 fragments per warp
   constexpr int BK = KCfg<VA && VB>::BK, STAGES = KCfg<VA && VB>::STAGES;
@@ -146,8 +146,10 @@ __global__ void __launch_bounds__((BMT / WTM) * (BNT / WTN) * 32)
   GemmItem it = gemm_item(d, b);
   const int m0 = blockIdx.y * BMT, n0 = blockIdx.x * BNT;
   if (m0 >= it.M || n0 >= it.N) return;
-  const int kbeg = chunk * kchunk;
-  const int kend = ksplit > 1 ? min(it.K, kbeg + kchunk) : it.K;
+  // [koff, koff + klen): the K window of this launch (vief_gemm_desc.kwin)
+  const int kbeg = koff + chunk * kchunk;
+  const int kend = ksplit > 1 ? min(min(it.K, koff + klen), kbeg + kchunk) : min(it.K, koff + klen);
+  if (koff > 0 && kend <= kbeg) return;  // a later window past this item's K: C stays
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;
   double* Bs = gsm + STAGES * TAt::SIZE;
@@ -293,8 +295,23 @@ static int launch_gemm(const vief_gemm_desc* d, cudaStream_t st) {
   if (ksplit > 1) {
     VF_CUDA(cudaMallocAsync(&ws, sizeof(double) * (size_t)d->M * d->N * d->batch * ksplit, st));
   }
+  // K windows (d->kwin > 0): a long K runs as windows of kwin columns, one
+  // launch each (beta = 1 after the first), so that a CTA lasts ~0.1 ms instead
+  // of ~1 ms at K = 8192.  For GEMMs that share the GPU with the ID chain: its
+  // latency-bound cluster kernels need whole SMs and wait for the resident
+  // GEMM CTAs to retire (solver_dense._factorize_levels).
+  if (ksplit == 1 && d->kwin > 0 && d->K >= 2 * d->kwin) {
+    vief_gemm_desc w = *d;
+    for (int k0 = 0; k0 < d->K; k0 += d->kwin) {
+      k_dgemm<BMT, BNT, WTM, WTN, TA, TB, VA, VB><<<grid, (BMT / WTM) * (BNT / WTN) * 32, smem, st>>>(
+          w, 1, d->K, nullptr, k0, d->kwin);
+      w.beta = 1.0;
+      if (k0) ++g_launches;
+    }
+    return VF_OK;
+  }
   k_dgemm<BMT, BNT, WTM, WTN, TA, TB, VA, VB><<<grid, (BMT / WTM) * (BNT / WTN) * 32, smem, st>>>(
-      *d, ksplit, kchunk, ws);
+      *d, ksplit, kchunk, ws, 0, d->K);
   if (ksplit > 1) {
     const long long mn = (long long)d->M * d->N;
     dim3 rg((unsigned)std::min<long long>(cdiv((int)std::min<long long>(mn, 1 << 30), 256), 1024),

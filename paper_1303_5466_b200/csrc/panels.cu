@@ -1203,7 +1203,6 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) k_select_hh(cons
     }
     if (own) nrm = (s0 + s1) + (s2 + s3);
   }
-  double nref = nrm;  // squared norm at the last exact evaluation
   const int* pm = perm ? perm + (long long)b * ldperm + J : nullptr;  // pair mode
   const int myid = pm && own ? pm[c0 + tid] : -1;
   for (int i = 0; i < bs; ++i) {
@@ -1279,17 +1278,18 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) k_select_hh(cons
 #pragma unroll
         for (int r = 0; r < HSK; ++r) ri = (r == i) ? y[r] : ri;
         nrm = fmax(nrm - ri * ri, 0.0);
-        // dlaqp2's safeguard: a downdated squared norm that has lost ~6 digits
-        // against the last exact one is recomputed from the reflected column
-        // (rows > i), or pivots of a fast-decaying block are picked from noise
-        if (nrm <= 1e-6 * nref) {
+        // dlaqp2's safeguard against cancellation in the downdated squared
+        // norm (pivots of a fast-decaying block were picked from noise), on a
+        // fixed schedule: every 4th step the norm is recomputed from the
+        // reflected column (rows > i) -- uniform over the CTA, no extra state
+        if ((i & 3) == 3) {
           double s0 = 0.0, s1 = 0.0;
 #pragma unroll
           for (int r = 0; r < HSK; r += 2) {
             s0 = (r > i) ? fma(y[r], y[r], s0) : s0;
             s1 = (r + 1 > i) ? fma(y[r + 1], y[r + 1], s1) : s1;
           }
-          nrm = nref = s0 + s1;
+          nrm = s0 + s1;
         }
       }
     }
