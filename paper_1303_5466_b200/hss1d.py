@@ -100,6 +100,13 @@ class Hss1dBatch:
 
     # -- construction ------------------------------------------------------
     @staticmethod
+    def from_dense(Ad, n):
+        """The matrices kept as they are (a depth-0 tree: one dense block each)."""
+        H = Hss1dBatch(Ad.shape[0], n, [np.array([[0, n]], dtype=np.int64)], Ad.device)
+        H.dense = Ad[:, :n, :n].contiguous()
+        return H
+
+    @staticmethod
     def compress(Ad, n, eps, leaf_size=32, align=None, seed=0, max_items=32768):
         """Ad: (nb, ld, ld) device tensor, item b column-major (Ad[b, c, r] =
         A_b(r, c)), the leading n x n part is used.  `eps`: relative ID

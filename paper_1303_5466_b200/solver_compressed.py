@@ -12,9 +12,11 @@ device) and the factors are F^-1 and E = ([I T_up] F^-1 [I; T_dn^T])^-1 per
 box (_dense_factors / _dense_E_from_lu, solver_compressed.py:437-483), the
 root F = cross + diag(E1, E2) (solver_compressed.py:560-577).  The reference
 stores the blocks of boxes with more than k_cut skeleton points in 1-D HSS
-form (eps-accurate, O(N) memory); here every block stays dense in HBM, so
-results agree with the reference to its eps while the storage is the
-dense-block one.  ti_mode (translation-invariant kernels) keeps one factor
+form (eps-accurate, O(N) memory); here the blocks are formed dense on the
+device and, with SolverOptions(block_storage="hss1d"), compressed level by
+level into batched 1-D HSS forms for storage and the solve sweeps
+(compressed_store.py, hss1d.py); the default keeps them dense in HBM (fastest
+solve).  ti_mode (translation-invariant kernels) keeps one factor
 record per level after the factorization (share_level_records: the sweeps read
 it with batch stride 0), as the reference's TI mode does; every box is still
 factored.  Complex kernels run realified like the
@@ -156,9 +158,16 @@ def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti
     # 548-552) when every box is a translate of it: uniform levels, no support
     # mask; otherwise every box is factored and uniform levels share a record
     share = ti_mode and support_mask is None and _levels_uniform(tree)
+    if opts.block_storage not in ("dense", "hss1d"):
+        raise ConfigError(f"unknown block_storage {opts.block_storage!r}")
     H, inv.factors = factorize(spec, grid, tree, eps, opts, quad, apriori=layers, ti=share)
     if ti_mode and not share:
         share_level_records(inv.factors)
+    if opts.block_storage == "hss1d":
+        # boxes above k_cut keep F^-1 and E in 1-D HSS form (solver_compressed.py:
+        # 490-511 _compressed_factors); TI records and refined levels stay dense
+        from . import compressed_store
+        inv.hss_levels = compressed_store.compact(inv.factors)
     inv.dense_delegate = inv.factors
     inv.dense_matvec_source = H
     return inv

@@ -1021,6 +1021,15 @@ class DenseBlockInverse:
         L, j = self.H._lvl_of[i]
         m = int(L.m[j])
         jr = 0 if getattr(L, "ti", False) else j   # TI: the level's shared record
+        if getattr(L, "hss", None) is not None:    # densified from the HSS forms (small n)
+            hF, hE = L.hss
+            if which == "E":
+                return hE.to_dense()[j].t().cpu().numpy()
+            P = hF.to_dense()[j].t().cpu().numpy()          # [sk, rs] order
+            wp = L.perm_r[j, :m].cpu().numpy()
+            out = np.empty_like(P)
+            out[np.ix_(wp, wp)] = P
+            return out
         if which == "E":
             k = int(L.k[j])
             return L.E[jr, :k, :k].t().cpu().numpy()
@@ -1039,6 +1048,11 @@ class DenseBlockInverse:
         for L in _real_levels(H):
             m = L.m.astype(np.int64)
             k = L.k.astype(np.int64) if L.lv > 0 else None
+            if getattr(L, "hss", None) is not None:   # 1-D HSS blocks + the dense T
+                from . import compressed_store
+                tot += compressed_store.hss_bytes(L)
+                tot += int((k * (m - k)).sum()) * 8 * H.group
+                continue
             if getattr(L, "ti", False):  # one shared record per level
                 m = m[:1]
                 k = k[:1]
@@ -1168,7 +1182,7 @@ class _Prefetch:
         return out
 
 
-def invert_dense_block(H, spill=None, free_source=False):
+def invert_dense_block(H, spill=None, free_source=False, storage="dense"):
     """Fine-to-coarse telescoping inversion, one batch per level
     (solver_dense.py:332-368).  `free_source` drops D/B once consumed;
     `spill` (a _Spill, or a threshold in MB) moves each finished level's
@@ -1190,6 +1204,9 @@ def invert_dense_block(H, spill=None, free_source=False):
                     L.D = None
                 else:
                     L.B12 = L.B21 = None
+            if storage == "hss1d" and i > 0:   # the parent's F is assembled: compress the child
+                from . import compressed_store
+                compressed_store.compact_level(H, levels[i - 1])
             if sp is not None and i > 0:   # the child level is no longer needed here
                 sp.spill_level(levels[i - 1])
         if sp is not None and levels:
@@ -1623,6 +1640,10 @@ def _sweep_up_level(H, L, fd, phi, ups, fac=None):
         C = H.levels[L.lv + 1]
         _lib.gather_rows(ups[C.lv], 2 * C.kmax, C.nb * C.kmax, L.cat_idx, mm, U, mm, ldv,
                          L.m_d, mm, None, r, nb)
+    if getattr(L, "hss", None) is not None:   # 1-D HSS blocks (compressed_store.py)
+        from . import compressed_store
+        compressed_store.sweep_up_level(H, L, U, phi, ups, r)
+        return
     Phi = torch.zeros((r, ldv), dtype=_F64, device=dev)
     _apply_Finv(L, Finv, U, Phi, r, 0.0)
     if getattr(L, "refine", False):
@@ -1730,7 +1751,13 @@ def _sweep_down(H, phi, ups, out, pd_top=None):
         nb, mm = L.nb, L.mmax
         ldv = nb * mm
         Phi = phi[L.lv]
-        if L.lv > 0:
+        if getattr(L, "hss", None) is not None:
+            from . import compressed_store
+            par = H.levels[L.lv - 1]
+            PD = pd_top if par is None else _phi_dn(H, L, phi, r)
+            Phi = compressed_store.sweep_down_level(H, L, PD, phi, ups, r)
+            del PD
+        elif L.lv > 0:
             kk = L.kmax
             par = H.levels[L.lv - 1]
             PD = pd_top if par is None else _phi_dn(H, L, phi, r)
