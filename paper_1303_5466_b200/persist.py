@@ -333,6 +333,10 @@ def save(obj, path):
         kind, H = "Hss2dMatrix", obj
     else:
         raise TypeError(f"cannot save a {type(obj).__name__}")
+    if any(getattr(L, "hss", None) is not None for L in H.levels if L is not None):
+        raise NotImplementedError("saving 1-D HSS / lean block storage (block_storage='hss1d') "
+                                  "is not supported: save the dense factors and convert after "
+                                  "load (compressed_store.compact)")
     torch.cuda.synchronize(H.device)
     problem = _problem_of(H)
     if kind == "CompressedInverse":
