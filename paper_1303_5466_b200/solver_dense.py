@@ -1024,11 +1024,11 @@ class DenseBlockInverse:
         if getattr(L, "hss", None) is not None:    # densified from the HSS forms (small n)
             hF, hE = L.hss
             if which == "E":
-                return hE.to_dense()[j].t().cpu().numpy()
-            P = hF.to_dense()[j].t().cpu().numpy()          # [sk, rs] order
-            wp = L.perm_r[j, :m].cpu().numpy()
+                k = int(L.k[j])
+                return hE.to_dense()[j, :k, :k].t().cpu().numpy()
+            P = hF.to_dense()[j].t()[:m, :m].cpu().numpy()  # rows perm_c, columns perm_r
             out = np.empty_like(P)
-            out[np.ix_(wp, wp)] = P
+            out[np.ix_(L.perm_c[j, :m].cpu().numpy(), L.perm_r[j, :m].cpu().numpy())] = P
             return out
         if which == "E":
             k = int(L.k[j])
@@ -1186,7 +1186,14 @@ def invert_dense_block(H, spill=None, free_source=False, storage="dense"):
     """Fine-to-coarse telescoping inversion, one batch per level
     (solver_dense.py:332-368).  `free_source` drops D/B once consumed;
     `spill` (a _Spill, or a threshold in MB) moves each finished level's
-    factor batches above the threshold to pinned host memory."""
+    factor batches above the threshold to pinned host memory.  `storage`:
+    "dense" keeps F^-1, E, W = F^-1 L and C = E R per box (fastest solve);
+    "lean" keeps F^-1 and E only, as the reference does (F_lu, E, T:
+    solver_dense.py:284-291), and the sweeps apply T (compressed_store.py);
+    "hss1d" also stores large a-priori-path blocks in 1-D HSS form.  Either way
+    a level is converted as soon as its parent is factored."""
+    if storage not in ("dense", "lean", "hss1d"):
+        raise ConfigError(f"unknown storage {storage!r}")
     inv = DenseBlockInverse(H)
     sp = _as_spill(spill)
     _mark("invert:start")
@@ -1204,9 +1211,10 @@ def invert_dense_block(H, spill=None, free_source=False, storage="dense"):
                     L.D = None
                 else:
                     L.B12 = L.B21 = None
-            if storage == "hss1d" and i > 0:   # the parent's F is assembled: compress the child
+            if storage in ("hss1d", "lean") and i > 0:   # the parent's F is assembled
                 from . import compressed_store
-                compressed_store.compact_level(H, levels[i - 1])
+                compressed_store.compact_level(
+                    H, levels[i - 1], min_size=None if storage == "hss1d" else float("inf"))
             if sp is not None and i > 0:   # the child level is no longer needed here
                 sp.spill_level(levels[i - 1])
         if sp is not None and levels:

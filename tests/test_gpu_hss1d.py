@@ -210,3 +210,37 @@ def test_hss1d_storage_at_512():
     assert hss.nbytes() < 0.6 * nd
     xh = hss.apply(f)
     assert np.linalg.norm(xh - xd) <= 1e-8 * np.linalg.norm(xd)
+
+
+@pytest.mark.parametrize("n,leaf,b,c", [(64, 64, "gaussian_bump", "one"), (128, 64, "gaussian_bump", "gaussian_bump"),
+                                        (30, 64, "gaussian_bump", "one")])
+def test_lean_storage_on_the_id_path(n, leaf, b, c):
+    """invert_dense_block(storage="lean") on the pivoted-ID path (k_cut = None:
+    row / column skeletons in pivot order, ranks varying from box to box): the
+    reference's own factor set (F, E, T: solver_dense.py:284-291) -- same
+    solution as the dense storage, the reference layout's byte count."""
+    import paper_1303_5466_b200 as P
+    import paper_1303_5466_b200.solver_dense as sd
+    spec = P.KernelSpec("laplace2d", b_field=P.make_field(b), c_field=P.make_field(c))
+    grid = P.Grid(n)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=leaf, k_cut=None)
+    rng = np.random.default_rng(6)
+    F = rng.standard_normal((grid.n, 4))
+    f1 = rng.standard_normal(grid.n)
+    tree = P.build_tree(grid, leaf)
+    dense = sd.invert_dense_block(sd.compress_outer(spec, grid, tree, 1e-10, opts))
+    H = sd.compress_outer(spec, grid, tree, 1e-10, opts)
+    lean = sd.invert_dense_block(H, storage="lean")
+    kinds = [getattr(L, "hss_kind", None) for L in H.levels if L is not None and L.lv > 0]
+    assert all(kd == "lean" for kd in kinds), kinds
+    # (as allocated: boxes are padded to the largest of their level)
+    assert abs(lean.nbytes() - dense.nbytes_reference_layout()) <= 0.08 * lean.nbytes()
+    assert lean.nbytes() <= dense.nbytes()
+    for f in (f1, F):
+        xd, xl = dense.apply(f), lean.apply(f)
+        assert np.linalg.norm(xl - xd) <= 1e-11 * np.linalg.norm(xd)
+    v = rng.standard_normal(grid.n)
+    assert np.linalg.norm(v - H.matvec(lean.apply(v))) <= 1e-9 * np.linalg.norm(v)
+    i = int(H.tree.nodes[1].idx)
+    assert np.abs(lean.E[i] - dense.E[i]).max() <= 1e-12 * np.abs(dense.E[i]).max()
+    assert np.abs(lean.Finv[i] - dense.Finv[i]).max() <= 1e-12 * np.abs(dense.Finv[i]).max()
