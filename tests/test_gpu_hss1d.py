@@ -244,3 +244,32 @@ def test_lean_storage_on_the_id_path(n, leaf, b, c):
     i = int(H.tree.nodes[1].idx)
     assert np.abs(lean.E[i] - dense.E[i]).max() <= 1e-12 * np.abs(dense.E[i]).max()
     assert np.abs(lean.Finv[i] - dense.Finv[i]).max() <= 1e-12 * np.abs(dense.Finv[i]).max()
+
+
+@pytest.mark.parametrize("mode", ["hss", "lean"])
+def test_helmholtz_compressed_with_block_storage(mode):
+    """Complex kernel (realified on the device): the converted storage solves
+    like the dense one and meets the reference's residual bar
+    (test_solver_compressed.py:243-253: <= 1e-7); the skeleton stays a set of
+    grid points ((Re, Im) pairs stay adjacent in the [sk, rs] ordering)."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200 import compressed_store
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    spec = P.KernelSpec("helmholtz2d", k=4 * np.pi)
+    grid = P.Grid(36)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=81, k_cut=16)
+    dense = compress_inverse(spec, grid, eps=1e-10, opts=opts)
+    conv = compress_inverse(spec, grid, eps=1e-10, opts=opts)
+    if mode == "hss":
+        assert compressed_store.compact(conv.factors, force_hss=True) >= 2
+    else:
+        compressed_store.compact(conv.factors, min_size=float("inf"))
+        kinds = [getattr(L, "hss_kind", None) for L in conv.dense_matvec_source.levels if L is not None]
+        assert kinds.count("lean") >= 2
+    rng = np.random.default_rng(12)
+    f = rng.standard_normal(grid.n) + 1j * rng.standard_normal(grid.n)
+    xd, xc = dense.apply(f), conv.apply(f)
+    assert xc.dtype == np.complex128
+    assert np.linalg.norm(xc - xd) <= 1e-8 * np.linalg.norm(xd)
+    A = P.assemble_dense(spec, grid, P.PLAIN, np.arange(grid.n), np.arange(grid.n))
+    assert np.linalg.norm(A @ xc - f) / np.linalg.norm(f) <= 1e-7
