@@ -41,7 +41,8 @@ def _args():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", "--side", dest="n", type=int, default=1024)  # --side under torchrun
+    ap.add_argument("--n", "--side", dest="n", type=int, default=None,   # --side under torchrun
+                    help="grid side (default 1024: config c4; 512 when several ranks share a GPU)")
     ap.add_argument("--nrhs", type=int, default=256)
     ap.add_argument("--cpu-n", type=int, default=128, help="oracle sample grid side")
     ap.add_argument("--no-e2e", action="store_true")
@@ -251,7 +252,10 @@ def run_sharded(a):
     from paper_1303_5466_b200 import CELL, Grid, KernelSpec, SolverOptions, build_tree, make_field, _lib
     from paper_1303_5466_b200.distributed import ShardedInverse, TorchComm
     comm = TorchComm()
-    n, nrhs = a.n, a.nrhs
+    # ranks sharing a GPU (no multi-GPU box): a functional check, not a scaling number --
+    # the 1024^2 factors of all ranks plus each process's pools do not fit one GPU
+    shared = ndev < world
+    n, nrhs = (a.n or (512 if shared else 1024)), a.nrhs
     N = n * n
     spec = KernelSpec("laplace2d", b_field=make_field("centre_bump", scale=math.pi / 2),
                       c_field=make_field("one"))
@@ -321,7 +325,9 @@ def run_sharded(a):
            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": dict(_config(n, nrhs, world), parallelism=f"subtree shards x{world} + "
-                          f"top boxes as a reduction tree ({backend} send/recv)"),
+                          f"top boxes as a reduction tree ({backend} send/recv)"
+                          + (f"; {world} ranks share {ndev} GPU(s): functional check at a size "
+                             f"that fits, not a scaling measurement" if shared else "")),
            "factor_s": tf / 1e3, "solve_s": ts / 1e3, "factor_bytes_rank": local_bytes,
            "roofline": roof, "gpu_launches": int(launches), "clocks": clk.summary(),
            "backend": backend, "devices": ndev}
@@ -614,6 +620,8 @@ if __name__ == "__main__":
     args = _args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(_spawn(args))
+    if int(os.environ.get("WORLD_SIZE", 1)) == 1 or args.impl == "reference":
+        args.n = args.n or 1024
     if args.impl == "reference":
         run_reference(args)
     else:
