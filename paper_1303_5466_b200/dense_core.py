@@ -126,13 +126,18 @@ def interp_decomp(A, eps, min_rank=0, max_rank=None, eps_abs=None, force_blocked
     |R_jj| <= eps |R_00| (residual form on the blocked path), then the
     min_rank / max_rank clamps; T = R11^{-1} R12.  Complex A runs realified
     with pairwise pivoting (each complex column is a pair of real columns), so
-    the skeleton is a set of complex columns and T the complex interpolation."""
+    the skeleton is a set of complex columns and T the complex interpolation.
+    `eps_abs` (dense_core.py:86-88): absolute floor of the rank threshold."""
     A = np.asarray(A)
     m, n = A.shape
     if n == 0 or m == 0:
         return IdFactor(np.zeros(0, np.int64), np.zeros((0, n), A.dtype), np.arange(n), 0.0)
     if eps_abs:
-        raise NotImplementedError("eps_abs (O(N)-path option) is not supported")
+        # |R_jj| <= max(eps |R_00|, eps_abs) with |R_00| = the largest column norm
+        # (the first pivot): one relative threshold for the device kernel
+        r00 = float(np.sqrt((np.abs(A) ** 2).sum(axis=0).max()))
+        if r00 > 0.0:
+            eps = max(float(eps), min(float(eps_abs) / r00, 1.0))
     if np.iscomplexobj(A):
         perm2, k2, T2 = _id_real(_realify_cols(A), eps, min_rank, max_rank, force_blocked, True)
         k = k2 // 2

@@ -204,3 +204,28 @@ def test_leaf_qrcp_matches_lapack():
             same += int(np.intersect1d(perm[:k], ref.perm[:ref.k]).size)
             tot += ref.k
     assert same >= 0.95 * tot, (same, tot)
+
+
+@pytest.mark.parametrize("blocked", [False, True])
+def test_eps_abs_floor(blocked):
+    """interp_decomp's absolute floor (dense_core.py:82-88): the rank is the
+    first j with |R_jj| <= max(eps |R_00|, eps_abs); a floor above |R_00| gives
+    rank 0 (then min_rank clamps)."""
+    import scipy.linalg as sla
+    from paper_1303_5466_b200.dense_core import interp_decomp
+    rng = np.random.default_rng(21)
+    m, n = 90, 70
+    sv = 10.0 ** -np.linspace(0, 12, n)
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    A = (u * sv) @ v.T
+    _, r, _ = sla.qr(A, mode="economic", pivoting=True)
+    d = np.abs(np.diag(r))
+    for eps_abs in (1e-4, 3e-7):
+        cut = max(1e-12 * d[0], eps_abs)
+        k_ref = int(np.argmax(d <= cut))
+        f = interp_decomp(A, 1e-12, eps_abs=eps_abs, force_blocked=blocked)
+        assert abs(f.rank - k_ref) <= 2, (f.rank, k_ref)
+        assert np.linalg.norm(A - reconstruct(A, f), 2) <= 100 * eps_abs
+    assert interp_decomp(A, 1e-12, eps_abs=10.0 * d[0], force_blocked=blocked).rank == 0
+    assert interp_decomp(A, 1e-12, eps_abs=10.0 * d[0], min_rank=3, force_blocked=blocked).rank == 3
