@@ -88,6 +88,9 @@ int vief_gen_idmat(const vief_problem* P, int kind,
                    const int* src_xy, const int* src_g, long long sSrc, const int* p, int maxp,
                    double* out, long long sOut, int ldo, int batch, void* stream);
 
+/* Batches: every batched entry point accepts any item count; more than 65535
+ * items (one CUDA grid dimension) run as consecutive chunks on the stream. */
+
 /* ---- dense FP64 building blocks (DMMA mma.sync.m8n8k4.f64) -------------- */
 typedef struct {
   const double* A; const double* B; double* C;

@@ -10,6 +10,8 @@
 #define VF_EARG 2
 #define VF_ESINGULAR 3
 #define VF_ENOMEM 4
+// items of one batched launch (a CUDA grid's y / z extent); larger batches run in chunks
+#define VF_MAXB 65535
 
 namespace vf {
 

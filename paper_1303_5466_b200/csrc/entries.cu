@@ -314,6 +314,14 @@ extern "C" int vief_gen_block(const vief_problem* P, const int* I, long long sI,
                               double* out, long long sOut, double* const* outp, int ldo,
                               int batch, void* stream) {
   if (batch <= 0 || maxI <= 0 || maxJ <= 0) return VF_OK;
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_gen_block(P, I + (long long)b0 * sI, sI, nI ? nI + b0 : nullptr, maxI, J + (long long)b0 * sJ, sJ, nJ ? nJ + b0 : nullptr, maxJ, out ? out + (long long)b0 * sOut : nullptr, sOut, outp ? outp + b0 : nullptr, ldo, nbk, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   dim3 grid(cdiv(maxI, 128), cdiv(maxJ, 8), batch);
   if (!(P->is_complex && P->realify)) grid.y = cdiv(maxJ, KC);
   if (grid.y > 65535 || batch > 65535) { set_error("gen_block: grid too large"); return VF_EARG; }
@@ -333,6 +341,14 @@ extern "C" int vief_gen_idmat(const vief_problem* P, int kind, const int* pts, l
                               long long sSrc, const int* p, int maxp, double* out, long long sOut,
                               int ldo, int batch, void* stream) {
   if (batch <= 0 || maxm <= 0 || maxp <= 0) return VF_OK;
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_gen_idmat(P, kind, pts + (long long)b0 * sPts, sPts, m ? m + b0 : nullptr, maxm, src_xy + 2 * (long long)b0 * sSrc, src_g + (long long)b0 * sSrc, sSrc, p ? p + b0 : nullptr, maxp, out + (long long)b0 * sOut, sOut, ldo, nbk, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   dim3 grid(cdiv((P->is_complex && P->realify) ? 2 * maxp : maxp, 128), cdiv(maxm, 8), batch);
   if (!(P->is_complex && P->realify)) grid.y = cdiv(maxm, KC);
   if (grid.y > 65535 || batch > 65535) { set_error("gen_idmat: grid too large"); return VF_EARG; }
@@ -351,6 +367,14 @@ extern "C" int vief_box_sources(const int* rects, int batch, int pad, int n_side
                                 int* src_g, long long sSrc, int* p_out, void* stream) {
   if (batch <= 0) return VF_OK;
   if (pad < 1 || pad > 8) { set_error("box_sources: pad %d out of range", pad); return VF_EARG; }
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_box_sources(rects + 4 * (long long)b0, nbk, pad, n_side, src_xy + 2 * (long long)b0 * sSrc, src_g + (long long)b0 * sSrc, sSrc, p_out + b0, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   dim3 grid(cdiv(sSrc, 256), batch);
   k_box_sources<<<grid, 256, 0, (cudaStream_t)stream>>>(rects, batch, pad, n_side, src_xy, src_g, sSrc, p_out);
   ++g_launches;

@@ -486,9 +486,32 @@ __global__ void __launch_bounds__(256) k_dgemv_t(vief_gemm_desc d) {
 
 using namespace vf;
 
+// d restricted to items [b0, b0 + nbk)
+static vief_gemm_desc gemm_chunk(const vief_gemm_desc* d, int b0, int nbk) {
+  vief_gemm_desc c = *d;
+  if (c.A) c.A += (long long)b0 * c.strideA;
+  if (c.B) c.B += (long long)b0 * c.strideB;
+  if (c.C) c.C += (long long)b0 * c.strideC;
+  if (c.Aptr) c.Aptr += b0;
+  if (c.Bptr) c.Bptr += b0;
+  if (c.Cptr) c.Cptr += b0;
+  if (c.Mb) c.Mb += b0;
+  if (c.Nb) c.Nb += b0;
+  if (c.Kb) c.Kb += b0;
+  c.batch = nbk;
+  return c;
+}
+
 extern "C" int vief_dgemm_batched(const vief_gemm_desc* d, void* stream) {
   if (!d || d->batch <= 0 || d->M <= 0 || d->N <= 0) return VF_OK;
-  if (d->batch > 65535) { set_error("dgemm: batch %d > 65535", d->batch); return VF_EARG; }
+  if (d->batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < d->batch; b0 += VF_MAXB) {
+      const vief_gemm_desc c = gemm_chunk(d, b0, std::min(VF_MAXB, d->batch - b0));
+      const int rc = vief_dgemm_batched(&c, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   // skinny M: 32 x 128 tiles (no idle DMMA rows); otherwise 64 x 64
   const int rc = d->M <= 32 ? dispatch_gemm<32, 128>(d, st) : dispatch_gemm<64, 64>(d, st);
@@ -503,7 +526,14 @@ constexpr int GV_TARGET_CTAS = 8 * 148;
 
 extern "C" int vief_dgemv_batched(const vief_gemm_desc* d, void* stream) {
   if (!d || d->batch <= 0 || d->M <= 0) return VF_OK;
-  if (d->batch > 65535) { set_error("dgemv: batch %d > 65535", d->batch); return VF_EARG; }
+  if (d->batch > VF_MAXB) {
+    for (int b0 = 0; b0 < d->batch; b0 += VF_MAXB) {
+      const vief_gemm_desc c = gemm_chunk(d, b0, std::min(VF_MAXB, d->batch - b0));
+      const int rc = vief_dgemv_batched(&c, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   if (!d->transA) {
     const int tiles = (int)cdiv(d->M, GV_ROWS) * d->batch;
     // K split (cluster size) so that ~4 CTAs per SM stream concurrently; each

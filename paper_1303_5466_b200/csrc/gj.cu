@@ -278,7 +278,15 @@ using namespace vf;
 extern "C" int vief_inv_batched(double* A, long long sA, int lda, int n, int batch,
                                 double* pivmin, double* pivmax, void* stream_) {
   if (batch <= 0 || n <= 0) return VF_OK;
-  if (batch > 65535) { set_error("inv_batched: batch too large"); return VF_EARG; }
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_inv_batched(A + (long long)b0 * sA, sA, lda, n, nbk, pivmin + b0,
+                                      pivmax + b0, stream_);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   cudaStream_t st = (cudaStream_t)stream_;
   ensure_pool();
   // measured: for n <= 64 (5 CTAs/SM) the register kernel beats the blocked path ~2x;

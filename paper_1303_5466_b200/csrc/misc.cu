@@ -198,6 +198,14 @@ extern "C" int vief_gather_rows(const double* src, long long sSrc, int lds, cons
                                 const int* nrow, int maxrow, const int* ncol, int maxcol,
                                 int batch, int accumulate, void* stream) {
   if (batch <= 0 || maxrow <= 0 || maxcol <= 0) return VF_OK;
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_gather_rows(src + (long long)b0 * sSrc, sSrc, lds, idx + (long long)b0 * sIdx, sIdx, dst + (long long)b0 * sDst, sDst, ldd, nrow ? nrow + b0 : nullptr, maxrow, ncol ? ncol + b0 : nullptr, maxcol, nbk, accumulate, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   k_gather_rows<<<grid2(maxrow, maxcol, batch), dim3(32, 8), 0, (cudaStream_t)stream>>>(
       src, sSrc, lds, idx, sIdx, dst, sDst, ldd, nrow, maxrow, ncol, maxcol, accumulate);
   ++g_launches;
@@ -210,6 +218,14 @@ extern "C" int vief_scatter_cols(const double* src, long long sSrc, int lds, con
                                  const int* nrow, int maxrow, const int* ncol, int maxcol,
                                  int batch, void* stream) {
   if (batch <= 0 || maxrow <= 0 || maxcol <= 0) return VF_OK;
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_scatter_cols(src + (long long)b0 * sSrc, sSrc, lds, idx + (long long)b0 * sIdx, sIdx, dst + (long long)b0 * sDst, sDst, ldd, nrow ? nrow + b0 : nullptr, maxrow, ncol ? ncol + b0 : nullptr, maxcol, nbk, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   k_scatter_cols<<<grid2(maxrow, maxcol, batch), dim3(32, 8), 0, (cudaStream_t)stream>>>(
       src, sSrc, lds, idx, sIdx, dst, sDst, ldd, nrow, maxrow, ncol, maxcol);
   ++g_launches;
@@ -222,6 +238,14 @@ extern "C" int vief_gather_cols(const double* src, long long sSrc, int lds, cons
                                 const int* nrow, int maxrow, const int* ncol, int maxcol,
                                 int batch, void* stream) {
   if (batch <= 0 || maxrow <= 0 || maxcol <= 0) return VF_OK;
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_gather_cols(src + (long long)b0 * sSrc, sSrc, lds, idx + (long long)b0 * sIdx, sIdx, dst + (long long)b0 * sDst, sDst, ldd, nrow ? nrow + b0 : nullptr, maxrow, ncol ? ncol + b0 : nullptr, maxcol, nbk, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   k_gather_cols<<<grid2(maxrow, maxcol, batch), dim3(32, 8), 0, (cudaStream_t)stream>>>(
       src, sSrc, lds, idx, sIdx, dst, sDst, ldd, nrow, maxrow, ncol, maxcol);
   ++g_launches;
@@ -234,6 +258,14 @@ extern "C" int vief_scatter_rows(const double* src, long long sSrc, int lds, con
                                  const int* nrow, int maxrow, const int* ncol, int maxcol,
                                  int batch, void* stream) {
   if (batch <= 0 || maxrow <= 0 || maxcol <= 0) return VF_OK;
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_scatter_rows(src + (long long)b0 * sSrc, sSrc, lds, idx + (long long)b0 * sIdx, sIdx, dst + (long long)b0 * sDst, sDst, ldd, nrow ? nrow + b0 : nullptr, maxrow, ncol ? ncol + b0 : nullptr, maxcol, nbk, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   k_scatter_rows<<<grid2(maxrow, maxcol, batch), dim3(32, 8), 0, (cudaStream_t)stream>>>(
       src, sSrc, lds, idx, sIdx, dst, sDst, ldd, nrow, maxrow, ncol, maxcol);
   ++g_launches;
@@ -245,6 +277,14 @@ extern "C" int vief_gather_int(const int* src, long long sSrc, const int* idx, l
                                int* out, long long sOut, const int* n, int maxn, int batch,
                                void* stream) {
   if (batch <= 0 || maxn <= 0) return VF_OK;
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_gather_int(src + (long long)b0 * sSrc, sSrc, idx + (long long)b0 * sIdx, sIdx, out + (long long)b0 * sOut, sOut, n ? n + b0 : nullptr, maxn, nbk, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   k_gather_int<<<dim3(cdiv(maxn, 128), batch), 128, 0, (cudaStream_t)stream>>>(
       src, sSrc, idx, sIdx, out, sOut, n, maxn);
   ++g_launches;
@@ -257,6 +297,14 @@ extern "C" int vief_copy2d(const double* src, long long sSrc, const double* cons
                            const int* rows, int maxrows, const int* cols, int maxcols, int batch,
                            void* stream) {
   if (batch <= 0 || maxrows <= 0 || maxcols <= 0) return VF_OK;
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_copy2d(src ? src + (long long)b0 * sSrc : nullptr, sSrc, srcp ? srcp + b0 : nullptr, lds, dst ? dst + (long long)b0 * sDst : nullptr, sDst, dstp ? dstp + b0 : nullptr, ldd, rows ? rows + b0 : nullptr, maxrows, cols ? cols + b0 : nullptr, maxcols, nbk, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   dim3 g = grid2(maxrows, maxcols, batch);
   if (g.y > 4096) g.y = 4096;
   k_copy2d<<<g, dim3(32, 8), 0, (cudaStream_t)stream>>>(src, sSrc, srcp, lds, dst, sDst, dstp,
@@ -269,6 +317,14 @@ extern "C" int vief_copy2d(const double* src, long long sSrc, const double* cons
 extern "C" int vief_pad_identity(double* A, long long sA, int lda, const int* nb, int n, int batch,
                                  void* stream) {
   if (batch <= 0 || n <= 0) return VF_OK;
+  if (batch > VF_MAXB) {  // one grid dimension carries the items: run in chunks
+    for (int b0 = 0; b0 < batch; b0 += VF_MAXB) {
+      const int nbk = batch - b0 < VF_MAXB ? batch - b0 : VF_MAXB;
+      const int rc = vief_pad_identity(A + (long long)b0 * sA, sA, lda, nb ? nb + b0 : nullptr, n, nbk, stream);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   k_pad_identity<<<grid2(n, n, batch), dim3(32, 8), 0, (cudaStream_t)stream>>>(A, sA, lda, nb, n);
   ++g_launches;
   VF_LAUNCH_CHECK("k_pad_identity");

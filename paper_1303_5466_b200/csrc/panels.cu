@@ -1150,6 +1150,12 @@ int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* a
   if (rows_per < PNB) rows_per = PNB;
   rows_per = (rows_per + 1) & ~1;
   size_t smem = (size_t)rows_per * PNB * sizeof(double) + sizeof(XGram);
+  if (smem > 190 * 1024) {  // beyond 16 CTAs' registers (12288 rows) and shared memory
+    set_error("qr_panel: a panel of %d rows exceeds one cluster's capacity (12288 rows); boxes "
+              "this large (the top levels of a 2048^2 grid) need a two-stage (TSQR) panel, "
+              "which is not built", rows);
+    return VF_EARG;
+  }
   void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
                   (void*)&J, (void*)&rows_per, (void*)&Vw, (void*)&sV, (void*)&ldv, (void*)&Tt,
                   (void*)&Rt};

@@ -977,8 +977,22 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
   ensure_pool();
   const int count = d->count;
   if (count <= 0) return VF_OK;
-  if (count > 65535) { set_error("id: count > 65535"); return VF_EARG; }
   if (d->group < 1 || count % d->group) { set_error("id: bad group"); return VF_EARG; }
+  if (count > VF_MAXB) {  // one grid dimension carries the items: whole groups per chunk
+    const int per = (VF_MAXB / d->group) * d->group;
+    for (int b0 = 0; b0 < count; b0 += per) {
+      vief_id_desc c = *d;
+      c.A += (long long)b0 * d->sA;
+      c.p += b0; c.m += b0; c.rank += b0;
+      c.perm += (long long)b0 * d->maxm;
+      c.T += (long long)b0 * d->sT;
+      if (c.kfix) c.kfix += b0;
+      c.count = std::min(per, count - b0);
+      const int rc = vief_id_batched(&c, stream_);
+      if (rc) return rc;
+    }
+    return VF_OK;
+  }
   if (d->ldT < d->maxm) { set_error("id: ldT must be >= maxm"); return VF_EARG; }
   if (d->couple && (count != 1 || d->kfix)) {
     set_error("id: cross-process coupling needs count = 1 and no kfix");

@@ -70,9 +70,6 @@ def _mark(tag):
         TIMER.mark(tag)
 
 
-_MAX_BATCH = 65535   # items of one batched library call (CUDA grid.y / grid.z extent)
-
-
 def _even(x):
     return int(x) + (int(x) & 1)
 
@@ -204,11 +201,6 @@ class Hss2dMatrix:
             L = _Level(lv, tree.ids[lv][sl[0]:sl[1]], tree.rects[lv][sl[0]:sl[1]],
                        lv == tree.depth)
             L.sl = sl
-            if L.nb * self.group > _MAX_BATCH:   # a batched call's items are one grid dimension
-                raise ConfigError(
-                    f"level {lv} has {L.nb} boxes: one process factors at most "
-                    f"{_MAX_BATCH // self.group} boxes per level (1024^2 with leaf 64 uses "
-                    f"16384); shard the tree over ranks (distributed.ShardedInverse)")
             self.levels.append(L)
         self.sharded = level_slices is not None
         self._lvl_of_cache = None
