@@ -1145,17 +1145,13 @@ int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* a
                    : rpt == 2 ? (const void*)k_qr_panel_rr<2> : (const void*)k_qr_panel_rr<3>;
     return launch_cluster(fn, count, cs, 0, st, args);
   }
+  // taller than one cluster holds (16 CTAs x 256 threads x 3 rows): two-stage panel
+  return qr_panel_tall(A, sA, lda, pv, active, bsv, J, maxp, count, Vw, sV, ldv, Tt, Rt, st);
   int cs = pick_cs(rows, 640, count);
   int rows_per = (rows + cs - 1) / cs;
   if (rows_per < PNB) rows_per = PNB;
   rows_per = (rows_per + 1) & ~1;
   size_t smem = (size_t)rows_per * PNB * sizeof(double) + sizeof(XGram);
-  if (smem > 190 * 1024) {  // beyond 16 CTAs' registers (12288 rows) and shared memory
-    set_error("qr_panel: a panel of %d rows exceeds one cluster's capacity (12288 rows); boxes "
-              "this large (the top levels of a 2048^2 grid) need a two-stage (TSQR) panel, "
-              "which is not built", rows);
-    return VF_EARG;
-  }
   void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
                   (void*)&J, (void*)&rows_per, (void*)&Vw, (void*)&sV, (void*)&ldv, (void*)&Tt,
                   (void*)&Rt};

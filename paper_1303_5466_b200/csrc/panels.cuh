@@ -16,6 +16,11 @@ int lu_panel(const double* A, long long sA, int lda, int n, int c0, int nbs, int
 int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* active,
              const int* bsv, int J, int maxp, int count, double* Vw, long long sV, int ldv,
              double* Tt, double* Rt, cudaStream_t st);
+// the same for panels taller than one cluster holds (two-stage TSQR +
+// Householder reconstruction, tallpanel.cu); qr_panel dispatches to it
+int qr_panel_tall(const double* A, long long sA, int lda, const int* pv, const int* active,
+                  const int* bsv, int J, int maxp, int count, double* Vw, long long sV, int ldv,
+                  double* Tt, double* Rt, cudaStream_t st);
 // perm (count x ldperm, or null): pair mode -- pivot 2s+1 is the column whose
 // perm id is (perm id of pivot 2s) ^ 1 (realified complex unknowns)
 int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const int* active,

@@ -112,6 +112,39 @@ def test_blocked_id_on_kernel_rows_vs_oracle(shape):
     assert len(set(perm.tolist())) == m
 
 
+def test_blocked_id_tall_panel_two_stage():
+    """Panels taller than one cluster holds (> 12288 rows; the level-1 boxes of
+    a 2048^2 grid have 16416) go through the two-stage panel (TSQR of two row
+    chunks + Householder reconstruction, csrc/tallpanel.cu).  Ragged batch:
+    the second matrix is shorter, so its second chunk is shorter too; the
+    third fits one cluster after the first blocks' rows are finished.  Same
+    contract as the one-stage path: rank within a few of LAPACK's ID
+    (oracle.column_id), reconstruction at the tolerance, perm a permutation."""
+    import oracle.hssd as O
+    from paper_1303_5466_b200.dense_core import interp_decomp_batched
+    rng = np.random.default_rng(11)
+    eps = 1e-10
+    mats = []
+    for p, m in [(16416, 144), (13001, 120), (12310, 96)]:
+        src = rng.uniform(-1, 1, (m, 2)) * 0.5
+        th = np.linspace(0, 2 * np.pi, p, endpoint=False)
+        tgt = np.column_stack([1.3 * np.cos(th), 1.3 * np.sin(th)]) + rng.normal(0, 0.05, (p, 2))
+        r = np.hypot(*(tgt[:, None, :] - src[None, :, :]).transpose(2, 0, 1))
+        mats.append(np.log(r))
+    res = interp_decomp_batched(mats, eps, force_blocked=True)
+    for A, (perm, k, T) in zip(mats, res):
+        m = A.shape[1]
+        ref = O.column_id(A, eps)
+        R = np.zeros((k, m))
+        R[np.arange(k), perm[:k]] = 1.0
+        R[:, perm[k:]] = T
+        err = np.linalg.norm(A - A[:, perm[:k]] @ R) / np.linalg.norm(A)
+        assert abs(k - ref.k) <= max(3, ref.k // 20), (k, ref.k)
+        assert err <= 50 * eps, err
+        assert len(set(perm.tolist())) == m
+        assert np.abs(T).max() <= 10.0
+
+
 def test_fixed_rank_is_least_squares():
     """vief_id_batched with kfix: no pivoting, rank = kfix, T = lstsq(A[:, :k],
     A[:, k:]) (the compressed path's interpolation).  Ragged batch: k off the
