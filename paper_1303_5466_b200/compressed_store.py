@@ -79,7 +79,10 @@ def compact_level(H, L, eps=None, leaf_size=None, min_size=None, force_hss=False
     pc = pr if L.perm_c is L.perm_r else torch.where(live, L.perm_c.long()[:, :n], jj)
     bidx = torch.arange(nb, device=dev)[:, None, None]
     Fp = L.Finv[bidx, pr[:, :, None], pc[:, None, :]]     # F^-1(perm_c[r'], perm_r[c'])
+    big = L.Finv.numel() * 8 > (1 << 30)
     L.Finv = L.C = L.W = None
+    if big:   # the HSS compression's workspace comes from the library's pool, not torch's cache
+        torch.cuda.empty_cache()
     kind = "lean"
     hF = hE = None
     k0 = int(k[0])

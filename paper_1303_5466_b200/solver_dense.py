@@ -1182,7 +1182,7 @@ class _Prefetch:
         return out
 
 
-def invert_dense_block(H, spill=None, free_source=False, storage="dense"):
+def invert_dense_block(H, spill=None, free_source=False, storage="dense", compress=False):
     """Fine-to-coarse telescoping inversion, one batch per level
     (solver_dense.py:332-368).  `free_source` drops D/B once consumed;
     `spill` (a _Spill, or a threshold in MB) moves each finished level's
@@ -1191,7 +1191,12 @@ def invert_dense_block(H, spill=None, free_source=False, storage="dense"):
     "lean" keeps F^-1 and E only, as the reference does (F_lu, E, T:
     solver_dense.py:284-291), and the sweeps apply T (compressed_store.py);
     "hss1d" also stores large a-priori-path blocks in 1-D HSS form.  Either way
-    a level is converted as soon as its parent is factored."""
+    a level is converted as soon as its parent is factored.  `compress`: H's
+    levels are compressed here, each just before it is inverted (a level's
+    compression needs its children's skeleton lists only), so that with
+    `free_source` one level's D / B / ID matrices are resident at a time
+    instead of the whole tree's -- the low-memory schedule for the largest
+    grids (compress_outer + invert_dense_block hold all levels' sources)."""
     if storage not in ("dense", "lean", "hss1d"):
         raise ConfigError(f"unknown storage {storage!r}")
     inv = DenseBlockInverse(H)
@@ -1199,8 +1204,14 @@ def invert_dense_block(H, spill=None, free_source=False, storage="dense"):
     _mark("invert:start")
     with _host_quiet():
         levels = list(reversed(_real_levels(H)))
+        pad = H.opts.resolved_proxy_layers(H.spec)
         for i, L in enumerate(levels):
             _lib.prof_prefix(f"L{L.lv:02d}.")
+            if compress and getattr(L, "m", None) is None:
+                _lib.release_memory()   # cached blocks back to the driver: torch's
+                # allocator and the library's stream-ordered pool share the HBM
+                _compress_level(H, L, pad, H.opts.seed)
+                _mark(f"compress:{L.lv}")
             _invert_level(inv, L)
             _mark(f"invert:{L.lv}")
             if free_source:  # a level whose box solves are refined keeps its F blocks
@@ -1213,6 +1224,8 @@ def invert_dense_block(H, spill=None, free_source=False, storage="dense"):
                     L.B12 = L.B21 = None
             if storage in ("hss1d", "lean") and i > 0:   # the parent's F is assembled
                 from . import compressed_store
+                if compress:
+                    _lib.release_memory()
                 compressed_store.compact_level(
                     H, levels[i - 1], min_size=None if storage == "hss1d" else float("inf"))
             if sp is not None and i > 0:   # the child level is no longer needed here

@@ -181,17 +181,39 @@ def test_sequential_inversion_compacts_level_by_level():
     P, spec, grid, opts = _problem(128, 64)
     f = np.random.default_rng(8).standard_normal(grid.n)
     sols = []
-    for storage in ("dense", "hss1d"):
+    for storage, on_demand in (("dense", False), ("hss1d", False), ("hss1d", True)):
         tree = build_tree(grid, 64)
         layers = ensure_apriori_skeletons(spec, tree, opts)
         H = sd.Hss2dMatrix(spec, grid, tree, 1e-10, opts, P.PLAIN)
         H.apriori = layers
-        sd.compress_levels(H)
-        inv = sd.invert_dense_block(H, storage=storage)
+        if on_demand:   # each level compressed just before its inversion, sources freed after
+            inv = sd.invert_dense_block(H, storage=storage, compress=True, free_source=True)
+            assert all(getattr(L, "D", None) is None and getattr(L, "B12", None) is None
+                       for L in H.levels if L is not None and not getattr(L, "refine", False))
+        else:
+            sd.compress_levels(H)
+            inv = sd.invert_dense_block(H, storage=storage)
         if storage == "hss1d":
             assert sum(getattr(L, "hss", None) is not None for L in H.levels) >= 1
         sols.append(inv.apply(f))
     assert np.linalg.norm(sols[1] - sols[0]) <= 1e-8 * np.linalg.norm(sols[0])
+    assert np.array_equal(sols[2], sols[1])   # same arithmetic, a different schedule
+
+
+def test_on_demand_compression_on_the_id_path():
+    """invert_dense_block(compress=True) on the pivoted-ID path (k_cut = None):
+    bitwise the solution of compress_outer + invert_dense_block."""
+    import paper_1303_5466_b200 as P
+    import paper_1303_5466_b200.solver_dense as sd
+    spec = P.KernelSpec("laplace2d", b_field=P.make_field("gaussian_bump"), c_field=P.make_field("one"))
+    grid = P.Grid(128)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=None)
+    tree = P.build_tree(grid, 64)
+    f = np.random.default_rng(3).standard_normal(grid.n)
+    x0 = sd.invert_dense_block(sd.compress_outer(spec, grid, tree, 1e-10, opts)).apply(f)
+    H = sd.Hss2dMatrix(spec, grid, tree, 1e-10, opts, P.PLAIN)
+    x1 = sd.invert_dense_block(H, compress=True, free_source=True, storage="lean").apply(f)
+    assert np.linalg.norm(x1 - x0) <= 1e-11 * np.linalg.norm(x0)
 
 
 def test_hss1d_storage_at_512():
