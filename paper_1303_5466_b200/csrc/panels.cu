@@ -1165,11 +1165,22 @@ int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* a
 // (the others no longer wait for an i-term orthogonalisation); each thread
 // then reflects its own column (thread per column: cols_per <= PT) and
 // downdates its residual norm by the new R(i, c)^2.
-template <int NT>  // threads = columns per CTA slot (cols_per <= NT); <= 128 registers
+//
+// TOURN (more than 16 x 512 live columns: the level-1 boxes of a 2048^2 grid
+// have ~12272): tournament pivoting over column ranges.  Stage 1 (`cand`):
+// the same selection restricted to columns [coff, coff + nlim) of the live
+// part, its picks written to the item's candidate list instead of a swap
+// record.  Final stage (`cmap`): the selection over the gathered candidate
+// columns (k_cand_gather), picks mapped back to live-column indices before
+// the swap record is emitted.
+constexpr int TPARTS = 4;  // column ranges of a tournament (final stage: TPARTS * PNB <= 128 columns)
+template <int NT, bool TOURN = false>  // threads = columns per CTA slot (cols_per <= NT); <= 128 registers
 __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) k_select_hh(const double* Yg, int ldy, long long sY,
                                                   const int* mv, const int* active, const int* bsv,
                                                   int J, int cols_per, int* swaps,
-                                                  const int* perm, int ldperm) {
+                                                  const int* perm, int ldperm, int coff = 0,
+                                                  int nlim = 0, int* cand = nullptr, int slot = 0,
+                                                  const int* cmap = nullptr) {
   cg::cluster_group cl = cg::this_cluster();
   const int cs = cl.num_blocks(), cr = cl.block_rank();
   const int b = blockIdx.x / cs;
@@ -1178,8 +1189,10 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) k_select_hh(cons
     if (cr == 0 && tid == 0) swaps[(long long)b * SWL] = 0;
     return;
   }
-  const int bs = bsv[b];
-  const int n = mv[b] - J;
+  const int n = TOURN ? min(max(mv[b] - J - coff, 0), nlim) : mv[b] - J;
+  const int bs = TOURN ? min(bsv[b], n) : bsv[b];  // picks of this stage
+  if (TOURN && cand && cr == 0 && tid == 0) cand[(long long)b * (TPARTS * (PNB + 1)) + slot] = bs;
+  if (TOURN && bs <= 0) return;  // an empty column range (uniform for the cluster)
   __shared__ XSel xch[2];
   __shared__ double hv[HSK];
   constexpr int NWt = NT / 32;
@@ -1194,7 +1207,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) k_select_hh(cons
   double y[HSK];
   double nrm = -1.0;
   {
-    const double* Y = Yg + b * sY + (long long)(J + c0 + (own ? tid : 0)) * ldy;
+    const double* Y = Yg + b * sY + (long long)(J + (TOURN ? coff : 0) + c0 + (own ? tid : 0)) * ldy;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
     for (int r = 0; r < HSK; r += 4) {
@@ -1298,8 +1311,99 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) k_select_hh(cons
   }
   csync(cl);
   if (cr != 0 || warp != 0) return;
+  if (TOURN && cand) {  // stage 1: this range's picks, as live-column indices
+    int* out = cand + (long long)b * (TPARTS * (PNB + 1)) + TPARTS + slot * PNB;
+    if (lane < bs) out[lane] = coff + sel[lane];
+    return;
+  }
+  if (TOURN && cmap) {  // final stage: candidate slot -> live-column index
+    const int id = lane < bs ? cmap[(long long)b * (TPARTS * PNB) + sel[lane]] : 0;
+    __syncwarp();
+    if (lane < bs) sel[lane] = id;
+    __syncwarp();
+  }
   __shared__ int mid[NM], mpos[NM];
-  emit_swaps(sel, bs, J, b, swaps, lane, mid, mpos);
+  emit_swaps(sel, TOURN ? bsv[b] : bs, J, b, swaps, lane, mid, mpos);
+}
+
+// Candidate columns of a tournament, compacted: Yc_b(:, t) = Y_b(:, J + id_t),
+// cmap_b[t] = id_t over the ranges' picks in range order; nc[b] = their count.
+__global__ void __launch_bounds__(128) k_cand_gather(const double* Yg, int ldy, long long sY,
+                                                     const int* active, const int* bsv, int J,
+                                                     const int* cand, double* Yc, int* cmap,
+                                                     int* nc) {
+  const int b = blockIdx.x, tid = threadIdx.x;
+  __shared__ int ids[TPARTS * PNB];
+  __shared__ int tot;
+  const int* cb = cand + (long long)b * (TPARTS * (PNB + 1));
+  if (tid == 0) {
+    int t = 0;
+    if (active[b] && bsv[b] > 0)
+      for (int q = 0; q < TPARTS; ++q)
+        for (int i = 0; i < cb[q]; ++i) ids[t++] = cb[TPARTS + q * PNB + i];
+    tot = t;
+    nc[b] = t;
+  }
+  __syncthreads();
+  const double* Y = Yg + b * sY;
+  double* Yo = Yc + (long long)b * (TPARTS * PNB) * HSK;
+  for (int t = tid; t < tot; t += blockDim.x) cmap[(long long)b * (TPARTS * PNB) + t] = ids[t];
+  for (int e = tid; e < tot * HSK; e += blockDim.x) {
+    const int t = e / HSK, r = e % HSK;
+    Yo[(long long)t * HSK + r] = Y[(long long)(J + ids[t]) * ldy + r];
+  }
+}
+
+static int sketch_select_tournament(const double* Y, int ldy, long long sY, const int* mv,
+                                    const int* active, const int* bsv, int J, int n, int count,
+                                    int* swaps, cudaStream_t st) {
+  const int parts = (n + 16 * 512 - 1) / (16 * 512);
+  if (parts > TPARTS) {
+    set_error("sketch_select: %d live columns exceed the tournament's range (%d)", n,
+              TPARTS * 16 * 512);
+    return VF_EARG;
+  }
+  const int width = (((n + parts - 1) / parts) + 15) & ~15;
+  int* cand = nullptr;
+  double* Yc = nullptr;
+  const size_t ni = (size_t)count * (TPARTS * (PNB + 1) + TPARTS * PNB + 1);
+  if (cudaMallocAsync((void**)&cand, ni * sizeof(int), st) != cudaSuccess ||
+      cudaMallocAsync((void**)&Yc, (size_t)count * TPARTS * PNB * HSK * sizeof(double), st) != cudaSuccess) {
+    if (cand) cudaFreeAsync(cand, st);
+    set_error("sketch_select (tournament): out of device memory");
+    return VF_ENOMEM;
+  }
+  cudaMemsetAsync(cand, 0, ni * sizeof(int), st);
+  int* cmap = cand + (size_t)count * TPARTS * (PNB + 1);
+  int* nc = cmap + (size_t)count * TPARTS * PNB;
+  const int* noperm = nullptr;
+  int ldperm = 0, rc = VF_OK;
+  const int cs = 16, cols_per = (width + cs - 1) / cs;  // <= 512
+  for (int q = 0; q < parts && rc == VF_OK; ++q) {
+    int coff = q * width, nlim = width, slot = q;
+    const int* nomap = nullptr;
+    void* args[] = {(void*)&Y, (void*)&ldy, (void*)&sY, (void*)&mv, (void*)&active, (void*)&bsv,
+                    (void*)&J, (void*)&cols_per, (void*)&swaps, (void*)&noperm, (void*)&ldperm,
+                    (void*)&coff, (void*)&nlim, (void*)&cand, (void*)&slot, (void*)&nomap};
+    rc = launch_cluster((const void*)k_select_hh<512, true>, count, cs, 0, st, args, 512);
+  }
+  if (rc == VF_OK) {
+    k_cand_gather<<<count, 128, 0, st>>>(Y, ldy, sY, active, bsv, J, cand, Yc, cmap, nc);
+    ++g_launches;
+    int ldc = HSK, one = TPARTS * PNB, coff = -J, nlim = TPARTS * PNB, slot = 0;
+    long long sYc = (long long)TPARTS * PNB * HSK;
+    int* nocand = nullptr;
+    const double* Ycc = Yc;
+    const int* ncc = nc;
+    const int* cmapc = cmap;
+    void* args[] = {(void*)&Ycc, (void*)&ldc, (void*)&sYc, (void*)&ncc, (void*)&active, (void*)&bsv,
+                    (void*)&J, (void*)&one, (void*)&swaps, (void*)&noperm, (void*)&ldperm,
+                    (void*)&coff, (void*)&nlim, (void*)&nocand, (void*)&slot, (void*)&cmapc};
+    rc = launch_cluster((const void*)k_select_hh<128, true>, count, 1, 0, st, args, 128);
+  }
+  cudaFreeAsync(cand, st);
+  cudaFreeAsync(Yc, st);
+  return rc;
 }
 
 int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const int* active,
@@ -1307,11 +1411,23 @@ int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const i
                   int ldperm, cudaStream_t st) {
   const int n = maxm - J;
   if (n <= 0) return VF_OK;
+  if (n > 16 * 512) {  // wider than one cluster's thread-per-column slots
+    if (perm) {
+      set_error("sketch_select: pair mode is limited to %d live columns (got %d)", 16 * 512, n);
+      return VF_EARG;
+    }
+    return sketch_select_tournament(Y, ldy, sY, mv, active, bsv, J, n, count, swaps, st);
+  }
   int cs = pick_cs(n, 256, count);   // <= 256 sketch columns per CTA (measured ~0.5 % faster than 512)
   int cols_per = (n + cs - 1) / cs;
   size_t smem = ((size_t)(HSK + 1) * cols_per + (size_t)cols_per) * sizeof(double);
+  int zero = 0;
+  int* nocand = nullptr;
+  const int* nomap = nullptr;
+  // (k_select_hh's tournament parameters follow; k_select_cl takes the first eleven)
   void* args[] = {(void*)&Y, (void*)&ldy, (void*)&sY, (void*)&mv, (void*)&active, (void*)&bsv,
-                  (void*)&J, (void*)&cols_per, (void*)&swaps, (void*)&perm, (void*)&ldperm};
+                  (void*)&J, (void*)&cols_per, (void*)&swaps, (void*)&perm, (void*)&ldperm,
+                  (void*)&zero, (void*)&zero, (void*)&nocand, (void*)&zero, (void*)&nomap};
   // Householder selection while a thread owns one column; wider slices
   // (maxm > 16 x 512, 2048^2 and up) use the Gram-Schmidt kernel
   if (cols_per <= 512) {

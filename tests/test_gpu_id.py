@@ -145,6 +145,35 @@ def test_blocked_id_tall_panel_two_stage():
         assert np.abs(T).max() <= 10.0
 
 
+def test_blocked_id_wide_block_tournament_selection():
+    """More than 8192 live columns (16 CTAs x 512 thread-per-column slots; the
+    level-1 boxes of a 2048^2 grid have ~12272): the sketch selection runs as
+    a tournament over column ranges (csrc/panels.cu sketch_select_tournament).
+    Same contract: rank within a few of LAPACK's ID, reconstruction at the
+    tolerance, bounded interpolation coefficients.  The second matrix is
+    narrower (its last range is empty)."""
+    import oracle.hssd as O
+    from paper_1303_5466_b200.dense_core import interp_decomp_batched
+    rng = np.random.default_rng(13)
+    eps = 1e-10
+    mats = []
+    for p, m in [(420, 9001), (380, 8200)]:
+        src = rng.uniform(-1, 1, (m, 2)) * 0.5
+        th = np.linspace(0, 2 * np.pi, p, endpoint=False)
+        tgt = np.column_stack([1.5 * np.cos(th), 1.5 * np.sin(th)]) + rng.normal(0, 0.05, (p, 2))
+        r = np.hypot(*(tgt[:, None, :] - src[None, :, :]).transpose(2, 0, 1))
+        mats.append(np.log(r))
+    res = interp_decomp_batched(mats, eps, force_blocked=True)
+    for A, (perm, k, T) in zip(mats, res):
+        m = A.shape[1]
+        ref = O.column_id(A, eps)
+        err = np.linalg.norm(A[:, perm[k:]] - A[:, perm[:k]] @ T) / np.linalg.norm(A)
+        assert abs(k - ref.k) <= max(3, ref.k // 20), (k, ref.k)
+        assert err <= 50 * eps, err
+        assert len(set(perm.tolist())) == m
+        assert np.abs(T).max() <= 10.0
+
+
 def test_fixed_rank_is_least_squares():
     """vief_id_batched with kfix: no pivoting, rank = kfix, T = lstsq(A[:, :k],
     A[:, k:]) (the compressed path's interpolation).  Ragged batch: k off the

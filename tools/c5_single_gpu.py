@@ -21,12 +21,13 @@ ap.add_argument("--nrhs", type=int, default=1)
 ap.add_argument("--frac", type=float, default=0.92)
 ap.add_argument("--storage", default="hss1d")
 ap.add_argument("--trace", action="store_true")
+ap.add_argument("--kcut", type=int, default=64, help="0: the pivoted-ID path (k_cut = None)")
 a = ap.parse_args()
 torch.cuda.set_per_process_memory_fraction(a.frac)   # an over-commit raises here, not on the box
 spec = P.KernelSpec("laplace2d", b_field=P.make_field("centre_bump", scale=math.pi / 2),
                     c_field=P.make_field("one"))
 grid = P.Grid(a.n)
-opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=64)
+opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=a.kcut or None)
 
 
 def sync_t():
@@ -36,9 +37,9 @@ def sync_t():
 
 t0 = sync_t()
 tree = P.build_tree(grid, 64)
-layers = ensure_apriori_skeletons(spec, tree, opts)
 H = sd.Hss2dMatrix(spec, grid, tree, 1e-10, opts, P.CELL)
-H.apriori = layers
+if a.kcut:
+    H.apriori = ensure_apriori_skeletons(spec, tree, opts)
 t1 = sync_t()
 t2 = sync_t()
 mem_c = torch.cuda.max_memory_allocated()
@@ -65,7 +66,7 @@ t5 = sync_t()
 op = FFTOperator(spec, grid, P.CELL, "cuda")
 res = float(((F - op.matvec(X)).norm(dim=0) / F.norm(dim=0)).max())
 kinds = {L.lv: getattr(L, "hss_kind", "dense") for L in H.levels if L is not None}
-print(json.dumps({"n_side": a.n, "N": grid.n, "nrhs": a.nrhs, "storage": a.storage,
+print(json.dumps({"n_side": a.n, "N": grid.n, "nrhs": a.nrhs, "storage": a.storage, "k_cut": a.kcut or None,
                   "tree_s": t1 - t0, "compress_invert_convert_s": t3 - t2,
                   "solve_first_s": t4 - t3, "solve_s": t5 - t4, "true_residual_fft": res,
                   "factor_bytes": inv.nbytes(), "peak_alloc_compress": mem_c,
