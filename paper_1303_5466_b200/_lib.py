@@ -153,6 +153,16 @@ def release_memory():
     call("vief_release_pool")
 
 
+def release_memory_if_low(frac=0.35):
+    """release_memory() when less than `frac` of the device's memory is free
+    (as the driver sees it: both allocators' caches count as used)."""
+    free, total = torch.cuda.mem_get_info()
+    if free < frac * total:
+        release_memory()
+        return True
+    return False
+
+
 def launch_count():
     return int(load().vief_launch_count())
 

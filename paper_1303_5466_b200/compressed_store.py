@@ -81,8 +81,8 @@ def compact_level(H, L, eps=None, leaf_size=None, min_size=None, force_hss=False
     Fp = L.Finv[bidx, pr[:, :, None], pc[:, None, :]]     # F^-1(perm_c[r'], perm_r[c'])
     big = L.Finv.numel() * 8 > (1 << 30)
     L.Finv = L.C = L.W = None
-    if big:   # the HSS compression's workspace comes from the library's pool, not torch's cache
-        torch.cuda.empty_cache()
+    if big and torch.cuda.mem_get_info()[0] < 0.35 * torch.cuda.mem_get_info()[1]:
+        torch.cuda.empty_cache()   # the HSS compression's workspace comes from the library's pool
     kind = "lean"
     hF = hE = None
     k0 = int(k[0])

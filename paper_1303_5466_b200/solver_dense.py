@@ -1208,8 +1208,9 @@ def invert_dense_block(H, spill=None, free_source=False, storage="dense", compre
         for i, L in enumerate(levels):
             _lib.prof_prefix(f"L{L.lv:02d}.")
             if compress and getattr(L, "m", None) is None:
-                _lib.release_memory()   # cached blocks back to the driver: torch's
+                # cached blocks back to the driver when memory runs short: torch's
                 # allocator and the library's stream-ordered pool share the HBM
+                _lib.release_memory_if_low()
                 _compress_level(H, L, pad, H.opts.seed)
                 _mark(f"compress:{L.lv}")
             _invert_level(inv, L)
@@ -1225,7 +1226,7 @@ def invert_dense_block(H, spill=None, free_source=False, storage="dense", compre
             if storage in ("hss1d", "lean") and i > 0:   # the parent's F is assembled
                 from . import compressed_store
                 if compress:
-                    _lib.release_memory()
+                    _lib.release_memory_if_low()
                 compressed_store.compact_level(
                     H, levels[i - 1], min_size=None if storage == "hss1d" else float("inf"))
             if sp is not None and i > 0:   # the child level is no longer needed here

@@ -8,6 +8,9 @@ Prints times, resident bytes and the true residual (FFT operator).
 """
 import argparse, json, math, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# growing segments instead of fixed blocks: at ~160 of 178 GB the caching allocator's
+# fragmentation (tens of GB reserved but unusable) is what runs out first
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 import numpy as np
 import torch
 import paper_1303_5466_b200 as P
