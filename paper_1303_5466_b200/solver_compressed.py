@@ -148,6 +148,11 @@ def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti
     if tree is None:
         tree = build_tree(grid, opts.leaf_size)
     inv = CompressedInverse(spec, grid, tree, eps, opts, quad, ti_mode)
+    if opts.block_storage not in ("dense", "hss1d"):
+        raise ConfigError(f"unknown block_storage {opts.block_storage!r}")
+    if opts.low_memory:
+        return _compress_inverse_low_memory(inv, spec, grid, tree, eps, opts, quad, ti_mode,
+                                            support_mask)
     if opts.k_cut is None or opts.k_cut == np.inf:
         # compress_outer + invert_dense_block, levels pipelined over two streams
         H, inv.dense_delegate = factorize(spec, grid, tree, eps, opts, quad)
@@ -158,8 +163,6 @@ def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti
     # 548-552) when every box is a translate of it: uniform levels, no support
     # mask; otherwise every box is factored and uniform levels share a record
     share = ti_mode and support_mask is None and _levels_uniform(tree)
-    if opts.block_storage not in ("dense", "hss1d"):
-        raise ConfigError(f"unknown block_storage {opts.block_storage!r}")
     H, inv.factors = factorize(spec, grid, tree, eps, opts, quad, apriori=layers, ti=share)
     if ti_mode and not share:
         share_level_records(inv.factors)
@@ -169,6 +172,28 @@ def compress_inverse(spec, grid, tree=None, eps=1e-10, opts=None, quad=PLAIN, ti
         from . import compressed_store
         inv.hss_levels = compressed_store.compact(inv.factors)
     inv.dense_delegate = inv.factors
+    inv.dense_matvec_source = H
+    return inv
+
+
+def _compress_inverse_low_memory(inv, spec, grid, tree, eps, opts, quad, ti_mode, support_mask):
+    """SolverOptions(low_memory=True): level-by-level compression and inversion
+    with one level's sources resident at a time (invert_dense_block(compress=
+    True, free_source=True)), lean or 1-D HSS factor storage.  2048^2 at eps =
+    1e-10 fits one B200 this way (profiles/r02_c5_2048_single_gpu*.json)."""
+    from . import solver_dense as sd
+    if ti_mode:
+        raise ConfigError("low_memory does not combine with ti_mode (TI records are small already)")
+    H = sd.Hss2dMatrix(spec, grid, tree, eps, opts, quad)
+    dense_path = opts.k_cut is None or opts.k_cut == np.inf
+    if not dense_path:
+        H.apriori = ensure_apriori_skeletons(spec, tree, opts, support_mask)
+    storage = "hss1d" if (opts.block_storage == "hss1d" and not dense_path) else "lean"
+    factors = invert_dense_block(H, free_source=True, storage=storage, compress=True)
+    if not dense_path:
+        inv.factors = factors
+        inv.hss_levels = sum(getattr(L, "hss_kind", None) == "hss" for L in H.levels if L is not None)
+    inv.dense_delegate = factors
     inv.dense_matvec_source = H
     return inv
 

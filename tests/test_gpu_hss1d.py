@@ -295,3 +295,28 @@ def test_helmholtz_compressed_with_block_storage(mode):
     assert np.linalg.norm(xc - xd) <= 1e-8 * np.linalg.norm(xd)
     A = P.assemble_dense(spec, grid, P.PLAIN, np.arange(grid.n), np.arange(grid.n))
     assert np.linalg.norm(A @ xc - f) / np.linalg.norm(f) <= 1e-7
+
+
+@pytest.mark.parametrize("k_cut,storage", [(None, "dense"), (64, "dense"), (64, "hss1d")])
+def test_low_memory_option_same_solution(k_cut, storage):
+    """SolverOptions(low_memory=True) (level-by-level compression + inversion,
+    sources dropped, lean / 1-D HSS factors) through the public
+    compress_inverse: the default schedule's solution and a true residual
+    (FFT operator: H's blocks are gone) at the tolerance."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    from paper_1303_5466_b200.verify import FFTOperator
+    spec = P.KernelSpec("laplace2d", b_field=P.make_field("gaussian_bump"), c_field=P.make_field("one"))
+    grid = P.Grid(128)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=k_cut, block_storage=storage)
+    f = np.random.default_rng(12).standard_normal((grid.n, 2))
+    x0 = compress_inverse(spec, grid, eps=1e-10, opts=opts).apply(f)
+    low = compress_inverse(spec, grid, eps=1e-10, opts=opts.with_(low_memory=True))
+    x1 = low.apply(f)
+    assert np.linalg.norm(x1 - x0) <= 1e-8 * np.linalg.norm(x0)
+    assert low.nbytes() > 0
+    op = FFTOperator(spec, grid, P.PLAIN, "cuda")
+    X = torch.as_tensor(x1, device="cuda")
+    F = torch.as_tensor(f, device="cuda")
+    res = float(((F - op.matvec(X)).norm(dim=0) / F.norm(dim=0)).max())
+    assert res <= (1e-9 if k_cut is None else 1e-6), res
