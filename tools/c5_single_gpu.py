@@ -56,6 +56,27 @@ if a.trace:
               file=sys.stderr, flush=True)
         return r
     cs.compact_level = _traced
+    # synchronised wall time per phase (compression / inversion / storage conversion / cache release)
+    from paper_1303_5466_b200 import _lib as lib
+    phase = {}
+    def _timed(mod, name, key):
+        fn = getattr(mod, name)
+        def w(*aa, **kw):
+            torch.cuda.synchronize(); t = time.time()
+            r = fn(*aa, **kw)
+            torch.cuda.synchronize()
+            lv = next((x.lv for x in aa if hasattr(x, "lv")), -1)
+            phase.setdefault(lv, {}).setdefault(key, 0.0)
+            phase[lv][key] += time.time() - t
+            return r
+        setattr(mod, name, w)
+    _timed(sd, "_compress_level", "compress")
+    _timed(sd, "_invert_level", "invert")
+    _timed(cs, "compact_level", "convert")
+    _timed(lib, "release_memory_if_low", "release")
+    import atexit
+    atexit.register(lambda: print("phase seconds per level: " + json.dumps(
+        {k: {a: round(b, 3) for a, b in v.items()} for k, v in sorted(phase.items())}), file=sys.stderr))
 # each level is compressed just before it is inverted: one level's sources resident at a time
 inv = sd.invert_dense_block(H, free_source=True, storage=a.storage, compress=True)
 t3 = sync_t()
