@@ -88,6 +88,16 @@ class _Writer:
         if isinstance(v, (tuple, list)):
             return {"t": "tuple" if isinstance(v, tuple) else "list",
                     "v": [self.encode(x) for x in v]}
+        if isinstance(v, dict):
+            return {"t": "dict", "v": [[self.encode(k), self.encode(x)] for k, x in v.items()]}
+        # lean / 1-D HSS block storage of a level (compressed_store.py): L.hss = (hF, hE)
+        from .hss1d import Hss1dBatch, _HLevel
+        if isinstance(v, Hss1dBatch):
+            return {"t": "hss1d", "v": {k: self.encode(getattr(v, k))
+                                        for k in ("nb", "n", "tree", "depth", "lv", "dense")}}
+        if isinstance(v, _HLevel):
+            return {"t": "hlevel", "v": {k: self.encode(getattr(v, k))
+                                         for k in _HLevel.__slots__ if hasattr(v, k)}}
         raise TypeError(f"cannot persist a {type(v).__name__}")
 
 
@@ -173,7 +183,7 @@ def _problem_json(pb):
                     "c_field": _field_json(sp.c_field)},
            "quad": pb["quad"].order,
            "opts": dataclasses.asdict(pb["opts"])}
-    for k in ("eps", "n_side", "n_max", "ti_mode"):
+    for k in ("eps", "n_side", "n_max", "ti_mode", "apriori"):
         if k in pb:
             out[k] = pb[k]
     sl = pb.get("level_slices")
@@ -199,6 +209,8 @@ def _problem_from_json(d):
            "eps": float(d["eps"]), "n_side": int(d["n_side"]), "n_max": int(d["n_max"])}
     if "ti_mode" in d:
         out["ti_mode"] = bool(d["ti_mode"])
+    if d.get("apriori") is not None:
+        out["apriori"] = int(d["apriori"])
     sl = d.get("level_slices")
     out["level_slices"] = None if sl is None else {int(lv): tuple(int(x) for x in v)
                                                    for lv, v in sl}
@@ -298,6 +310,20 @@ def read_state(path, device):
                 base = torch.from_numpy(base)
             typed = base.view(_TD[e["dtype"]])
             return torch.as_strided(typed, e["shape"], e["stride"], e["o"])
+        if t == "dict":
+            return {decode(k): decode(x) for k, x in e["v"]}
+        if t == "hss1d":
+            from .hss1d import Hss1dBatch
+            d = {k: decode(x) for k, x in e["v"].items()}
+            h = Hss1dBatch(d["nb"], d["n"], d["tree"], device)
+            h.lv, h.dense = d["lv"], d["dense"]
+            return h
+        if t == "hlevel":
+            from .hss1d import _HLevel
+            h = _HLevel()
+            for k, x in e["v"].items():
+                setattr(h, k, decode(x))
+            return h
         raise ValueError(f"bad entry type {t!r}")
 
     levels = [None if st is None else {k: decode(v) for k, v in st.items()}
@@ -319,7 +345,8 @@ def _problem_of(H):
 
 def save(obj, path):
     """Write an `Hss2dMatrix`, a `DenseBlockInverse` or a `CompressedInverse`
-    (k_cut=None) to `path`.  The factors stay where they are (HBM)."""
+    (either path; dense, lean or 1-D HSS block storage) to `path`.  The factors
+    stay where they are (HBM)."""
     from .solver_compressed import CompressedInverse
     from .solver_dense import DenseBlockInverse, Hss2dMatrix
     if isinstance(obj, CompressedInverse):
@@ -333,14 +360,12 @@ def save(obj, path):
         kind, H = "Hss2dMatrix", obj
     else:
         raise TypeError(f"cannot save a {type(obj).__name__}")
-    if any(getattr(L, "hss", None) is not None for L in H.levels if L is not None):
-        raise NotImplementedError("saving 1-D HSS / lean block storage (block_storage='hss1d') "
-                                  "is not supported: save the dense factors and convert after "
-                                  "load (compressed_store.compact)")
     torch.cuda.synchronize(H.device)
     problem = _problem_of(H)
     if kind == "CompressedInverse":
         problem["ti_mode"] = obj.ti_mode
+    if getattr(H, "apriori", None):   # the finite-k_cut path: the a-priori band width
+        problem["apriori"] = int(H.apriori)
     write_state(path, problem, kind,
                 [None if L is None else _level_state(L) for L in H.levels])
 
@@ -361,6 +386,7 @@ def load(path, device=None):
     with torch.cuda.device(device):
         H = Hss2dMatrix(pb["spec"], grid, tree, pb["eps"], pb["opts"], pb["quad"],
                         level_slices=pb["level_slices"])
+    H.apriori = pb.get("apriori")
     for L, st in zip(H.levels, levels):
         if (L is None) != (st is None):
             raise ValueError(f"{path}: level layout does not match the rebuilt tree")
@@ -375,4 +401,9 @@ def load(path, device=None):
     ci = CompressedInverse(pb["spec"], grid, tree, pb["eps"], pb["opts"], pb["quad"],
                            pb.get("ti_mode", False))
     ci.dense_delegate, ci.dense_matvec_source = inv, H
+    if H.apriori:   # the compressed path's factor views (factor_of, record_count) read these
+        from .solver_compressed import ensure_apriori_skeletons
+        ensure_apriori_skeletons(pb["spec"], tree, pb["opts"])   # (a support mask is not recorded)
+        ci.factors = inv
+        ci.hss_levels = sum(getattr(L, "hss_kind", None) == "hss" for L in H.levels if L is not None)
     return ci

@@ -139,3 +139,48 @@ def test_dense_inverse_and_matrix_save_load(tmp_path):
     for i in list(inv.E)[:10]:
         assert np.array_equal(inv.E[i], inv2.E[i])
     assert np.array_equal(inv.Finv[0], inv2.Finv[0])
+
+
+@pytest.mark.gpu
+def test_lean_factors_save_load_bitwise(tmp_path):
+    """The low-memory schedule's lean factor set (F^-1, E, T: what a 2048^2
+    factorization holds) written and read back: bitwise the same solves."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200 import solver_compressed as sc
+    spec = P.KernelSpec("laplace2d", b_field=P.make_field("gaussian_bump"), c_field=P.make_field("one"))
+    grid = P.Grid(128)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=None, low_memory=True)
+    inv = sc.compress_inverse(spec, grid, eps=1e-10, opts=opts)
+    H = inv.dense_matvec_source
+    assert all(getattr(L, "hss_kind", None) == "lean" for L in H.levels if L is not None and L.lv > 0)
+    f = np.random.default_rng(5).standard_normal((grid.n, 3))
+    x0 = inv.apply(f)
+    path = str(tmp_path / "lean.vief")
+    inv.save(path)
+    inv2 = sc.CompressedInverse.load(path)
+    assert np.array_equal(inv2.apply(f), x0)
+    assert np.array_equal(inv2.apply(f[:, 0]), inv.apply(f[:, 0]))
+    assert inv2.nbytes() == inv.nbytes()
+
+
+@pytest.mark.gpu
+def test_hss1d_factors_save_load_bitwise(tmp_path):
+    """Finite k_cut with the large blocks in 1-D HSS form: the forms (tree
+    intervals, generators per level, ranks) and the a-priori band width
+    survive the file; solves and factor views are bitwise the same."""
+    import paper_1303_5466_b200 as P
+    from paper_1303_5466_b200 import compressed_store, solver_compressed as sc
+    spec = P.KernelSpec("laplace2d", b_field=P.make_field("gaussian_bump"), c_field=P.make_field("one"))
+    grid = P.Grid(64)
+    opts = P.SolverOptions(eps=1e-10, leaf_size=64, k_cut=32)
+    inv = sc.compress_inverse(spec, grid, eps=1e-10, opts=opts)
+    assert compressed_store.compact(inv.factors, force_hss=True) >= 2
+    f = np.random.default_rng(6).standard_normal((grid.n, 2))
+    x0 = inv.apply(f)
+    path = str(tmp_path / "hss.vief")
+    inv.save(path)
+    inv2 = sc.CompressedInverse.load(path)
+    assert np.array_equal(inv2.apply(f), x0)
+    assert inv2.nbytes() == inv.nbytes()
+    b0, b1 = inv.factor_of(inv.tree.nodes[1]), inv2.factor_of(inv2.tree.nodes[1])
+    assert b0.k == b1.k and np.array_equal(b0.E, b1.E) and np.array_equal(b0.Finv, b1.Finv)
