@@ -229,6 +229,27 @@ def test_factor_singular_box_reports_where():
     assert ei.value.where.startswith("box ")
 
 
+def test_factor_singular_leaf_in_a_deep_tree_reports_the_leaf():
+    """Every leaf F singular in a three-level tree: the exception names a leaf
+    box (the finest level is tested first), on the sequential and the
+    pipelined factorization alike."""
+    P, sd = _api()
+    zero = P.make_field("tanh_box", d=1.0, eps_edge=5.0, scale=0.0)
+    spec = P.KernelSpec("laplace2d", a_field=zero, b_field=zero, c_field=zero)
+    grid = P.Grid(16)
+    tree = P.build_tree(grid, 64)
+    leaf_level = max(b.level for b in tree.nodes)
+    assert leaf_level >= 2
+    H = sd.compress_outer(spec, grid, tree, 1e-10, P.SolverOptions(leaf_size=64))
+    with pytest.raises(P.SingularFactorError) as ei:
+        sd.invert_dense_block(H)
+    assert ei.value.where.startswith("box ") and ei.value.where.endswith(f"level {leaf_level}")
+    from paper_1303_5466_b200.solver_compressed import compress_inverse
+    with pytest.raises(P.SingularFactorError) as ei:
+        compress_inverse(spec, grid, eps=1e-10, opts=P.SolverOptions(leaf_size=64, k_cut=None))
+    assert ei.value.where.endswith(f"level {leaf_level}")
+
+
 # ---- parity with the reference's solutions (golden vectors) ----------------
 
 def _case_spec(name):
