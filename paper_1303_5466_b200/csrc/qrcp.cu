@@ -547,9 +547,7 @@ struct HState {
   double* G;      // count x HB x (HB*D): V_i^T V_cat
   int D;          // inner blocks per delayed trailing update
   double* Y;      // count x HS x maxm sketch
-  double* Om;     // count x HS x maxp: Omega H_1 ... H_i (sketch in original coordinates)
-  double* OV;     // count x HS x HB
-  double* OVT;    // count x HS x HB
+  double* OV;     // count x HS x HB: (Omega Q)(:, J:J+bs) of the current block (k_dg_coeff)
   int* any;       // 1 int: any active
   int ldtn;       // row stride of tn (= maxm)
 };
@@ -580,12 +578,35 @@ __global__ void k_zero_rows(double* V, long long sV, int ldv, int r0, int r1, co
   }
 }
 
-// per-item copy of the shared Gaussian sketch matrix
-__global__ void k_bcast_omega(const double* Om, long long n, double* Omr, int count) {
-  const int b = blockIdx.y;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    Omr[b * n + i] = Om[i];
+// Sketch downdate without a running Omega Q (Duersch & Gu's sample update):
+// after the swap Y(:, J:J+bs) is the sketch of the panel's columns, and the
+// panel's QR gives Y(:, J:J+bs) = W R11 with W = (Omega Q)(:, J:J+bs), so
+// W = Y(:, J:J+bs) R11^-1 by forward substitution (thread = sketch row) and
+// the trailing sketch loses W R12 (one GEMM).  A zero pivot (exactly
+// dependent column) contributes nothing.
+__global__ void __launch_bounds__(64) k_dg_coeff(const double* Y, long long sY, const double* Rt,
+                                                 const int* active, const int* bsv, int J,
+                                                 double* OV) {
+  const int b = blockIdx.x, r = threadIdx.x;
+  if (!active[b] || bsv[b] <= 0) return;
+  const int bs = bsv[b];
+  __shared__ double R[HB][HB + 1];
+  const double* Rb = Rt + (long long)b * HB * HB;
+  for (int i = r; i < HB * HB; i += 64) R[i % HB][i / HB] = Rb[i];
+  __syncthreads();
+  if (r >= HS) return;
+  const double* Yb = Y + b * sY + (long long)J * HS + r;
+  double* Wo = OV + (long long)b * HS * HB + r;
+  double x[HB];
+#pragma unroll
+  for (int c = 0; c < HB; ++c) {
+    double s = c < bs ? Yb[(long long)c * HS] : 0.0;
+#pragma unroll
+    for (int k = 0; k < c; ++k) s = fma(-x[k], R[k][c], s);
+    const double d = R[c][c];
+    x[c] = (c < bs && d != 0.0) ? s / d : 0.0;
+    Wo[c * HS] = x[c];
+  }
 }
 
 // apply the block's net column permutation (from the select kernel: column
@@ -1057,20 +1078,17 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     S.X = buf.get<double>((size_t)HB * maxm * count);
     S.G = buf.get<double>((size_t)HB * HB * D * count);
     S.Y = buf.get<double>((size_t)HS * maxm * count);
-    S.Om = buf.get<double>((size_t)HS * maxp * count);
     S.OV = buf.get<double>((size_t)HS * HB * count);
-    S.OVT = buf.get<double>((size_t)HS * HB * count);
     S.any = buf.get<int>(2);   // [0]: some group unfinished, [1]: some item needs exact norms
     S.ldtn = maxm;
     double* Om = buf.get<double>((size_t)HS * maxp);
-    if (!S.Y || !S.Vw || !S.Up || !S.X || !S.Om || !Om || !S.any) {
+    if (!S.Y || !S.Vw || !S.Up || !S.X || !S.OV || !Om || !S.any) {
       set_error("id: out of device memory (blocked)");
       return VF_ENOMEM;
     }
     prof_push(st, "id.init+sketch");
     const long long sY = (long long)HS * maxm, sV = (long long)ldv * HB * D;
     const long long sU = (long long)ldU * maxm, sX = (long long)HB * maxm;
-    const long long sOm = (long long)HS * maxp;
     k_iota<<<dim3(cdiv(maxm, 128), count), 128, 0, st>>>(d->perm, maxm, d->m, count);
     k_colnorms<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(d->A, d->sA, d->lda, d->p, d->m,
                                                            nullptr, 0, S.tn, maxm);
@@ -1081,9 +1099,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
     if (fixed) k_fixed_init<<<cdiv(count, 128), 128, 0, st>>>(S, d->kfix, count);
     k_gaussian<<<cdiv((long long)HS * maxp, 256), 256, 0, st>>>(Om, (long long)HS * maxp,
                                                                d->seed ^ 0x5eedULL);
-    k_bcast_omega<<<dim3(std::min<unsigned>(cdiv((long long)HS * maxp, 256), 64u), count), 256, 0, st>>>(
-        Om, sOm, S.Om, count);
-    g_launches += 6;
+    g_launches += 5;
     VF_LAUNCH_CHECK("id init");
     int rc;
     if (!fixed) {  // Y = Omega A
@@ -1215,29 +1231,13 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         // Y_trail -= Omega_i(:, J:J+bs) R(J block, trail)
         if (!fixed) {
         prof_push(st, "id.sketch_downdate");
-        vief_gemm_desc o1{};  // OV = Omega(:, J:p) V_i
-        o1.A = S.Om + (long long)J * HS; o1.strideA = sOm; o1.lda = HS;
-        o1.B = Vi + J; o1.strideB = sV; o1.ldb = ldv;
-        o1.C = S.OV; o1.strideC = (long long)HS * HB; o1.ldc = HS;
-        o1.M = HS; o1.N = HB; o1.K = maxp - J; o1.Mb = S.sact; o1.Nb = S.bs; o1.Kb = S.pact;
-        o1.alpha = 1.0; o1.beta = 0.0; o1.batch = count;
-        if ((rc = vief_dgemm_batched(&o1, st))) return rc;
-        vief_gemm_desc o2{};  // OVT = OV T_i
-        o2.A = S.OV; o2.strideA = (long long)HS * HB; o2.lda = HS;
-        o2.B = S.Tt; o2.strideB = (long long)HB * HB; o2.ldb = HB;
-        o2.C = S.OVT; o2.strideC = (long long)HS * HB; o2.ldc = HS;
-        o2.M = HS; o2.N = HB; o2.K = HB; o2.Mb = S.sact; o2.Nb = S.bs; o2.Kb = S.bs;
-        o2.alpha = 1.0; o2.beta = 0.0; o2.batch = count;
-        if ((rc = vief_dgemm_batched(&o2, st))) return rc;
-        vief_gemm_desc o3{};  // Omega(:, J:p) -= OVT V_i^T
-        o3.A = S.OVT; o3.strideA = (long long)HS * HB; o3.lda = HS;
-        o3.B = Vi + J; o3.strideB = sV; o3.ldb = ldv; o3.transB = 1;
-        o3.C = S.Om + (long long)J * HS; o3.strideC = sOm; o3.ldc = HS;
-        o3.M = HS; o3.N = maxp - J; o3.K = HB; o3.Mb = S.sact; o3.Nb = S.pact; o3.Kb = S.bs;
-        o3.alpha = -1.0; o3.beta = 1.0; o3.batch = count;
-        if ((rc = vief_dgemm_batched(&o3, st))) return rc;
+        // Omega Q's columns of this block from the sketch itself: Y(:, J:J+bs) =
+        // (Omega Q)(:, J:J+bs) R11  (the swapped-in sketch columns are the sketch
+        // of the panel's columns), so no running Omega Q is kept
+        k_dg_coeff<<<count, 64, 0, st>>>(S.Y, sY, S.Rt, S.active, S.bs, J, S.OV);
+        ++g_launches;
         vief_gemm_desc y{};
-        y.A = S.Om + (long long)J * HS; y.strideA = sOm; y.lda = HS;
+        y.A = S.OV; y.strideA = (long long)HS * HB; y.lda = HS;
         y.B = Rm + (long long)T0 * ldR + J; y.strideB = sR; y.ldb = ldR;
         y.C = S.Y + (long long)T0 * HS; y.strideC = sY; y.ldc = HS;
         y.M = HS; y.N = maxm; y.K = HB; y.Mb = S.sact; y.Nb = S.nrem; y.Kb = S.bs;
