@@ -11,9 +11,13 @@
 //
 //   k_lu_panel_cl    partial-pivoting LU of the Gauss-Jordan panel (rows
 //                    c0..n-1, <= 32 columns) -> pivots, |U_jj| min/max, A11^{-1}
-//   k_qr_panel_cl    Householder QR of the ID block panel (p x bs); explicit
-//                    Q = (I - V T V^T) [I;0] in WY form (one more barrier)
-//   k_select_cl      QRCP on the sketch Y(:, J:m) choosing bs pivots -> swap list
+//   k_lu_panel_rr    the same with the panel rows in registers
+//   k_qr_panel_rr    Householder QR of the ID block panel (p x bs) in registers
+//                    -> V (unit lower trapezoidal), T, R  (taller than one
+//                    cluster holds: tallpanel.cu)
+//   k_select_hh      Householder QRCP on the sketch Y(:, J:m) choosing bs
+//                    pivots -> swap list (wider than one cluster's slots:
+//                    tournament over column ranges)
 #include <cooperative_groups.h>
 #include <cstdlib>
 #include <mutex>
@@ -168,195 +172,6 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(const double* A, long long s
 }
 
 // ---------------------------------------------------------------------------
-// Householder QR of P = A(:, J:J+bs), explicit Q, R.
-struct XQr {
-  double ss, alpha;
-  double S[PNB];
-  double rowj[PNB];
-};
-struct XGram {
-  double G[PNB * PNB];
-  double V1[PNB * PNB];
-};
-
-__global__ void __launch_bounds__(PT) k_qr_panel_cl(const double* A, long long sA, int lda,
-                                                    const int* pv, const int* active,
-                                                    const int* bsv, int J, int rows_per,
-                                                    double* Vw, long long sV, int ldv,
-                                                    double* Tt, double* Rt) {
-  cg::cluster_group cl = cg::this_cluster();
-  const int cs = cl.num_blocks(), cr = cl.block_rank();
-  const int b = blockIdx.x / cs;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (!active[b] || bsv[b] <= 0) return;  // uniform for the whole cluster
-  const int bs = bsv[b];
-  const int p = pv[b] - J;  // panel rows J..p-1
-  extern __shared__ double sm[];
-  __shared__ XQr xch[2];
-  // Gram exchange lives in dynamic shared memory after the panel slice
-  __shared__ double tau[PNB], Rl[PNB][PNB + 1], w[PNB], Tm[PNB][PNB + 1], Mm[PNB][PNB + 1];
-  __shared__ double red[32];
-  __shared__ double Sp[16][PNB];
-  const int r0 = cr * rows_per, r1 = min(p, r0 + rows_per), nr = max(r1 - r0, 0);
-  const int ldp = rows_per;
-  double* P = sm;
-  XGram& xg = *reinterpret_cast<XGram*>(sm + (long long)rows_per * PNB);
-  const double* Ab = A + b * sA + (long long)J * lda + J;
-  for (int idx = tid; idx < nr * bs; idx += PT) {
-    int i = idx % nr, c = idx / nr;
-    P[c * ldp + i] = Ab[(long long)c * lda + r0 + i];
-  }
-  for (int idx = tid; idx < PNB * PNB; idx += PT) Rl[idx % PNB][idx / PNB] = 0.0;
-  if (tid < PNB) tau[tid] = 0.0;
-  __syncthreads();
-  const int jmax = min(bs, p);
-  for (int j = 0; j < jmax; ++j) {
-    XQr& x = xch[j & 1];
-    const int oj = j / rows_per;
-    const double* cj = P + j * ldp;
-    const int i0 = max(j + 1 - r0, 0);
-    // partials: ss = sum x_r^2, S_l = sum x_r c_l(r), rows r > j
-    double ss = 0.0;
-    for (int i = i0 + tid; i < nr; i += PT) ss = fma(cj[i], cj[i], ss);
-    ss = block_sum(ss, red);
-    for (int l = j + 1 + warp; l < bs; l += NW) {
-      const double* c = P + l * ldp;
-      double s = 0.0;
-      for (int i = i0 + lane; i < nr; i += 32) s = fma(cj[i], c[i], s);
-      s = warp_sum(s);
-      if (lane == 0) x.S[l] = s;
-    }
-    if (tid == 0) {
-      x.ss = ss;
-      if (cr == oj) x.alpha = cj[j - r0];
-    }
-    if (cr == oj)
-      for (int l = j + 1 + tid; l < bs; l += PT) x.rowj[l] = P[l * ldp + (j - r0)];
-    csync(cl);
-    if (tid < 32) {
-      double v = tid < cs ? remote(cl, &x, tid)->ss : 0.0;
-      v = warp_sum(v);
-      if (tid == 0) red[0] = v;
-    }
-    __syncthreads();
-    const double tot = red[0];
-    XQr* xo = remote(cl, &x, oj);
-    const double alpha = xo->alpha;
-    double tj, beta, sc;
-    {
-      const double xn = sqrt(tot);
-      if (xn == 0.0) { tj = 0.0; beta = alpha; sc = 0.0; }
-      else {
-        beta = -copysign(hypot(alpha, xn), alpha);
-        tj = (beta - alpha) / beta;
-        sc = 1.0 / (alpha - beta);
-      }
-    }
-    // remote partials: one DSMEM load per thread (all in flight together),
-    // then a fixed-order sum over ranks from shared memory
-    for (int idx = tid; idx < cs * PNB; idx += PT) {
-      const int q = idx / PNB, l = idx % PNB;
-      if (l > j && l < bs) Sp[q][l] = remote(cl, &x, q)->S[l];
-    }
-    __syncthreads();
-    for (int l = j + 1 + tid; l < bs; l += PT) {
-      double s = 0.0;
-      for (int q = 0; q < cs; ++q) s += Sp[q][l];
-      const double rjl = xo->rowj[l];
-      const double wl = tj * fma(sc, s, rjl);
-      w[l] = wl;
-      Rl[j][l] = rjl - wl;
-    }
-    if (tid == 0) { tau[j] = tj; Rl[j][j] = beta; }
-    __syncthreads();
-    // v = [1; x*sc]; columns l > j: c_l -= w_l v
-    double* v = P + j * ldp;
-    if (tj != 0.0) {
-      for (int i = i0 + tid; i < nr; i += PT) v[i] *= sc;
-      __syncthreads();
-      for (int l = j + 1 + warp; l < bs; l += NW) {
-        double* c = P + l * ldp;
-        const double wl = w[l];
-        for (int i = i0 + lane; i < nr; i += 32) c[i] = fma(-wl, v[i], c[i]);
-        if (cr == oj && lane == 0) c[j - r0] -= wl;
-      }
-    } else {
-      // H_j = I: v below the diagonal is unused (tau = 0); zero it for the Gram
-      for (int i = i0 + tid; i < nr; i += PT) v[i] = 0.0;
-    }
-    __syncthreads();
-  }
-  // V (unit lower trapezoid: zero above the diagonal, 1 on it) in place of P
-  for (int idx = tid; idx < nr * bs; idx += PT) {
-    int i = idx % nr, c = idx / nr;
-    const int r = r0 + i;
-    if (r < c) P[c * ldp + i] = 0.0;
-    else if (r == c) P[c * ldp + i] = 1.0;
-  }
-  __syncthreads();
-  // Gram G = V^T V (partial over local rows), V1 = V[0:bs, 0:bs] from CTA 0
-  for (int idx = warp; idx < bs * bs; idx += NW) {
-    const int a = idx % bs, c = idx / bs;
-    if (a > c) continue;
-    const double* va = P + a * ldp;
-    const double* vc = P + c * ldp;
-    double s = 0.0;
-    for (int i = lane; i < nr; i += 32) s = fma(va[i], vc[i], s);
-    s = warp_sum(s);
-    if (lane == 0) xg.G[c * PNB + a] = s;
-  }
-  if (cr == 0)
-    for (int idx = tid; idx < bs * bs; idx += PT) {
-      const int r = idx % bs, c = idx / bs;
-      xg.V1[c * PNB + r] = r < nr ? P[c * ldp + r] : 0.0;
-    }
-  csync(cl);
-  // T (upper, dlarft forward columnwise) from tau and G; M = T V1^T
-  for (int idx = tid; idx < bs * bs; idx += PT) {
-    const int a = idx % bs, c = idx / bs;
-    double s = 0.0;
-    if (a <= c)
-      for (int q = 0; q < cs; ++q) s += remote(cl, &xg, q)->G[c * PNB + a];
-    Mm[a][c] = s;  // temporarily G(a,c) for a <= c
-  }
-  XGram* x0 = remote(cl, &xg, 0);
-  __syncthreads();
-  if (tid < PNB) {
-    // column-by-column: T(0:j, j) = -tau_j T(0:j,0:j) G(0:j, j); thread i owns row i
-    const int i = tid;
-    for (int c = 0; c < bs; ++c) {
-      double t = 0.0;
-      if (i < c) {
-        double s = 0.0;
-        for (int k = i; k < c; ++k) s = fma(Tm[i][k], Mm[k][c], s);
-        t = -tau[c] * s;
-      } else if (i == c) {
-        t = tau[c];
-      }
-      Tm[i][c] = (i <= c) ? t : 0.0;
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  csync(cl);  // remote reads done before any CTA may exit / reuse
-  // V (already unit lower trapezoidal in P) at absolute rows J.., T and R from CTA 0
-  double* Vo = Vw + b * sV + J;
-  for (int idx = tid; idx < nr * bs; idx += PT) {
-    const int i = idx % nr, c = idx / nr;
-    Vo[(long long)c * ldv + r0 + i] = P[c * ldp + i];
-  }
-  if (cr == 0) {
-    double* Rr = Rt + (long long)b * PNB * PNB;
-    double* To = Tt + (long long)b * PNB * PNB;
-    for (int idx = tid; idx < PNB * PNB; idx += PT) {
-      int i = idx % PNB, c = idx / PNB;
-      Rr[c * PNB + i] = Rl[i][c];
-      To[c * PNB + i] = Tm[i][c];
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // QRCP on the sketch Y(:, J:m) (HSK rows) selecting bs pivots; columns split
 // over the cluster.  Output: swap list (dst = J+i, src position).
 // Net permutation of the column window (warp 0 of cluster rank 0): the
@@ -414,197 +229,6 @@ struct XSel {
   int cand_i;
   double y[HSK];
 };
-
-template <bool WIDE>  // WIDE: more than PT columns per CTA (two per thread per pass)
-__global__ void __launch_bounds__(PT) k_select_cl(const double* Yg, int ldy, long long sY,
-                                                  const int* mv, const int* active, const int* bsv,
-                                                  int J, int cols_per, int* swaps,
-                                                  const int* perm, int ldperm) {
-  cg::cluster_group cl = cg::this_cluster();
-  const int cs = cl.num_blocks(), cr = cl.block_rank();
-  const int b = blockIdx.x / cs;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (!active[b] || bsv[b] <= 0) {
-    if (cr == 0 && tid == 0) swaps[(long long)b * SWL] = 0;
-    return;
-  }
-  const int bs = bsv[b];
-  const int n = mv[b] - J;
-  extern __shared__ double sm[];
-  __shared__ XSel xch[2];
-  __shared__ double Qb[PNB][HSK + 1];  // odd row stride: lane-per-row dot products are conflict free
-  __shared__ double yv[HSK], dv[PNB];
-  __shared__ double redv[NW];
-  __shared__ int redi[NW];
-  __shared__ int sel[PNB];
-  const int c0 = cr * cols_per, c1 = min(n, c0 + cols_per), nc = max(c1 - c0, 0);
-  constexpr int LDY = HSK + 1;  // odd column stride: thread-per-column reads are conflict free
-  double* Ys = sm;              // LDY x cols_per
-  double* nrm = Ys + (long long)LDY * cols_per;
-  const double* Y = Yg + b * sY + (long long)(J + c0) * ldy;
-  for (int idx = tid; idx < nc * HSK; idx += PT) {
-    int r = idx % HSK, c = idx / HSK;
-    Ys[c * LDY + r] = Y[(long long)c * ldy + r];
-  }
-  __syncthreads();
-  // column norms^2 and this thread's best candidate (thread per column)
-  double bv = -1.0;
-  int bi = 0x7fffffff;
-  for (int c = tid; c < nc; c += PT) {
-    const double* yc = Ys + c * LDY;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int r = 0; r < HSK; r += 4) {
-      s0 = fma(yc[r], yc[r], s0); s1 = fma(yc[r + 1], yc[r + 1], s1);
-      s2 = fma(yc[r + 2], yc[r + 2], s2); s3 = fma(yc[r + 3], yc[r + 3], s3);
-    }
-    const double s = (s0 + s1) + (s2 + s3);
-    nrm[c] = s;
-    if (s > bv) { bv = s; bi = c0 + c; }
-  }
-  // per step: CTA argmax (1 barrier), cluster exchange (1 cluster barrier),
-  // warp 0 picks the winner and orthogonalises its sketch column against the
-  // chosen ones (no block barriers), then every thread downdates its columns'
-  // residual norms and keeps its next candidate (1 barrier)
-  const int* pm = perm ? perm + (long long)b * ldperm + J : nullptr;  // pair mode
-  for (int i = 0; i < bs; ++i) {
-    XSel& x = xch[i & 1];
-    if (pm && (i & 1)) {  // pivot 2s+1: the partner component of pivot 2s
-      const int want = pm[sel[i - 1]] ^ 1;
-      for (int c = tid; c < nc; c += PT)
-        if (nrm[c] >= 0.0 && pm[c0 + c] == want) { bv = 1e300; bi = c0 + c; }
-    }
-    double v = bv;
-    int iv = bi;
-    warp_argmax(v, iv);
-    if (lane == 0) { redv[warp] = v; redi[warp] = iv; }
-    __syncthreads();
-    if (warp == 0) {
-      double cv = lane < NW ? redv[lane] : -2.0;
-      int ci = lane < NW ? redi[lane] : 0x7fffffff;
-      warp_argmax(cv, ci);
-      if (lane == 0) { x.cand_v = cv; x.cand_i = ci; }
-      if (cv >= 0.0) {
-        x.y[lane] = Ys[(ci - c0) * LDY + lane];
-        if (lane + 32 < HSK) x.y[lane + 32] = Ys[(ci - c0) * LDY + lane + 32];
-      }
-    }
-    csync(cl);
-    if (warp == 0) {
-      double cv = -2.0;
-      int ci = 0x7fffffff;
-      if (lane < cs) { XSel* xr = remote(cl, &x, lane); cv = xr->cand_v; ci = xr->cand_i; }
-      warp_argmax(cv, ci);
-      if (ci < 0 || ci >= n) ci = min(i, n - 1);  // defensive (NaN data): stay in range
-      const XSel* xo = remote(cl, &x, ci / cols_per);
-      double y0 = xo->y[lane];
-      double y1 = lane + 32 < HSK ? xo->y[lane + 32] : 0.0;
-      if (lane == 0) {
-        sel[i] = ci;
-        if (ci >= c0 && ci < c1) nrm[ci - c0] = -1.0;
-      }
-      // classical Gram-Schmidt against Qb[0..i); a second pass only when the
-      // first removed more than half of the vector ("twice is enough")
-      double nn_prev = warp_sum(y0 * y0 + y1 * y1);
-      for (int pass = 0; pass < 2 && i > 0; ++pass) {
-        yv[lane] = y0;
-        if (lane + 32 < HSK) yv[lane + 32] = y1;
-        __syncwarp();
-        if (lane < i) {  // lane c: dv[c] = Qb[c] . y
-          double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-          for (int r = 0; r < HSK; r += 4) {
-            d0 = fma(Qb[lane][r], yv[r], d0); d1 = fma(Qb[lane][r + 1], yv[r + 1], d1);
-            d2 = fma(Qb[lane][r + 2], yv[r + 2], d2); d3 = fma(Qb[lane][r + 3], yv[r + 3], d3);
-          }
-          dv[lane] = (d0 + d1) + (d2 + d3);
-        }
-        __syncwarp();
-        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-        int c = 0;
-        for (; c + 1 < i; c += 2) {
-          a0 = fma(dv[c], Qb[c][lane], a0); a1 = fma(dv[c + 1], Qb[c + 1][lane], a1);
-          if (lane + 32 < HSK) {
-            b0 = fma(dv[c], Qb[c][lane + 32], b0); b1 = fma(dv[c + 1], Qb[c + 1][lane + 32], b1);
-          }
-        }
-        if (c < i) {
-          a0 = fma(dv[c], Qb[c][lane], a0);
-          if (lane + 32 < HSK) b0 = fma(dv[c], Qb[c][lane + 32], b0);
-        }
-        y0 -= a0 + a1;
-        y1 -= b0 + b1;
-        __syncwarp();
-        const double nn_now = warp_sum(y0 * y0 + y1 * y1);
-        if (nn_now > 0.25 * nn_prev) break;  // uniform across the warp
-        nn_prev = nn_now;
-      }
-      const double nn = warp_sum(y0 * y0 + y1 * y1);
-      const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-      Qb[i][lane] = y0 * inv;
-      if (lane + 32 < HSK) Qb[i][lane + 32] = y1 * inv;
-    }
-    __syncthreads();
-    // downdate every live column's residual norm and pick the next candidate
-    bv = -1.0;
-    bi = 0x7fffffff;
-    if constexpr (WIDE) {
-      double qv[HSK];
-#pragma unroll
-      for (int r = 0; r < HSK; ++r) qv[r] = Qb[i][r];
-      // two columns per pass (c, c + PT): 8 independent FMA chains
-      for (int c = tid; c < nc; c += 2 * PT) {
-        const int c2 = c + PT;
-        const bool h2 = c2 < nc;
-        const double cur1 = nrm[c], cur2 = h2 ? nrm[c2] : -1.0;
-        const double* y1 = Ys + c * LDY;
-        const double* y2 = Ys + (h2 ? c2 : c) * LDY;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
-#pragma unroll
-        for (int r = 0; r < HSK; r += 4) {
-          a0 = fma(qv[r], y1[r], a0); a1 = fma(qv[r + 1], y1[r + 1], a1);
-          a2 = fma(qv[r + 2], y1[r + 2], a2); a3 = fma(qv[r + 3], y1[r + 3], a3);
-          e0 = fma(qv[r], y2[r], e0); e1 = fma(qv[r + 1], y2[r + 1], e1);
-          e2 = fma(qv[r + 2], y2[r + 2], e2); e3 = fma(qv[r + 3], y2[r + 3], e3);
-        }
-        if (cur1 >= 0.0) {
-          const double d = (a0 + a1) + (a2 + a3);
-          const double nv = fmax(cur1 - d * d, 0.0);
-          nrm[c] = nv;
-          if (nv > bv) { bv = nv; bi = c0 + c; }
-        }
-        if (cur2 >= 0.0) {
-          const double d = (e0 + e1) + (e2 + e3);
-          const double nv = fmax(cur2 - d * d, 0.0);
-          nrm[c2] = nv;
-          if (nv > bv) { bv = nv; bi = c0 + c2; }
-        }
-      }
-    } else {
-      const double* q = Qb[i];
-      for (int c = tid; c < nc; c += PT) {
-        const double cur = nrm[c];
-        if (cur < 0.0) continue;
-        const double* yc = Ys + c * LDY;
-        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-        for (int r = 0; r < HSK; r += 4) {
-          d0 = fma(q[r], yc[r], d0); d1 = fma(q[r + 1], yc[r + 1], d1);
-          d2 = fma(q[r + 2], yc[r + 2], d2); d3 = fma(q[r + 3], yc[r + 3], d3);
-        }
-        const double d = (d0 + d1) + (d2 + d3);
-        const double nv = fmax(cur - d * d, 0.0);
-        nrm[c] = nv;
-        if (nv > bv) { bv = nv; bi = c0 + c; }
-      }
-    }
-  }
-  csync(cl);
-  if (cr != 0 || warp != 0) return;
-  __shared__ int mid[NM], mpos[NM];
-  emit_swaps(sel, bs, J, b, swaps, lane, mid, mpos);
-}
-
 
 // ---------------------------------------------------------------------------
 // Register-resident panels.  Each thread keeps RPT whole panel rows (32
@@ -1147,22 +771,11 @@ int qr_panel(const double* A, long long sA, int lda, const int* pv, const int* a
   }
   // taller than one cluster holds (16 CTAs x 256 threads x 3 rows): two-stage panel
   return qr_panel_tall(A, sA, lda, pv, active, bsv, J, maxp, count, Vw, sV, ldv, Tt, Rt, st);
-  int cs = pick_cs(rows, 640, count);
-  int rows_per = (rows + cs - 1) / cs;
-  if (rows_per < PNB) rows_per = PNB;
-  rows_per = (rows_per + 1) & ~1;
-  size_t smem = (size_t)rows_per * PNB * sizeof(double) + sizeof(XGram);
-  void* args[] = {(void*)&A, (void*)&sA, (void*)&lda, (void*)&pv, (void*)&active, (void*)&bsv,
-                  (void*)&J, (void*)&rows_per, (void*)&Vw, (void*)&sV, (void*)&ldv, (void*)&Tt,
-                  (void*)&Rt};
-  return launch_cluster((const void*)k_qr_panel_cl, count, cs, smem, st, args);
 }
 
-// Same selection as k_select_cl (QRCP of the sketch), with the chosen
-// columns eliminated by Householder reflections applied to every live sketch
-// column instead of Gram-Schmidt of each new pivot against the chosen basis:
-// warp 0's serial part per step shrinks to one reflector of length HSK - i
-// (the others no longer wait for an i-term orthogonalisation); each thread
+// QRCP of the sketch, the chosen columns eliminated by Householder
+// reflections applied to every live sketch column: warp 0's serial part per
+// step is one reflector of length HSK - i; each thread
 // then reflects its own column (thread per column: cols_per <= PT) and
 // downdates its residual norm by the new R(i, c)^2.
 //
@@ -1420,24 +1033,17 @@ int sketch_select(const double* Y, int ldy, long long sY, const int* mv, const i
   }
   int cs = pick_cs(n, 256, count);   // <= 256 sketch columns per CTA (measured ~0.5 % faster than 512)
   int cols_per = (n + cs - 1) / cs;
-  size_t smem = ((size_t)(HSK + 1) * cols_per + (size_t)cols_per) * sizeof(double);
   int zero = 0;
   int* nocand = nullptr;
   const int* nomap = nullptr;
-  // (k_select_hh's tournament parameters follow; k_select_cl takes the first eleven)
   void* args[] = {(void*)&Y, (void*)&ldy, (void*)&sY, (void*)&mv, (void*)&active, (void*)&bsv,
                   (void*)&J, (void*)&cols_per, (void*)&swaps, (void*)&perm, (void*)&ldperm,
                   (void*)&zero, (void*)&zero, (void*)&nocand, (void*)&zero, (void*)&nomap};
-  // Householder selection while a thread owns one column; wider slices
-  // (maxm > 16 x 512, 2048^2 and up) use the Gram-Schmidt kernel
-  if (cols_per <= 512) {
-    const int nt = cols_per <= 128 ? 128 : (cols_per <= 256 ? 256 : 512);
-    const void* fn = nt == 128 ? (const void*)k_select_hh<128>
-                   : nt == 256 ? (const void*)k_select_hh<256> : (const void*)k_select_hh<512>;
-    return launch_cluster(fn, count, cs, 0, st, args, nt);
-  }
-  const void* fn = cols_per > PT ? (const void*)k_select_cl<true> : (const void*)k_select_cl<false>;
-  return launch_cluster(fn, count, cs, smem, st, args);
+  // a thread owns one sketch column: cols_per <= 512 for n <= 16 x 512
+  const int nt = cols_per <= 128 ? 128 : (cols_per <= 256 ? 256 : 512);
+  const void* fn = nt == 128 ? (const void*)k_select_hh<128>
+                 : nt == 256 ? (const void*)k_select_hh<256> : (const void*)k_select_hh<512>;
+  return launch_cluster(fn, count, cs, 0, st, args, nt);
 }
 
 }  // namespace vf

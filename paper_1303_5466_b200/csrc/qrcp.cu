@@ -564,6 +564,10 @@ __global__ void k_block_setup(int J, int Jf, const int* pv, const int* mv, int c
   S.pact[b] = act ? max(pv[b] - J, 0) : 0;
   S.pf[b] = act ? max(pv[b] - Jf, 0) : 0;
   S.sact[b] = act ? HS : 0;
+  // this block's flags (read by k_need_exact / k_rank_check / the host after the block)
+  S.certany[b] = 0;
+  S.flagany[b] = 0;
+  if (b == 0) { S.any[0] = 0; S.any[1] = 0; }
 }
 
 // rows [r0, r1) of the HB columns of a pending-reflector block are zero
@@ -1259,9 +1263,7 @@ extern "C" int vief_id_batched(const vief_id_desc* d, void* stream_) {
         ++g_launches;
         continue;
       }
-      prof_push(st, "id.norms+rank");
-      VF_CUDA(cudaMemsetAsync(S.any, 0, 2 * sizeof(int), st));
-      VF_CUDA(cudaMemsetAsync(S.certany, 0, sizeof(int) * 2 * count, st));
+      prof_push(st, "id.norms+rank");   // (flags zeroed by k_block_setup)
       k_norm_downdate<<<dim3(cdiv(maxm, 8), count), 256, 0, st>>>(
           d->p, d->m, S.active, S.bs, J, Rm, sR, ldR, S.tn, S.tn0, S.flag, maxm, S.cut,
           S.certany, S.flagany);
