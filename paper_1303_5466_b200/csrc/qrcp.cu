@@ -920,6 +920,11 @@ struct Buf {
     void* p = nullptr;
     if (cudaMallocAsync(&p, n * sizeof(T) + 16, st) != cudaSuccess) return nullptr;
     ptrs.push_back(p);
+    // pool memory comes back with whatever its last user left (another call's
+    // data, possibly NaN bit patterns): parts of the work buffers are only ever
+    // multiplied by zeros (reflector columns >= bs, rows of inactive items), and
+    // 0 x NaN would leak into R.  The buffers are small next to A.
+    cudaMemsetAsync(p, 0, n * sizeof(T) + 16, st);
     return static_cast<T*>(p);
   }
   ~Buf() { for (void* p : ptrs) cudaFreeAsync(p, st); }

@@ -397,6 +397,9 @@ class ShardedInverse:
             Hh.id_split = (1, cp, lambda perm, T: self._send_col(perm, T, helper, owner, tag),
                            None)
             st = torch.cuda.Stream(self.dev)
+            # the top object's virtual level (skeleton lists, padded copies) was built by
+            # kernels on the caller's stream: the ID stream starts after them
+            st.wait_stream(torch.cuda.current_stream(self.dev))
             with torch.cuda.stream(st):
                 sd.compress_levels(Hh)
             st.synchronize()

@@ -172,10 +172,21 @@ def test_sharded_processes_match_reference(world):
     procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
+    import queue
+    import time
     res = {}
-    for _ in range(world):
-        r, xa, xr, ntop = q.get(timeout=600)
-        res[r] = (xa, xr, ntop)
+    deadline = time.time() + 600
+    while len(res) < world:   # a rank that died must fail the test now, not after its peers' timeouts
+        try:
+            r, xa, xr, ntop = q.get(timeout=2)
+            res[r] = (xa, xr, ntop)
+        except queue.Empty:
+            dead = [i for i, p in enumerate(procs) if p.exitcode not in (None, 0)]
+            if dead or time.time() > deadline:
+                for p in procs:
+                    if p.is_alive():
+                        p.terminate()
+                pytest.fail(f"ranks {dead} exited with an error" if dead else "timed out")
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
